@@ -1,0 +1,189 @@
+// ============================================================================
+// TEST INFRASTRUCTURE ONLY.  A thin extern "C" shim over the UNMODIFIED
+// reference library, compiled in place from /root/reference/proj by
+// oracle/Makefile into oracle/_ref/libref.so (git-ignored).  Nothing here
+// restates an algorithm: each entry point forwards to the reference call named
+// beside it.  Used (a) here, to generate tests/golden/ fixtures and to pin the
+// restatement in oracle/oracle.cpp, and (b) by bench.py --impl reference and
+// the cpu_baseline leg, to time the reference's own CPU path.
+// ============================================================================
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "spatial/dbscan.hpp"
+#include "spatial/generate.hpp"
+#include "spatial/io.hpp"
+#include "spatial/traversal.hpp"
+
+using namespace spatial;
+
+namespace {
+
+template <int Dim>
+std::vector<Point<Dim>> as_points(const float *v, int64_t n) {
+  std::vector<Point<Dim>> p((size_t)n);
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < Dim; ++k) p[(size_t)i][k] = v[i * Dim + k];
+  return p;
+}
+
+template <int Dim>
+std::vector<Aabb<Dim>> as_boxes(const float *v, int64_t n, bool is_points) {
+  std::vector<Aabb<Dim>> b((size_t)n);
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < Dim; ++k) {
+      b[(size_t)i].min_corner[k] = is_points ? v[i * Dim + k] : v[i * 2 * Dim + k];
+      b[(size_t)i].max_corner[k] = is_points ? v[i * Dim + k] : v[i * 2 * Dim + Dim + k];
+    }
+  return b;
+}
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+template <int Dim>
+int build_t(const float *v, int64_t n, int is_points, int width, int32_t *il, int32_t *ir, float *ib, int32_t *lo,
+            int32_t *lr, float *lb) {
+  auto boxes = as_boxes<Dim>(v, n, is_points != 0);
+  Bvh<Dim> bvh;
+  try {
+    bvh = Bvh<Dim>::build(std::span<const Aabb<Dim>>(boxes), width == 32 ? CodeWidth::k32 : CodeWidth::k64);
+  } catch (const std::exception &) {
+    return 1;
+  }
+  for (size_t i = 0; i < bvh.internals.size(); ++i) {
+    il[i] = bvh.internals[i].left_child.value;
+    ir[i] = bvh.internals[i].rope.value;
+    for (int k = 0; k < Dim; ++k) {
+      ib[i * 2 * Dim + k] = bvh.internals[i].volume.min_corner[k];
+      ib[i * 2 * Dim + Dim + k] = bvh.internals[i].volume.max_corner[k];
+    }
+  }
+  for (size_t p = 0; p < bvh.leaves.size(); ++p) {
+    lo[p] = bvh.leaves[p].object_index;
+    lr[p] = bvh.leaves[p].rope.value;
+    for (int k = 0; k < Dim; ++k) {
+      lb[p * 2 * Dim + k] = bvh.leaves[p].volume.min_corner[k];
+      lb[p * 2 * Dim + Dim + k] = bvh.leaves[p].volume.max_corner[k];
+    }
+  }
+  return bvh.validate().ok ? 0 : 2;
+}
+
+template <int Dim>
+int dbscan_t(const float *v, int64_t n, float eps, int32_t min_pts, int algo, int32_t *labels, uint8_t *core,
+             int64_t *stats, double *phase_ms) {
+  auto pts = as_points<Dim>(v, n);
+  DbscanOutput out;
+  try {
+    std::span<const Point<Dim>> s(pts);
+    if (algo == 0) out = fdbscan(s, DbscanParams{eps, min_pts});
+    else if (algo == 1) out = friends_of_friends(s, eps);
+    else if (algo == 2) out = fdbscan_densebox(s, DbscanParams{eps, min_pts});
+    else if (algo == 3) out = dbscan_reference(s, DbscanParams{eps, min_pts});
+    else out = adjacency_graph_dbscan(s, eps);
+  } catch (const std::exception &) {
+    return 1;
+  }
+  if (labels) std::memcpy(labels, out.labels.data(), out.labels.size() * 4);
+  if (core) std::memcpy(core, out.core_flags.data(), out.core_flags.size());
+  if (stats) {
+    stats[0] = out.stats.distance_checks;
+    stats[1] = out.stats.num_dense_cells;
+    stats[2] = out.stats.num_dense_points;
+  }
+  if (phase_ms) {
+    phase_ms[0] = out.timings.build_ms;
+    phase_ms[1] = out.timings.core_ms;
+    phase_ms[2] = out.timings.merge_ms;
+    phase_ms[3] = out.timings.finalize_ms;
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+// generate() (src/generate.cpp:96-100)
+int ref_generate_uniform(int64_t n, int dim, double extent, uint64_t seed, float *out) {
+  auto d = generate(UniformSpec{n, dim, extent, seed});
+  std::memcpy(out, d.values.data(), d.values.size() * sizeof(float));
+  return 0;
+}
+
+int ref_generate_gaussian(int64_t n, int dim, int32_t k, double sigma, double extent, uint64_t seed, float *out) {
+  auto d = generate(GaussianClustersSpec{n, dim, k, sigma, extent, seed});
+  std::memcpy(out, d.values.data(), d.values.size() * sizeof(float));
+  return 0;
+}
+
+// Bvh<D>::build (bvh.hpp:243-261) node arrays; returns 2 if validate() fails.
+int ref_bvh_build(const float *v, int64_t n, int dim, int is_points, int width, int32_t *il, int32_t *ir, float *ib,
+                  int32_t *lo, int32_t *lr, float *lb) {
+  return dim == 2 ? build_t<2>(v, n, is_points, width, il, ir, ib, lo, lr, lb)
+                  : build_t<3>(v, n, is_points, width, il, ir, ib, lo, lr, lb);
+}
+
+// algo: 0 fdbscan, 1 friends_of_friends, 2 fdbscan_densebox, 3 dbscan_reference,
+// 4 adjacency_graph_dbscan (dbscan.hpp:188-504)
+int ref_dbscan(const float *v, int64_t n, int dim, float eps, int32_t min_pts, int algo, int32_t *labels,
+               uint8_t *core, int64_t *stats, double *phase_ms) {
+  return dim == 2 ? dbscan_t<2>(v, n, eps, min_pts, algo, labels, core, stats, phase_ms)
+                  : dbscan_t<3>(v, n, eps, min_pts, algo, labels, core, stats, phase_ms);
+}
+
+// Bvh::build + sort_queries + range_query(count) over sphere queries centred on
+// `centres` (traversal.hpp:67-87, 209-218).  ms[0..2] = build, sort, query.
+int ref_range_count(const float *pts, int64_t n, const float *centres, int64_t nq, float radius, int32_t cap,
+                    int32_t *counts, double *ms) {
+  auto p = as_points<3>(pts, n);
+  auto q = as_points<3>(centres, nq);
+  std::vector<Aabb<3>> boxes((size_t)n);
+  for (int64_t i = 0; i < n; ++i) boxes[(size_t)i] = point_box(p[(size_t)i]);
+  double t0 = now_ms();
+  auto bvh = Bvh<3>::build(std::span<const Aabb<3>>(boxes));
+  double t1 = now_ms();
+  std::vector<RangePredicate<3>> preds((size_t)nq);
+  for (int64_t i = 0; i < nq; ++i) preds[(size_t)i].geometry = Sphere<3>{q[(size_t)i], radius};
+  auto order = sort_queries<3, RangePredicate<3>>(preds);
+  std::vector<RangePredicate<3>> sorted((size_t)nq);
+  for (int64_t i = 0; i < nq; ++i) sorted[(size_t)i] = preds[(size_t)order[(size_t)i]];
+  double t2 = now_ms();
+  std::memset(counts, 0, (size_t)nq * 4);
+  range_query(bvh, std::span<const RangePredicate<3>>(sorted), [&](std::int32_t qq, std::int32_t) {
+    int32_t &c = counts[order[(size_t)qq]];
+    ++c;
+    return (cap > 0 && c >= cap) ? CallbackControl::kTerminateQuery : CallbackControl::kContinue;
+  });
+  double t3 = now_ms();
+  if (ms) { ms[0] = t1 - t0; ms[1] = t2 - t1; ms[2] = t3 - t2; }
+  return 0;
+}
+
+// Bvh::build + nearest_query (traversal.hpp:93-156); idx is nq*k (ascending).
+int ref_knn(const float *pts, int64_t n, const float *origins, int64_t nq, int32_t k, int32_t *idx, double *ms) {
+  auto p = as_points<3>(pts, n);
+  auto o = as_points<3>(origins, nq);
+  std::vector<Aabb<3>> boxes((size_t)n);
+  for (int64_t i = 0; i < n; ++i) boxes[(size_t)i] = point_box(p[(size_t)i]);
+  double t0 = now_ms();
+  auto bvh = Bvh<3>::build(std::span<const Aabb<3>>(boxes));
+  double t1 = now_ms();
+  std::vector<NearestPredicate<3>> preds((size_t)nq);
+  for (int64_t i = 0; i < nq; ++i) preds[(size_t)i] = {o[(size_t)i], k};
+  std::vector<int32_t> fill((size_t)nq, 0);
+  for (int64_t i = 0; i < nq * k; ++i) idx[i] = -1;
+  nearest_query(bvh, std::span<const NearestPredicate<3>>(preds), [&](std::int32_t q, std::int32_t obj) {
+    idx[(size_t)q * k + (size_t)fill[(size_t)q]++] = obj;
+  });
+  double t2 = now_ms();
+  if (ms) { ms[0] = t1 - t0; ms[1] = t2 - t1; }
+  return 0;
+}
+
+}  // extern "C"

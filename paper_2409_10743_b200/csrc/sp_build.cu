@@ -1,0 +1,513 @@
+// Hierarchy construction on sm_100a: scene bounds (K1), Morton codes (K2), a
+// stable onesweep LSD radix sort (K3) and a single bottom-up Apetrei pass that
+// emits the reference's Karras-numbered nodes, exact union boxes and ropes in
+// one sweep (K4).  Reference: Bvh<D>::build, bvh.hpp:100-261; morton.hpp:17-121.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <climits>
+
+#include "sp_common.cuh"
+#include "sp_internal.hpp"
+
+namespace spb {
+
+thread_local int64_t *g_launch_counter = nullptr;
+
+// ---------------------------------------------------------------------------
+// K1: scene box + finiteness (bvh.hpp:247-254, geometry.hpp:58-69, 98-114)
+// ---------------------------------------------------------------------------
+__global__ void k_bounds_init(int32_t *ord6, int *bad) {
+  int t = threadIdx.x;
+  if (t < 3) ord6[t] = INT_MAX;
+  else if (t < 6) ord6[t] = INT_MIN;
+  if (t == 0) *bad = 0;
+}
+
+template <bool POINTS>
+__global__ void __launch_bounds__(256) k_bounds(const float *__restrict__ obj, int64_t n, int dim,
+                                                int32_t *__restrict__ ord6, int *__restrict__ bad) {
+  int32_t mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {INT_MIN, INT_MIN, INT_MIN};
+  bool ok = true;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int sz = POINTS ? dim : 2 * dim;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float *o = obj + i * sz;
+    for (int k = 0; k < dim; ++k) {
+      float lo = o[k];
+      float hi = POINTS ? lo : o[dim + k];
+      ok = ok && isfinite(lo) && isfinite(hi);
+      mn[k] = min(mn[k], ord_of(lo));
+      mx[k] = max(mx[k], ord_of(hi));
+    }
+  }
+  for (int k = 0; k < 3; ++k) {
+    mn[k] = __reduce_min_sync(0xffffffffu, mn[k]);
+    mx[k] = __reduce_max_sync(0xffffffffu, mx[k]);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    for (int k = 0; k < dim; ++k) {
+      atomicMin(&ord6[k], mn[k]);
+      atomicMax(&ord6[3 + k], mx[k]);
+    }
+  }
+  if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) *bad = 1;
+}
+
+// ord6 -> float scene[6]; axes beyond dim are 0 (2-D data lives at z = 0).
+__global__ void k_bounds_final(const int32_t *ord6, int dim, int64_t n, float *scene) {
+  int t = threadIdx.x;
+  if (t < 6) {
+    int k = t % 3;
+    scene[t] = (k < dim && n > 0) ? float_of_ord(ord6[t]) : 0.f;
+  }
+}
+
+void scene_bounds(Ctx &c, const float *objects, int64_t n, int dim, bool points, float *scene, int *bad) {
+  DevBuf<int32_t> ord(6, c.stream);
+  k_bounds_init<<<1, 32, 0, c.stream>>>(ord.get(), bad);
+  SPB_LAUNCHED();
+  if (n > 0) {
+    unsigned g = grid_for(n, 256, 148 * 8);
+    if (points) k_bounds<true><<<g, 256, 0, c.stream>>>(objects, n, dim, ord.get(), bad);
+    else k_bounds<false><<<g, 256, 0, c.stream>>>(objects, n, dim, ord.get(), bad);
+    SPB_LAUNCHED();
+  }
+  k_bounds_final<<<1, 32, 0, c.stream>>>(ord.get(), dim, n, scene);
+  SPB_LAUNCHED();
+}
+
+// ---------------------------------------------------------------------------
+// K2: Morton codes (morton.hpp:17-109; centroid geometry.hpp:130-137)
+// ---------------------------------------------------------------------------
+// Bit spreading: bit b of the input moves to bit b*stride.
+__device__ __forceinline__ uint64_t spread_by3(uint64_t v) {  // 21 bits -> 63
+  v &= 0x1fffffull;
+  v = (v | (v << 32)) & 0x001f00000000ffffull;
+  v = (v | (v << 16)) & 0x001f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+__device__ __forceinline__ uint64_t spread_by2(uint64_t v) {  // 32 bits -> 64
+  v &= 0xffffffffull;
+  v = (v | (v << 16)) & 0x0000ffff0000ffffull;
+  v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
+  v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+
+// Quantise one axis exactly as bin() does: floor((c - lo) / extent * 2^bits)
+// in double, clamped; a non-positive extent gives bin 0.  The division is the
+// IEEE-correct double division (a reciprocal multiply would not be bit-exact).
+__device__ __forceinline__ uint32_t axis_bin(float c, float lo, float hi, double scale, uint32_t top) {
+  double extent = __dsub_rn((double)hi, (double)lo);
+  if (!(extent > 0.0)) return 0u;
+  double t = __ddiv_rn(__dsub_rn((double)c, (double)lo), extent);
+  double f = floor(__dmul_rn(t, scale));
+  if (f <= 0.0) return 0u;
+  if (f >= (double)top) return top;
+  return (uint32_t)f;
+}
+
+__device__ __forceinline__ uint64_t encode_bins(uint32_t b0, uint32_t b1, uint32_t b2, int dim) {
+  if (dim == 3) return spread_by3(b0) | (spread_by3(b1) << 1) | (spread_by3(b2) << 2);
+  return spread_by2(b0) | (spread_by2(b1) << 1);
+}
+
+template <bool POINTS>
+__global__ void __launch_bounds__(256) k_morton(const float *__restrict__ obj, int64_t n, int dim, int width,
+                                                const float *__restrict__ scene, uint64_t *__restrict__ codes,
+                                                uint32_t *__restrict__ vals) {
+  const int bits = width / dim;
+  const uint32_t top = bits >= 32 ? 0xffffffffu : ((1u << bits) - 1u);
+  const double scale = (double)(1ull << bits);
+  float slo[3], shi[3];
+  for (int k = 0; k < 3; ++k) { slo[k] = scene[k]; shi[k] = scene[3 + k]; }
+  const int sz = POINTS ? dim : 2 * dim;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float *o = obj + i * sz;
+    uint32_t b[3] = {0u, 0u, 0u};
+    for (int k = 0; k < dim; ++k) {
+      float cen;
+      if (POINTS) cen = o[k];
+      else cen = __double2float_rn(__dmul_rn(__dadd_rn((double)o[k], (double)o[dim + k]), 0.5));
+      b[k] = axis_bin(cen, slo[k], shi[k], scale, top);
+    }
+    codes[i] = encode_bins(b[0], b[1], b[2], dim);
+    if (vals) vals[i] = (uint32_t)i;
+  }
+}
+
+void morton_codes(Ctx &c, const float *objects, int64_t n, int dim, bool points, int width, const float *scene,
+                  uint64_t *codes, uint32_t *vals) {
+  if (n <= 0) return;
+  unsigned g = grid_for(n, 256, 148 * 16);
+  if (points) k_morton<true><<<g, 256, 0, c.stream>>>(objects, n, dim, width, scene, codes, vals);
+  else k_morton<false><<<g, 256, 0, c.stream>>>(objects, n, dim, width, scene, codes, vals);
+  SPB_LAUNCHED();
+}
+
+// ---------------------------------------------------------------------------
+// K3: stable onesweep LSD radix sort of (u64 key, u32 value), 8-bit digits.
+// One upfront histogram pass for all digit positions, then one kernel per
+// digit: each CTA ranks a 4096-key tile (warp match_any ranking keeps the
+// original order within equal digits), obtains its global digit offsets by
+// decoupled look-back over the preceding tiles, stages the tile in shared
+// memory in digit order and writes it out coalesced.  Stability of every pass
+// makes the final order equal std::stable_sort's (morton.hpp:113-121).
+// ---------------------------------------------------------------------------
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_ITEMS = 16;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096
+constexpr int RS_BINS = 256;
+constexpr int RS_WH = RS_BINS + 1;  // + one slot for out-of-range items
+constexpr size_t RS_SMEM = (size_t)RS_TILE * 8 + (size_t)RS_TILE * 4 + (size_t)RS_WARPS * RS_WH * 4;
+
+__global__ void __launch_bounds__(256) k_rs_hist(const uint64_t *__restrict__ keys, int64_t n, int npass,
+                                                 uint32_t *__restrict__ ghist) {
+  __shared__ uint32_t h[8 * RS_BINS];
+  for (int i = threadIdx.x; i < npass * RS_BINS; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint64_t k = keys[i];
+    for (int p = 0; p < npass; ++p) atomicAdd(&h[p * RS_BINS + ((k >> (8 * p)) & 0xff)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < npass * RS_BINS; i += blockDim.x)
+    if (h[i]) atomicAdd(&ghist[i], h[i]);
+}
+
+// Exclusive scan of each pass's 256 counts (one CTA per pass).
+__global__ void k_rs_scan(uint32_t *ghist) {
+  __shared__ uint32_t wsum[RS_WARPS];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  uint32_t *h = ghist + blockIdx.x * RS_BINS;
+  uint32_t v = h[t], x = v;
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  uint32_t off = 0;
+  for (int w = 0; w < warp; ++w) off += wsum[w];
+  h[t] = off + x - v;
+}
+
+__device__ __forceinline__ void st_volatile_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(RS_THREADS) k_rs_onesweep(const uint64_t *__restrict__ kin,
+                                                            const uint32_t *__restrict__ vin,
+                                                            uint64_t *__restrict__ kout, uint32_t *__restrict__ vout,
+                                                            int64_t n, int shift, const uint32_t *__restrict__ binbase,
+                                                            unsigned long long *lookback, uint32_t *tile_ctr,
+                                                            uint32_t tag) {
+  extern __shared__ __align__(16) unsigned char rs_smem[];
+  uint64_t *skeys = reinterpret_cast<uint64_t *>(rs_smem);
+  uint32_t *svals = reinterpret_cast<uint32_t *>(skeys + RS_TILE);
+  uint32_t *whist = svals + RS_TILE;
+  __shared__ uint32_t s_dstart[RS_BINS];
+  __shared__ uint32_t s_gbase[RS_BINS];
+  __shared__ uint32_t s_wsum[RS_WARPS];
+  __shared__ uint32_t s_tile;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < RS_WARPS * RS_WH; i += RS_THREADS) whist[i] = 0;
+  if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t base = (int64_t)tile * RS_TILE;
+
+  uint64_t key[RS_ITEMS];
+  uint32_t val[RS_ITEMS];
+  uint32_t dig[RS_ITEMS];
+  uint32_t rk[RS_ITEMS];
+  const int64_t wbase = base + (int64_t)warp * (RS_ITEMS * 32);
+#pragma unroll
+  for (int i = 0; i < RS_ITEMS; ++i) {
+    int64_t idx = wbase + i * 32 + lane;
+    if (idx < n) {
+      key[i] = kin[idx];
+      val[i] = vin ? vin[idx] : (uint32_t)idx;
+      dig[i] = (uint32_t)(key[i] >> shift) & 0xffu;
+    } else {
+      key[i] = 0;
+      val[i] = 0;
+      dig[i] = RS_BINS;
+    }
+  }
+  // Warp-local stable ranks: items are visited in original order (item i of
+  // lane l is element i*32 + l of the warp's slice).
+  uint32_t *wh = whist + warp * RS_WH;
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int i = 0; i < RS_ITEMS; ++i) {
+    uint32_t peers = __match_any_sync(0xffffffffu, dig[i]);
+    uint32_t cnt = __popc(peers);
+    uint32_t below = __popc(peers & lt);
+    int leader = __ffs(peers) - 1;
+    uint32_t b = wh[dig[i]];
+    __syncwarp();
+    if (lane == leader) wh[dig[i]] = b + cnt;
+    __syncwarp();
+    rk[i] = b + below;
+  }
+  __syncthreads();
+
+  // Thread t owns digit t: exclusive prefix over warps, then look-back.
+  uint32_t tot = 0;
+#pragma unroll
+  for (int w = 0; w < RS_WARPS; ++w) {
+    uint32_t cw = whist[w * RS_WH + tid];
+    whist[w * RS_WH + tid] = tot;
+    tot += cw;
+  }
+  const unsigned long long agg_tag = (unsigned long long)tag << 32;
+  const unsigned long long inc_tag = (unsigned long long)(tag + 1) << 32;
+  unsigned long long *mine = lookback + (size_t)tile * RS_BINS + tid;
+  uint32_t excl = 0;
+  if (tile == 0) {
+    st_volatile_u64(mine, inc_tag | tot);
+  } else {
+    st_volatile_u64(mine, agg_tag | tot);
+    int64_t j = (int64_t)tile - 1;
+    while (true) {
+      unsigned long long v = ld_volatile_u64(lookback + (size_t)j * RS_BINS + tid);
+      unsigned long long st = v & 0xffffffff00000000ull;
+      if (st == inc_tag) {
+        excl += (uint32_t)v;
+        break;
+      }
+      if (st == agg_tag) {
+        excl += (uint32_t)v;
+        --j;
+      }
+    }
+    st_volatile_u64(mine, inc_tag | (excl + tot));
+  }
+  s_gbase[tid] = binbase[tid] + excl;
+
+  // Tile-local digit starts: exclusive scan of tot over the 256 digits.
+  uint32_t x = tot;
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) s_wsum[warp] = x;
+  __syncthreads();
+  uint32_t off = 0;
+  for (int w = 0; w < warp; ++w) off += s_wsum[w];
+  s_dstart[tid] = off + x - tot;
+  __syncthreads();
+
+#pragma unroll
+  for (int i = 0; i < RS_ITEMS; ++i) {
+    if (dig[i] < RS_BINS) {
+      uint32_t pos = s_dstart[dig[i]] + wh[dig[i]] + rk[i];
+      skeys[pos] = key[i];
+      svals[pos] = val[i];
+    }
+  }
+  __syncthreads();
+  const int valid = (int)((n - base) < (int64_t)RS_TILE ? (n - base) : (int64_t)RS_TILE);
+  for (int pos = tid; pos < valid; pos += RS_THREADS) {
+    uint64_t k = skeys[pos];
+    uint32_t d = (uint32_t)(k >> shift) & 0xffu;
+    uint32_t o = s_gbase[d] + (uint32_t)pos - s_dstart[d];
+    kout[o] = k;
+    vout[o] = svals[pos];
+  }
+}
+
+void radix_sort_pairs(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_alt, uint32_t **vals_alt, int64_t n,
+                      int key_bits, bool vals_iota) {
+  if (n <= 1) {
+    if (n == 1 && vals_iota) SPB_CUDA(cudaMemsetAsync(*vals, 0, sizeof(uint32_t), c.stream));
+    return;
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    SPB_CUDA(cudaFuncSetAttribute(k_rs_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RS_SMEM));
+    attr_set = true;
+  }
+  const int npass = std::max(1, (key_bits + 7) / 8);
+  const int64_t ntiles = (n + RS_TILE - 1) / RS_TILE;
+  DevBuf<uint32_t> hist((size_t)npass * RS_BINS + npass, c.stream);
+  DevBuf<unsigned long long> lookback((size_t)ntiles * RS_BINS, c.stream);
+  SPB_CUDA(cudaMemsetAsync(hist.get(), 0, hist.n * sizeof(uint32_t), c.stream));
+  SPB_CUDA(cudaMemsetAsync(lookback.get(), 0, lookback.n * sizeof(unsigned long long), c.stream));
+  k_rs_hist<<<grid_for(n, 256, 148 * 4), 256, 0, c.stream>>>(*keys, n, npass, hist.get());
+  SPB_LAUNCHED();
+  k_rs_scan<<<npass, RS_BINS, 0, c.stream>>>(hist.get());
+  SPB_LAUNCHED();
+  uint32_t *ctr = hist.get() + (size_t)npass * RS_BINS;
+  for (int p = 0; p < npass; ++p) {
+    k_rs_onesweep<<<(unsigned)ntiles, RS_THREADS, RS_SMEM, c.stream>>>(
+        *keys, (p == 0 && vals_iota) ? nullptr : *vals, *keys_alt, *vals_alt, n, 8 * p, hist.get() + (size_t)p * RS_BINS, lookback.get(), ctr + p,
+        (uint32_t)(2 * p + 1));
+    SPB_LAUNCHED();
+    std::swap(*keys, *keys_alt);
+    std::swap(*vals, *vals_alt);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: hierarchy in one bottom-up pass (bvh.hpp:100-223).
+// ---------------------------------------------------------------------------
+// Adjacent prefix lengths of the augmented keys (code, object id): delta[i]
+// compares sorted entries i and i+1 (bvh.hpp:106-115).
+__global__ void __launch_bounds__(256) k_delta(const uint64_t *__restrict__ sk, const uint32_t *__restrict__ sv,
+                                               int64_t n, int width, int32_t *__restrict__ delta) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n; i += stride) {
+    uint64_t a = sk[i], b = sk[i + 1];
+    int d;
+    if (a != b) d = __clzll((long long)(a ^ b)) - (64 - width);
+    else d = width + __clz((int)(sv[i] ^ sv[i + 1]));
+    delta[i] = d;
+  }
+}
+
+struct HierView {
+  int64_t n;
+  const int32_t *delta;
+  __device__ __forceinline__ int D(int64_t i) const { return (i < 0 || i >= n - 1) ? -1 : __ldg(delta + i); }
+  // A node covering [l, r] is its parent's left child iff it shares a longer
+  // prefix with the key after it than with the key before it.
+  __device__ __forceinline__ bool is_left(int64_t l, int64_t r) const {
+    return l == 0 || (r != n - 1 && D(r) > D(l - 1));
+  }
+  // The rope of any node whose key range ends at r: the right child that
+  // starts at r+1 (a leaf iff leaf r+1 is itself a right child), or the
+  // sentinel on the right-most path (bvh.hpp:176-222).
+  __device__ __forceinline__ int32_t rope(int64_t r) const {
+    if (r == n - 1) return kSentinel;
+    if (r + 1 == n - 1 || D(r + 1) < D(r)) return (int32_t)(n - 1 + r + 1);
+    return (int32_t)(r + 1);
+  }
+};
+
+// Thread p writes leaf p, then climbs: the first child to arrive at a parent
+// records its far bound in flags[split] and stops; the second knows the
+// parent's full range [l, r] and split, recovers its Karras index (r for a
+// left child, l for a right child, 0 for the root), joins the two child boxes
+// left-first and writes {box, left, rope}.
+template <bool POINTS>
+__global__ void __launch_bounds__(256) k_hierarchy(int64_t n, const int32_t *__restrict__ delta,
+                                                   const uint32_t *__restrict__ perm, const float *__restrict__ obj,
+                                                   int dim, float4 *nodes, int32_t *flags,
+                                                   int32_t *__restrict__ perm_out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  HierView H{n, delta};
+  const uint32_t oi = perm[p];
+  perm_out[p] = (int32_t)oi;
+  const int sz = POINTS ? dim : 2 * dim;
+  const float *o = obj + (int64_t)oi * sz;
+  float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f};
+  for (int k = 0; k < dim; ++k) {
+    lo[k] = o[k];
+    hi[k] = POINTS ? lo[k] : o[dim + k];
+  }
+  const int64_t leaf = n - 1 + p;
+  nodes[2 * leaf] = make_float4(lo[0], lo[1], lo[2], __int_as_float((int)oi));
+  nodes[2 * leaf + 1] = make_float4(hi[0], hi[1], hi[2], __int_as_float(H.rope(p)));
+  if (n == 1) return;
+
+  int64_t l = p, r = p;
+  while (true) {
+    const bool L = H.is_left(l, r);
+    const int64_t a = L ? r : l - 1;  // the parent's split position
+    __threadfence();
+    const int32_t other = atomicExch(&flags[a], (int32_t)(L ? l : r));
+    if (other < 0) return;  // first arrival
+    __threadfence();
+    if (L) r = other;
+    else l = other;
+    const int64_t left = (a == l) ? n - 1 + l : a;
+    const int64_t right = (a + 1 == r) ? n - 1 + r : a + 1;
+    const int64_t sib = L ? right : left;
+    const float4 slo = __ldcg(nodes + 2 * sib);
+    const float4 shi = __ldcg(nodes + 2 * sib + 1);
+    if (L) {  // this node is the left child
+      lo[0] = keep_min(lo[0], slo.x); lo[1] = keep_min(lo[1], slo.y); lo[2] = keep_min(lo[2], slo.z);
+      hi[0] = keep_max(hi[0], shi.x); hi[1] = keep_max(hi[1], shi.y); hi[2] = keep_max(hi[2], shi.z);
+    } else {
+      lo[0] = keep_min(slo.x, lo[0]); lo[1] = keep_min(slo.y, lo[1]); lo[2] = keep_min(slo.z, lo[2]);
+      hi[0] = keep_max(shi.x, hi[0]); hi[1] = keep_max(shi.y, hi[1]); hi[2] = keep_max(shi.z, hi[2]);
+    }
+    const bool root = (l == 0 && r == n - 1);
+    const int64_t k = root ? 0 : (H.is_left(l, r) ? r : l);
+    nodes[2 * k] = make_float4(lo[0], lo[1], lo[2], __int_as_float((int)left));
+    nodes[2 * k + 1] = make_float4(hi[0], hi[1], hi[2], __int_as_float(H.rope(r)));
+    if (root) return;
+  }
+}
+
+void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, int width, Tree &t) {
+  t.n = n;
+  t.dim = dim;
+  t.width = width;
+  t.points = points;
+  t.stream = c.stream;
+  SPB_CUDA(cudaMallocAsync(&t.scene, 6 * sizeof(float), c.stream));
+  DevBuf<int> bad(1, c.stream);
+  scene_bounds(c, objects, n, dim, points, t.scene, bad.get());
+  int h_bad = 0;
+  SPB_CUDA(cudaMemcpyAsync(&h_bad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  if (h_bad) throw InvalidArgument("bvh: non-finite object bounds");
+  if (n == 0) return;
+
+  const int64_t num_nodes = 2 * n - 1;
+  SPB_CUDA(cudaMallocAsync(&t.nodes, (size_t)num_nodes * 2 * sizeof(float4), c.stream));
+  SPB_CUDA(cudaMallocAsync(&t.perm, (size_t)n * sizeof(int32_t), c.stream));
+
+  DevBuf<uint64_t> k0(n, c.stream), k1(n, c.stream);
+  DevBuf<uint32_t> v0(n, c.stream), v1(n, c.stream);
+  morton_codes(c, objects, n, dim, points, width, t.scene, k0.get(), nullptr);
+  uint64_t *ka = k0.get(), *kb = k1.get();
+  uint32_t *va = v0.get(), *vb = v1.get();
+  radix_sort_pairs(c, &ka, &va, &kb, &vb, n, (width / dim) * dim, /*vals_iota=*/true);
+  DevBuf<int32_t> delta(n > 1 ? n - 1 : 1, c.stream), flags(n > 1 ? n - 1 : 1, c.stream);
+  if (n > 1) {
+    k_delta<<<grid_for(n, 256, 148 * 16), 256, 0, c.stream>>>(ka, va, n, width, delta.get());
+    SPB_LAUNCHED();
+    SPB_CUDA(cudaMemsetAsync(flags.get(), 0xff, (size_t)(n - 1) * sizeof(int32_t), c.stream));
+  }
+  unsigned g = (unsigned)((n + 255) / 256);
+  if (points) k_hierarchy<true><<<g, 256, 0, c.stream>>>(n, delta.get(), va, objects, dim, t.nodes, flags.get(), t.perm);
+  else k_hierarchy<false><<<g, 256, 0, c.stream>>>(n, delta.get(), va, objects, dim, t.nodes, flags.get(), t.perm);
+  SPB_LAUNCHED();
+}
+
+void sort_points(Ctx &c, const float *pts, int64_t n, int dim, int32_t *order) {
+  if (n <= 0) return;
+  DevBuf<float> scene(6, c.stream);
+  DevBuf<int> bad(1, c.stream);
+  scene_bounds(c, pts, n, dim, true, scene.get(), bad.get());
+  DevBuf<uint64_t> k0(n, c.stream), k1(n, c.stream);
+  DevBuf<uint32_t> v0(n, c.stream), v1(n, c.stream);
+  morton_codes(c, pts, n, dim, true, 64, scene.get(), k0.get(), nullptr);
+  uint64_t *ka = k0.get(), *kb = k1.get();
+  uint32_t *va = v0.get(), *vb = v1.get();
+  radix_sort_pairs(c, &ka, &va, &kb, &vb, n, (64 / dim) * dim, /*vals_iota=*/true);
+  SPB_CUDA(cudaMemcpyAsync(order, va, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.stream));
+}
+
+}  // namespace spb

@@ -1,0 +1,437 @@
+// The extern "C" boundary (include/sp_b200.h).  Translates host/device
+// buffers, runs the device pipelines on the context stream, and maps C++
+// exceptions to sp_status codes — nothing throws across the ABI.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/sp_b200.h"
+#include "sp_common.cuh"
+#include "sp_internal.hpp"
+#include "sp_query.hpp"
+
+struct sp_ctx {
+  spb::Ctx c;
+};
+
+struct sp_bvh {
+  spb::Tree t;
+  int device = 0;
+};
+
+namespace {
+
+using spb::DevBuf;
+
+// Input array: device pointer as-is, or a device copy of a host array.
+template <class T>
+struct In {
+  DevBuf<T> buf;
+  const T *p = nullptr;
+  In(spb::Ctx &c, const T *src, size_t count, int mem) {
+    if (!src || count == 0) return;
+    if (mem == SP_MEM_DEVICE) {
+      p = src;
+      return;
+    }
+    buf = DevBuf<T>(count, c.stream);
+    SPB_CUDA(cudaMemcpyAsync(buf.get(), src, count * sizeof(T), cudaMemcpyHostToDevice, c.stream));
+    p = buf.get();
+  }
+};
+
+// Output array: device pointer as-is, or a device scratch copied back by flush().
+template <class T>
+struct Out {
+  DevBuf<T> buf;
+  T *p = nullptr;
+  T *host = nullptr;
+  size_t count = 0;
+  Out(spb::Ctx &c, T *dst, size_t n, int mem) : count(n) {
+    if (!dst || n == 0) return;
+    if (mem == SP_MEM_DEVICE) {
+      p = dst;
+      return;
+    }
+    buf = DevBuf<T>(n, c.stream);
+    p = buf.get();
+    host = dst;
+  }
+  void flush(spb::Ctx &c) {
+    if (host) SPB_CUDA(cudaMemcpyAsync(host, buf.get(), count * sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+  }
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <class F>
+int guarded(sp_ctx *ctx, F &&f) {
+  if (!ctx) return SP_EINVAL;
+  DeviceGuard dg(ctx->c.device);
+  spb::g_launch_counter = &ctx->c.launches;
+  int rc = SP_OK;
+  try {
+    f(ctx->c);
+  } catch (const spb::InvalidArgument &e) {
+    ctx->c.last_error = e.what();
+    rc = SP_EINVAL;
+  } catch (const spb::CapacityError &e) {
+    ctx->c.last_error = e.what();
+    rc = SP_ECAPACITY;
+  } catch (const spb::CudaError &e) {
+    ctx->c.last_error = e.what();
+    rc = strstr(e.what(), "allocation") ? SP_ENOMEM : SP_ECUDA;
+  } catch (const std::bad_alloc &e) {
+    ctx->c.last_error = "host allocation failed";
+    rc = SP_ENOMEM;
+  } catch (const std::exception &e) {
+    ctx->c.last_error = e.what();
+    rc = SP_ECUDA;
+  }
+  spb::g_launch_counter = nullptr;
+  if (rc == SP_OK) ctx->c.last_error.clear();
+  return rc;
+}
+
+void check_dim(int dim) {
+  if (dim != 2 && dim != 3) throw spb::InvalidArgument("dimension must be 2 or 3");
+}
+
+void finish(spb::Ctx &c) { SPB_CUDA(cudaStreamSynchronize(c.stream)); }
+
+}  // namespace
+
+extern "C" {
+
+int sp_ctx_create(int device, void *stream, sp_ctx **out) {
+  if (!out) return SP_EINVAL;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return SP_ECUDA;
+  DeviceGuard dg(device);
+  sp_ctx *ctx = new (std::nothrow) sp_ctx;
+  if (!ctx) return SP_ENOMEM;
+  ctx->c.device = device;
+  if (stream) {
+    ctx->c.stream = (cudaStream_t)stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete ctx;
+      return SP_ECUDA;
+    }
+    ctx->c.owns_stream = true;
+  }
+  // Keep freed stream-ordered allocations reserved: a caching allocator.
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = ctx;
+  return SP_OK;
+}
+
+int sp_ctx_destroy(sp_ctx *ctx) {
+  if (!ctx) return SP_OK;
+  {
+    DeviceGuard dg(ctx->c.device);
+    cudaStreamSynchronize(ctx->c.stream);
+    if (ctx->c.owns_stream) cudaStreamDestroy(ctx->c.stream);
+  }
+  delete ctx;
+  return SP_OK;
+}
+
+int sp_ctx_set_stream(sp_ctx *ctx, void *stream) {
+  if (!ctx) return SP_EINVAL;
+  DeviceGuard dg(ctx->c.device);
+  cudaStreamSynchronize(ctx->c.stream);
+  if (ctx->c.owns_stream) cudaStreamDestroy(ctx->c.stream);
+  ctx->c.owns_stream = false;
+  if (stream) {
+    ctx->c.stream = (cudaStream_t)stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking) != cudaSuccess) return SP_ECUDA;
+    ctx->c.owns_stream = true;
+  }
+  return SP_OK;
+}
+
+int sp_ctx_synchronize(sp_ctx *ctx) {
+  return guarded(ctx, [&](spb::Ctx &c) { finish(c); });
+}
+
+const char *sp_last_error(const sp_ctx *ctx) { return ctx ? ctx->c.last_error.c_str() : "null context"; }
+
+int64_t sp_ctx_kernel_launches(const sp_ctx *ctx) { return ctx ? ctx->c.launches : 0; }
+
+int sp_bvh_build(sp_ctx *ctx, const float *objects, int64_t n, int dim, int is_points, int code_width, int mem,
+                 sp_bvh **out) {
+  if (out) *out = nullptr;
+  return guarded(ctx, [&](spb::Ctx &c) {
+    check_dim(dim);
+    if (code_width != 32 && code_width != 64) throw spb::InvalidArgument("code width must be 32 or 64");
+    if (n < 0 || n > (1LL << 30)) throw spb::InvalidArgument("object count out of range");
+    if (!out) throw spb::InvalidArgument("null output handle");
+    const size_t per = is_points ? dim : 2 * dim;
+    In<float> obj(c, objects, (size_t)n * per, mem);
+    sp_bvh *b = new sp_bvh;
+    b->device = c.device;
+    try {
+      spb::build_tree(c, obj.p, n, dim, is_points != 0, code_width, b->t);
+      finish(c);
+    } catch (...) {
+      delete b;
+      throw;
+    }
+    *out = b;
+  });
+}
+
+int sp_bvh_destroy(sp_bvh *bvh) {
+  if (!bvh) return SP_OK;
+  {
+    DeviceGuard dg(bvh->device);
+    cudaStreamSynchronize(bvh->t.stream);
+    bvh->t.free_all();
+    cudaStreamSynchronize(bvh->t.stream);
+  }
+  delete bvh;
+  return SP_OK;
+}
+
+int64_t sp_bvh_size(const sp_bvh *bvh) { return bvh ? bvh->t.n : 0; }
+
+int sp_bvh_export(sp_ctx *ctx, const sp_bvh *bvh, int32_t *internal_left, int32_t *internal_rope,
+                  float *internal_boxes, int32_t *leaf_object, int32_t *leaf_rope, float *leaf_boxes, float *scene) {
+  return guarded(ctx, [&](spb::Ctx &c) {
+    if (!bvh) throw spb::InvalidArgument("null bvh");
+    const spb::Tree &t = bvh->t;
+    const int dim = t.dim;
+    if (scene) {
+      float s[6] = {0, 0, 0, 0, 0, 0};
+      if (t.scene) SPB_CUDA(cudaMemcpyAsync(s, t.scene, sizeof(s), cudaMemcpyDeviceToHost, c.stream));
+      finish(c);
+      for (int k = 0; k < dim; ++k) {
+        scene[k] = s[k];
+        scene[dim + k] = s[3 + k];
+      }
+    }
+    if (t.n == 0) return;
+    const int64_t nn = 2 * t.n - 1;
+    std::vector<float4> h((size_t)nn * 2);
+    SPB_CUDA(cudaMemcpyAsync(h.data(), t.nodes, h.size() * sizeof(float4), cudaMemcpyDeviceToHost, c.stream));
+    finish(c);
+    auto bits = [](float f) {
+      int32_t i;
+      memcpy(&i, &f, 4);
+      return i;
+    };
+    for (int64_t r = 0; r < nn; ++r) {
+      const float4 &lo = h[(size_t)(2 * r)], &hi = h[(size_t)(2 * r + 1)];
+      const float l3[3] = {lo.x, lo.y, lo.z}, h3[3] = {hi.x, hi.y, hi.z};
+      const bool leaf = r >= t.n - 1;
+      const int64_t i = leaf ? r - (t.n - 1) : r;
+      int32_t *link = leaf ? leaf_object : internal_left;
+      int32_t *rope = leaf ? leaf_rope : internal_rope;
+      float *box = leaf ? leaf_boxes : internal_boxes;
+      if (link) link[i] = bits(lo.w);
+      if (rope) rope[i] = bits(hi.w);
+      if (box)
+        for (int k = 0; k < dim; ++k) {
+          box[i * 2 * dim + k] = l3[k];
+          box[i * 2 * dim + dim + k] = h3[k];
+        }
+    }
+  });
+}
+
+int sp_range_count(sp_ctx *ctx, const sp_bvh *bvh, int pred_kind, const float *preds, int64_t nq, int32_t cap,
+                   int32_t *counts, int mem) {
+  return guarded(ctx, [&](spb::Ctx &c) {
+    if (!bvh) throw spb::InvalidArgument("null bvh");
+    if (nq < 0) throw spb::InvalidArgument("negative query count");
+    const int dim = bvh->t.dim;
+    const size_t per = pred_kind == SP_PRED_BOX ? 2 * dim : dim + 1;
+    In<float> p(c, preds, (size_t)nq * per, mem);
+    Out<int32_t> o(c, counts, (size_t)nq, mem);
+    spb::range_count(c, bvh->t, pred_kind == SP_PRED_BOX ? spb::RQ_BOXES : spb::RQ_SPHERES, p.p, nq, 0.f, cap, o.p,
+                     nullptr);
+    o.flush(c);
+    finish(c);
+  });
+}
+
+int sp_range_count_radius(sp_ctx *ctx, const sp_bvh *bvh, const float *centres, int64_t nq, float radius, int32_t cap,
+                          int32_t *counts, int mem) {
+  return guarded(ctx, [&](spb::Ctx &c) {
+    if (!bvh) throw spb::InvalidArgument("null bvh");
+    if (nq < 0) throw spb::InvalidArgument("negative query count");
+    In<float> p(c, centres, (size_t)nq * bvh->t.dim, mem);
+    Out<int32_t> o(c, counts, (size_t)nq, mem);
+    spb::range_count(c, bvh->t, spb::RQ_RADIUS, p.p, nq, radius, cap, o.p, nullptr);
+    o.flush(c);
+    finish(c);
+  });
+}
+
+int sp_range_crs(sp_ctx *ctx, const sp_bvh *bvh, int pred_kind, const float *preds, int64_t nq, int64_t *offsets,
+                 int32_t *values, int64_t capacity, int mem) {
+  return guarded(ctx, [&](spb::Ctx &c) {
+    if (!bvh) throw spb::InvalidArgument("null bvh");
+    const int dim = bvh->t.dim;
+    const size_t per = pred_kind == SP_PRED_BOX ? 2 * dim : dim + 1;
+    In<float> p(c, preds, (size_t)nq * per, mem);
+    Out<int64_t> off(c, offsets, (size_t)nq + 1, mem);
+    // values: device scratch of `capacity` or the caller's device array
+    DevBuf<int32_t> vbuf;
+    int32_t *vdev = values;
+    if (mem == SP_MEM_HOST && values && capacity > 0) {
+      vbuf = DevBuf<int32_t>((size_t)capacity, c.stream);
+      vdev = vbuf.get();
+    }
+    int64_t total = spb::range_crs(c, bvh->t, pred_kind == SP_PRED_BOX ? spb::RQ_BOXES : spb::RQ_SPHERES, p.p, nq,
+                                   off.p, vdev, values ? capacity : 0);
+    off.flush(c);
+    if (total <= capacity && values && mem == SP_MEM_HOST && total > 0)
+      SPB_CUDA(cudaMemcpyAsync(values, vdev, (size_t)total * sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+    finish(c);
+    if (total > capacity && values) throw spb::CapacityError();
+  });
+}
+
+int sp_knn(sp_ctx *ctx, const sp_bvh *bvh, const float *origins, int64_t nq, int32_t k, int32_t *idx, float *dist,
+           int mem) {
+  return guarded(ctx, [&](spb::Ctx &c) {
+    if (!bvh) throw spb::InvalidArgument("null bvh");
+    if (k <= 0 || nq <= 0) return;
+    In<float> o(c, origins, (size_t)nq * bvh->t.dim, mem);
+    Out<int32_t> oi(c, idx, (size_t)nq * k, mem);
+    Out<float> od(c, dist, (size_t)nq * k, mem);
+    spb::knn(c, bvh->t, o.p, nq, k, oi.p, od.p);
+    oi.flush(c);
+    od.flush(c);
+    finish(c);
+  });
+}
+
+int sp_pair_list(sp_ctx *ctx, const sp_bvh *bvh, float eps, int32_t *pairs, int64_t capacity, int64_t *num_pairs,
+                 int mem) {
+  return guarded(ctx, [&](spb::Ctx &c) {
+    if (!bvh) throw spb::InvalidArgument("null bvh");
+    DevBuf<int32_t> pbuf;
+    int32_t *pdev = pairs;
+    if (mem == SP_MEM_HOST && pairs && capacity > 0) {
+      pbuf = DevBuf<int32_t>((size_t)capacity * 2, c.stream);
+      pdev = pbuf.get();
+    }
+    int64_t total = spb::pair_list(c, bvh->t, eps, pdev, pairs ? capacity : 0);
+    if (num_pairs) *num_pairs = total;
+    if (total <= capacity && pairs && mem == SP_MEM_HOST && total > 0)
+      SPB_CUDA(cudaMemcpyAsync(pairs, pdev, (size_t)total * 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+    finish(c);
+    if (total > capacity && pairs) throw spb::CapacityError();
+  });
+}
+
+int sp_sort_queries(sp_ctx *ctx, const float *points, int64_t nq, int dim, int32_t *order, int mem) {
+  return guarded(ctx, [&](spb::Ctx &c) {
+    check_dim(dim);
+    In<float> p(c, points, (size_t)nq * dim, mem);
+    Out<int32_t> o(c, order, (size_t)nq, mem);
+    spb::sort_points(c, p.p, nq, dim, o.p);
+    o.flush(c);
+    finish(c);
+  });
+}
+
+int sp_morton_codes(sp_ctx *ctx, const float *objects, int64_t n, int dim, int is_points, int code_width,
+                    uint64_t *codes, int mem) {
+  return guarded(ctx, [&](spb::Ctx &c) {
+    check_dim(dim);
+    if (code_width != 32 && code_width != 64) throw spb::InvalidArgument("code width must be 32 or 64");
+    const size_t per = is_points ? dim : 2 * dim;
+    In<float> obj(c, objects, (size_t)n * per, mem);
+    Out<uint64_t> o(c, codes, (size_t)n, mem);
+    DevBuf<float> scene(6, c.stream);
+    DevBuf<int> bad(1, c.stream);
+    spb::scene_bounds(c, obj.p, n, dim, is_points != 0, scene.get(), bad.get());
+    spb::morton_codes(c, obj.p, n, dim, is_points != 0, code_width, scene.get(), o.p, nullptr);
+    o.flush(c);
+    finish(c);
+  });
+}
+
+int sp_dbscan(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, int32_t min_pts, int algo,
+              int code_width, int32_t *labels, uint8_t *core, sp_timings *timings, sp_stats *stats, int mem) {
+  return guarded(ctx, [&](spb::Ctx &c) {
+    check_dim(dim);
+    if (algo < 0 || algo > 2) throw spb::InvalidArgument("unknown algorithm");
+    if (code_width != 32 && code_width != 64) throw spb::InvalidArgument("code width must be 32 or 64");
+    if (n < 0 || n > (1LL << 30)) throw spb::InvalidArgument("point count out of range");
+    In<float> p(c, points, (size_t)n * dim, mem);
+    Out<int32_t> ol(c, labels, (size_t)n, mem);
+    Out<uint8_t> oc(c, core, (size_t)n, mem);
+    DevBuf<int32_t> lscratch;
+    DevBuf<uint8_t> cscratch;
+    int32_t *lp = ol.p;
+    uint8_t *cp = oc.p;
+    if (!lp && n) { lscratch = DevBuf<int32_t>((size_t)n, c.stream); lp = lscratch.get(); }
+    if (!cp && n) { cscratch = DevBuf<uint8_t>((size_t)n, c.stream); cp = cscratch.get(); }
+    spb::DbscanResult res;
+    spb::dbscan(c, p.p, n, dim, eps, min_pts, algo, code_width, lp, cp, &res);
+    ol.flush(c);
+    oc.flush(c);
+    finish(c);
+    if (timings) {
+      timings->build_ms = res.ms[0];
+      timings->core_ms = res.ms[1];
+      timings->merge_ms = res.ms[2];
+      timings->finalize_ms = res.ms[3];
+    }
+    if (stats) {
+      stats->distance_checks = res.distance_checks;
+      stats->num_dense_cells = res.num_dense_cells;
+      stats->num_dense_points = res.num_dense_points;
+    }
+  });
+}
+
+int sp_generate_field(sp_ctx *ctx, int64_t n_total, int64_t first, int64_t count, uint64_t seed, float *out,
+                      int mem) {
+  return guarded(ctx, [&](spb::Ctx &c) {
+    if (n_total <= 0 || first < 0 || count < 0 || first + count > n_total)
+      throw spb::InvalidArgument("generate_field: bad slice");
+    Out<float> o(c, out, (size_t)count * 3, mem);
+    spb::generate_field(c, n_total, first, count, seed, o.p);
+    o.flush(c);
+    finish(c);
+  });
+}
+
+int sp_generate_uniform(sp_ctx *ctx, int64_t n, int dim, uint64_t seed, float *out, int mem) {
+  return guarded(ctx, [&](spb::Ctx &c) {
+    check_dim(dim);
+    Out<float> o(c, out, (size_t)n * dim, mem);
+    spb::generate_uniform(c, n, dim, seed, o.p);
+    o.flush(c);
+    finish(c);
+  });
+}
+
+}  // extern "C"

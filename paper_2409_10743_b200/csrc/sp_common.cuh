@@ -1,0 +1,175 @@
+// Shared device definitions for the B200 geometric-search path.
+//
+// Node layout (HBM): one unified array of 2n-1 nodes indexed by the
+// reference's NodeRef numbering (bvh.hpp:20-28) — internal nodes [0, n-1)
+// in Karras order, leaves [n-1, 2n-1) in Morton order — each node one 32-byte
+// sector read as two float4:
+//     lo = {min.x, min.y, min.z, bits(left child | object index)}
+//     hi = {max.x, max.y, max.z, bits(rope)}
+// 2-D data is stored with z = 0, which adds an exact 0.0 to every distance
+// accumulation, so one set of kernels serves both dimensions; only the Morton
+// stage and the dense grid look at `dim`.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <cmath>
+
+#include <stdexcept>
+#include <string>
+
+namespace spb {
+
+constexpr int32_t kSentinel = -1;
+constexpr int kNumSMs = 148;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct CapacityError : std::runtime_error {
+  CapacityError() : std::runtime_error("crs result exceeds capacity") {}
+};
+
+#define SPB_CUDA(expr)                                                                                   \
+  do {                                                                                                   \
+    cudaError_t _e = (expr);                                                                             \
+    if (_e != cudaSuccess)                                                                               \
+      throw ::spb::CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e) + " (" + __FILE__ + ":" + \
+                             std::to_string(__LINE__) + ")");                                            \
+  } while (0)
+
+// Launch bookkeeping: every kernel launch in the library goes through this
+// macro so the context can report how many of OUR kernels ran.
+extern thread_local int64_t *g_launch_counter;
+#define SPB_LAUNCHED()                                 \
+  do {                                                 \
+    SPB_CUDA(cudaGetLastError());                      \
+    if (::spb::g_launch_counter) ++*::spb::g_launch_counter; \
+  } while (0)
+
+inline unsigned grid_for(int64_t n, int block, int64_t cap = 148LL * 32) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+// ---- exact comparison arithmetic (geometry.hpp:73-96, 116-119) -------------
+// The reference decides `float(sqrt(S)) <= r` with S the double-accumulated
+// squared gap.  Since S -> float(sqrt_rn(S)) is monotone, that equals
+// `S <= T(r)` for T(r) = the largest double with float(sqrt(T)) <= r.  T is
+// found once per radius (a few ulps from (r + ulp/2)^2) and the hot loops
+// never take a square root.  All arithmetic uses explicit _rn intrinsics so
+// no FMA contraction can change a bit.
+__host__ __device__ inline double next_up(double x) {
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double(__double_as_longlong(x) + 1);
+#else
+  int64_t b;
+  memcpy(&b, &x, 8);
+  ++b;
+  memcpy(&x, &b, 8);
+  return x;
+#endif
+}
+__host__ __device__ inline double next_down(double x) {
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double(__double_as_longlong(x) - 1);
+#else
+  int64_t b;
+  memcpy(&b, &x, 8);
+  --b;
+  memcpy(&x, &b, 8);
+  return x;
+#endif
+}
+
+__host__ __device__ __forceinline__ bool sqrt_le(double s, float r) {
+#ifdef __CUDA_ARCH__
+  return __double2float_rn(__dsqrt_rn(s)) <= r;
+#else
+  return (float)std::sqrt(s) <= r;  // IEEE sqrt, round-to-nearest cast
+#endif
+}
+
+// T(r); negative/NaN r -> -1 (no squared gap qualifies); +inf -> +inf.
+// Start from m^2, m = r + ulp(r)/2 (exact in double: m has <= 25 significant
+// bits), then step the few ulps the double rounding of sqrt can move it.
+__host__ __device__ inline double radius_threshold(float r) {
+  if (!(r >= 0.f)) return -1.0;
+  const double kInf = 1.0 / 0.0;
+  if (r > 3.4028234663852886e38f) return kInf;
+  double ulp;
+  if (r == 3.4028234663852886e38f) {
+    ulp = 20282409603651670423947251286016.0;  // 2^104
+  } else {
+#ifdef __CUDA_ARCH__
+    ulp = (double)nextafterf(r, kInf) - (double)r;
+#else
+    ulp = (double)std::nextafter(r, (float)kInf) - (double)r;
+#endif
+  }
+  double m = (double)r + 0.5 * ulp;
+  double t = m * m;
+  for (int i = 0; i < 64 && sqrt_le(next_up(t), r); ++i) t = next_up(t);
+  for (int i = 0; i < 64 && t > 0.0 && !sqrt_le(t, r); ++i) t = next_down(t);
+  return t;
+}
+
+// Squared distance from c to the box [lo, hi] accumulated exactly as
+// min_distance does: gap_k = max(lo-c, c-hi, 0) in double, s = ((0+g0²)+g1²)+g2².
+__device__ __forceinline__ double gap2(float cx, float cy, float cz, const float4 &lo, const float4 &hi) {
+  double gx = fmax(fmax(__dsub_rn((double)lo.x, (double)cx), __dsub_rn((double)cx, (double)hi.x)), 0.0);
+  double gy = fmax(fmax(__dsub_rn((double)lo.y, (double)cy), __dsub_rn((double)cy, (double)hi.y)), 0.0);
+  double gz = fmax(fmax(__dsub_rn((double)lo.z, (double)cz), __dsub_rn((double)cz, (double)hi.z)), 0.0);
+  double s = __dmul_rn(gx, gx);
+  s = __dadd_rn(s, __dmul_rn(gy, gy));
+  s = __dadd_rn(s, __dmul_rn(gz, gz));
+  return s;
+}
+
+// Point-to-point squared distance (distance(), geometry.hpp:73-81).
+__device__ __forceinline__ double dist2(float ax, float ay, float az, float bx, float by, float bz) {
+  double dx = __dsub_rn((double)ax, (double)bx);
+  double dy = __dsub_rn((double)ay, (double)by);
+  double dz = __dsub_rn((double)az, (double)bz);
+  double s = __dmul_rn(dx, dx);
+  s = __dadd_rn(s, __dmul_rn(dy, dy));
+  s = __dadd_rn(s, __dmul_rn(dz, dz));
+  return s;
+}
+
+// Closed-interval box overlap (geometry.hpp:121-128).
+__device__ __forceinline__ bool box_touch(const float4 &alo, const float4 &ahi, const float *b) {
+  return !(alo.x > b[3] || b[0] > ahi.x || alo.y > b[4] || b[1] > ahi.y || alo.z > b[5] || b[2] > ahi.z);
+}
+
+// std::min/std::max tie semantics (keep the first unless the second is
+// strictly smaller/larger) so unions reproduce the reference's signed zeros.
+__host__ __device__ __forceinline__ float keep_min(float a, float b) { return b < a ? b : a; }
+__host__ __device__ __forceinline__ float keep_max(float a, float b) { return a < b ? b : a; }
+
+// Monotone int encoding of floats for atomicMin/atomicMax bounds.
+__device__ __forceinline__ int32_t ord_of(float f) {
+  int32_t i = __float_as_int(f);
+  return i >= 0 ? i : (i ^ 0x7fffffff);
+}
+__host__ __device__ __forceinline__ float float_of_ord(int32_t i) {
+  int32_t b = i >= 0 ? i : (i ^ 0x7fffffff);
+#ifdef __CUDA_ARCH__
+  return __int_as_float(b);
+#else
+  float f;
+  memcpy(&f, &b, 4);
+  return f;
+#endif
+}
+
+__device__ __forceinline__ float4 ld_node(const float4 *nodes, int64_t i) { return __ldg(nodes + i); }
+
+}  // namespace spb

@@ -1,0 +1,190 @@
+// Clustering on sm_100a: FDBSCAN / friends-of-friends with the pair traversal
+// fused with lock-free union-find (K6), capped core counting (K5 with early
+// termination), the border claim latch, and label finalisation (K7).
+// Reference: dbscan.hpp:72-292, union_find.hpp:17-82, traversal.hpp:162-184.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+
+#include "sp_common.cuh"
+#include "sp_internal.hpp"
+#include "sp_query.hpp"
+#include "sp_traverse.cuh"
+
+namespace spb {
+
+// Union-find lives in LEAF-POSITION space: leaf p's neighbours in Morton order
+// are its neighbours in memory, so parent[] accesses stay local.  Canonical
+// labels (the smallest ORIGINAL index of each set, finalize_labels,
+// dbscan.hpp:72-98) are recovered in the finalisation pass.
+
+__global__ void k_iota(int32_t *a, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) a[i] = (int32_t)i;
+}
+
+// Capped neighbour counts for every point (detect_core_counts,
+// dbscan.hpp:146-182); queries run in leaf order, which is the order
+// sort_queries gives the same points (traversal.hpp:209-218).
+__global__ void __launch_bounds__(128) k_core_flags(const float4 *__restrict__ nodes, int64_t n, double thr,
+                                                    int32_t min_pts, uint8_t *__restrict__ corep) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const float4 me = ld_node(nodes, 2 * (n - 1 + p));
+  corep[p] = count_sphere(nodes, n, me.x, me.y, me.z, thr, min_pts) >= min_pts;
+}
+
+// Pair traversal fused with the merge rule.  FOF: every close pair unions and
+// marks both ends as having a partner (core <=> set size > 1,
+// dbscan.hpp:102-110, 259-263).  Otherwise merge_close_pair
+// (dbscan.hpp:123-137): core-core unions; core-noncore unions iff the
+// non-core side wins its one-shot claim latch (union_find.hpp:63-82).
+template <bool FOF>
+__global__ void __launch_bounds__(128) k_merge_pairs(const float4 *__restrict__ nodes, int64_t n, double thr,
+                                                     int32_t *parent, uint8_t *corep, uint32_t *claims) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int64_t first_leaf = n - 1;
+  const float4 me = ld_node(nodes, 2 * (first_leaf + p));
+  int32_t cur = node_rope(ld_node(nodes, 2 * (first_leaf + p) + 1));
+  bool any = false;
+  const bool core_p = FOF ? true : corep[p] != 0;
+  while (cur != kSentinel) {
+    const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
+    const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+    const bool hit = gap2(me.x, me.y, me.z, lo, hi) <= thr;
+    if (cur >= first_leaf) {
+      if (hit) {
+        const int32_t q = (int32_t)(cur - first_leaf);
+        if (FOF) {
+          uf_union(parent, (int32_t)p, q);
+          corep[q] = 1;
+          any = true;
+        } else {
+          const bool core_q = corep[q] != 0;
+          if (core_p && core_q) {
+            uf_union(parent, (int32_t)p, q);
+          } else if (core_p || core_q) {
+            const int32_t b = core_p ? q : (int32_t)p;  // the non-core side
+            const uint32_t bit = 1u << (b & 31);
+            if (!(atomicOr(&claims[b >> 5], bit) & bit)) uf_union(parent, (int32_t)p, q);
+          }
+        }
+      }
+      cur = node_rope(hi);
+    } else {
+      cur = hit ? node_link(lo) : node_rope(hi);
+    }
+  }
+  if (FOF && any) corep[p] = 1;
+}
+
+__device__ __forceinline__ bool is_member(const uint8_t *corep, const uint32_t *claims, int64_t p) {
+  return corep[p] != 0 || (claims && ((claims[p >> 5] >> (p & 31)) & 1u));
+}
+
+// Finalisation 1: compress every member to its root and fold the smallest
+// original index into minobj[root] (warp-aggregated: Morton-adjacent members
+// usually share a root).
+__global__ void __launch_bounds__(256) k_final_roots(int64_t n, int32_t *parent, const uint8_t *__restrict__ corep,
+                                                     const uint32_t *__restrict__ claims,
+                                                     const int32_t *__restrict__ perm, int32_t *minobj) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int32_t key = -1, v = 0x7fffffff;
+  if (p < n && is_member(corep, claims, p)) {
+    key = uf_root(parent, (int32_t)p);
+    parent[p] = key;
+    v = perm[p];
+  }
+  const uint32_t peers = __match_any_sync(0xffffffffu, key);
+  const int32_t m = (int32_t)__reduce_min_sync(peers, (uint32_t)v);
+  if (key >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicMin(&minobj[key], m);
+}
+
+// Finalisation 2: scatter labels/core flags to original order; a point that
+// is neither core nor claimed is a singleton and therefore noise.
+__global__ void __launch_bounds__(256) k_final_labels(int64_t n, const int32_t *__restrict__ parent,
+                                                      const uint8_t *__restrict__ corep,
+                                                      const uint32_t *__restrict__ claims,
+                                                      const int32_t *__restrict__ perm,
+                                                      const int32_t *__restrict__ minobj, int32_t *__restrict__ labels,
+                                                      uint8_t *__restrict__ core) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int32_t obj = perm[p];
+  const bool member = is_member(corep, claims, p);
+  labels[obj] = member ? minobj[parent[p]] : -1;
+  core[obj] = corep[p];
+}
+
+void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t min_pts, int algo, int width,
+            int32_t *labels, uint8_t *core, DbscanResult *res) {
+  if (!(eps > 0.f) || !std::isfinite(eps)) throw InvalidArgument("dbscan: eps must be positive and finite");
+  if (algo == 1) min_pts = 2;
+  if (min_pts < 2) throw InvalidArgument("dbscan: min_pts must be at least 2");
+  if (n == 0) return;
+  if (algo == 2) {
+    extern void densebox(Ctx &, const float *, int64_t, int, float, int32_t, int, int32_t *, uint8_t *,
+                         DbscanResult *);
+    densebox(c, points, n, dim, eps, min_pts, width, labels, core, res);
+    return;
+  }
+  cudaEvent_t ev[5];
+  for (auto &e : ev) SPB_CUDA(cudaEventCreate(&e));
+  SPB_CUDA(cudaEventRecord(ev[0], c.stream));
+  Tree t;
+  try {
+    build_tree(c, points, n, dim, true, width, t);
+  } catch (const InvalidArgument &) {
+    for (auto &e : ev) cudaEventDestroy(e);
+    throw InvalidArgument("dbscan: non-finite coordinate");
+  }
+  SPB_CUDA(cudaEventRecord(ev[1], c.stream));
+  const double thr = radius_threshold(eps);
+  const bool count_phase = min_pts > 2;
+  const unsigned g128 = (unsigned)((n + 127) / 128), g256 = (unsigned)((n + 255) / 256);
+  DevBuf<uint8_t> corep((size_t)n, c.stream);
+  DevBuf<int32_t> parent((size_t)n, c.stream), minobj((size_t)n, c.stream);
+  DevBuf<uint32_t> claims(count_phase ? (size_t)((n + 31) / 32) : 0, c.stream);
+  if (count_phase) {
+    k_core_flags<<<g128, 128, 0, c.stream>>>(t.nodes, n, thr, min_pts, corep.get());
+    SPB_LAUNCHED();
+  } else {
+    SPB_CUDA(cudaMemsetAsync(corep.get(), 0, (size_t)n, c.stream));
+  }
+  SPB_CUDA(cudaEventRecord(ev[2], c.stream));
+  k_iota<<<grid_for(n, 256, 148 * 16), 256, 0, c.stream>>>(parent.get(), n);
+  SPB_LAUNCHED();
+  if (count_phase) {
+    SPB_CUDA(cudaMemsetAsync(claims.get(), 0, claims.n * sizeof(uint32_t), c.stream));
+    k_merge_pairs<false><<<g128, 128, 0, c.stream>>>(t.nodes, n, thr, parent.get(), corep.get(), claims.get());
+  } else {
+    k_merge_pairs<true><<<g128, 128, 0, c.stream>>>(t.nodes, n, thr, parent.get(), corep.get(), nullptr);
+  }
+  SPB_LAUNCHED();
+  SPB_CUDA(cudaEventRecord(ev[3], c.stream));
+  SPB_CUDA(cudaMemsetAsync(minobj.get(), 0x7f, (size_t)n * sizeof(int32_t), c.stream));
+  k_final_roots<<<g256, 256, 0, c.stream>>>(n, parent.get(), corep.get(), claims.get(), t.perm, minobj.get());
+  SPB_LAUNCHED();
+  k_final_labels<<<g256, 256, 0, c.stream>>>(n, parent.get(), corep.get(), claims.get(), t.perm, minobj.get(), labels,
+                                             core);
+  SPB_LAUNCHED();
+  SPB_CUDA(cudaEventRecord(ev[4], c.stream));
+  SPB_CUDA(cudaEventSynchronize(ev[4]));
+  if (res) {
+    for (int i = 0; i < 4; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      res->ms[i] = ms;
+    }
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
+  corep.reset();
+  parent.reset();
+  minobj.reset();
+  claims.reset();
+  t.free_all();
+}
+
+}  // namespace spb

@@ -1,0 +1,103 @@
+// Host-side internals shared by the translation units of libspb200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <utility>
+
+#include "sp_common.cuh"
+
+namespace spb {
+
+// A context: one device, one stream, stream-ordered allocations from the
+// device's default memory pool (release threshold raised so freed blocks stay
+// reserved — a caching allocator without host synchronisation).
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool owns_stream = false;
+  std::string last_error;
+  int64_t launches = 0;
+};
+
+template <class T>
+struct DevBuf {
+  T *p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t count, cudaStream_t stream) : n(count), s(stream) {
+    if (count) {
+      cudaError_t e = cudaMallocAsync((void **)&p, count * sizeof(T), stream);
+      if (e != cudaSuccess) {
+        p = nullptr;
+        throw CudaError(std::string("device allocation of ") + std::to_string(count * sizeof(T)) +
+                        " bytes failed: " + cudaGetErrorString(e));
+      }
+    }
+  }
+  DevBuf(const DevBuf &) = delete;
+  DevBuf &operator=(const DevBuf &) = delete;
+  DevBuf(DevBuf &&o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf &operator=(DevBuf &&o) noexcept {
+    reset();
+    p = o.p; n = o.n; s = o.s;
+    o.p = nullptr; o.n = 0;
+    return *this;
+  }
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  T *release() { T *q = p; p = nullptr; n = 0; return q; }
+  T *get() const { return p; }
+};
+
+// A device-resident hierarchy (the B200 counterpart of Bvh<D>, bvh.hpp:43-86).
+struct Tree {
+  int64_t n = 0;
+  int dim = 3;
+  int width = 64;
+  bool points = true;       // built over point boxes (min == max)
+  float4 *nodes = nullptr;  // 2 float4 per node, 2n-1 nodes (NodeRef order)
+  int32_t *perm = nullptr;  // leaf position -> object index
+  float *scene = nullptr;   // device float[6]: min xyz, max xyz
+  cudaStream_t stream = nullptr;
+  Tree() = default;
+  Tree(const Tree &) = delete;
+  Tree &operator=(const Tree &) = delete;
+  ~Tree() { free_all(); }
+  void free_all() {
+    if (nodes) cudaFreeAsync(nodes, stream);
+    if (perm) cudaFreeAsync(perm, stream);
+    if (scene) cudaFreeAsync(scene, stream);
+    nodes = nullptr;
+    perm = nullptr;
+    scene = nullptr;
+  }
+};
+
+// ---- build stages (sp_build.cu) ----------------------------------------------
+// objects: device float[n*dim] (points) or float[n*2*dim] (boxes).
+// Computes the scene box into scene[6] and returns false (after a sync) if any
+// coordinate is non-finite.
+void scene_bounds(Ctx &c, const float *objects, int64_t n, int dim, bool points, float *scene, int *bad);
+// codes[i] = code_of(centroid(object i), scene); vals[i] = i.
+void morton_codes(Ctx &c, const float *objects, int64_t n, int dim, bool points, int width, const float *scene,
+                  uint64_t *codes, uint32_t *vals);
+// Stable LSD radix sort of (key, value) pairs over key bits [0, key_bits).
+// Sorted output ends in (*keys, *vals); the alternate buffers are scratch and
+// the pointers may be swapped.
+void radix_sort_pairs(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_alt, uint32_t **vals_alt, int64_t n,
+                      int key_bits, bool vals_iota);
+// Full Bvh::build into `t` (allocates t.nodes/perm/scene). Throws
+// InvalidArgument on non-finite input.
+void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, int width, Tree &t);
+// sort_queries: the stable 64-bit Morton order of points against their scene.
+void sort_points(Ctx &c, const float *pts, int64_t n, int dim, int32_t *order);
+
+}  // namespace spb

@@ -1,0 +1,469 @@
+// Query kernels over a device hierarchy: range counts (K5), CRS collection,
+// pair enumeration and k-nearest neighbours (K10).
+// Reference: traversal.hpp:23-266.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "sp_common.cuh"
+#include "sp_internal.hpp"
+#include "sp_query.hpp"
+#include "sp_traverse.cuh"
+
+namespace spb {
+
+// ---------------------------------------------------------------------------
+// predicates
+// ---------------------------------------------------------------------------
+struct SpherePred {
+  float x, y, z;
+  double thr;
+};
+
+// Representatives for sort_queries (traversal.hpp:188-218): sphere centres, or
+// box centroids (double midpoint rounded to float, geometry.hpp:130-137).
+__global__ void k_representatives(const float *__restrict__ preds, int64_t nq, int dim, int kind,
+                                  float *__restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride) {
+    for (int k = 0; k < dim; ++k) {
+      float v;
+      if (kind == 0) v = preds[q * (dim + 1) + k];
+      else v = __double2float_rn(__dmul_rn(__dadd_rn((double)preds[q * 2 * dim + k], (double)preds[q * 2 * dim + dim + k]), 0.5));
+      out[q * dim + k] = v;
+    }
+  }
+}
+
+void query_order(Ctx &c, const float *preds, int64_t nq, int dim, int kind, int32_t *order) {
+  if (nq <= 0) return;
+  if (kind == 0 && false) return;
+  DevBuf<float> reps((size_t)nq * dim, c.stream);
+  k_representatives<<<grid_for(nq, 256, 148 * 16), 256, 0, c.stream>>>(preds, nq, dim, kind, reps.get());
+  SPB_LAUNCHED();
+  sort_points(c, reps.get(), nq, dim, order);
+}
+
+// mode 0: spheres of one radius over centres float[nq*dim]
+// mode 1: spheres with per-query radius float[nq*(dim+1)]
+// mode 2: boxes float[nq*2*dim]
+template <int MODE>
+__global__ void __launch_bounds__(128) k_range_count(const float4 *__restrict__ nodes, int64_t n,
+                                                     const float *__restrict__ preds, int dim,
+                                                     const int32_t *__restrict__ order, int64_t nq, double thr0,
+                                                     int32_t cap, int32_t *__restrict__ counts) {
+  const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (qi >= nq) return;
+  const int64_t q = order ? order[qi] : qi;
+  int32_t c;
+  if (MODE < 2) {
+    const int stride = MODE == 0 ? dim : dim + 1;
+    const float *p = preds + q * stride;
+    float cx = p[0], cy = p[1], cz = dim == 3 ? p[2] : 0.f;
+    double thr = MODE == 0 ? thr0 : radius_threshold(p[dim]);
+    c = count_sphere(nodes, n, cx, cy, cz, thr, cap);
+  } else {
+    float b[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int k = 0; k < dim; ++k) {
+      b[k] = preds[q * 2 * dim + k];
+      b[3 + k] = preds[q * 2 * dim + dim + k];
+    }
+    c = 0;
+    int32_t cur = 0;
+    while (cur != kSentinel) {
+      const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
+      const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+      const bool hit = box_touch(lo, hi, b);
+      if (cur >= n - 1) {
+        if (hit && ++c == cap) break;
+        cur = node_rope(hi);
+      } else {
+        cur = hit ? node_link(lo) : node_rope(hi);
+      }
+    }
+  }
+  counts[q] = c;
+}
+
+void range_count(Ctx &c, const Tree &t, int kind, const float *preds, int64_t nq, float radius, int32_t cap,
+                 int32_t *counts, const int32_t *order_in) {
+  if (nq <= 0) return;
+  if (t.n == 0) {
+    SPB_CUDA(cudaMemsetAsync(counts, 0, (size_t)nq * sizeof(int32_t), c.stream));
+    return;
+  }
+  DevBuf<int32_t> order;
+  const int32_t *ord = order_in;
+  if (!ord) {
+    order = DevBuf<int32_t>((size_t)nq, c.stream);
+    if (kind == RQ_RADIUS) {
+      sort_points(c, preds, nq, t.dim, order.get());
+    } else {
+      query_order(c, preds, nq, t.dim, kind == RQ_SPHERES ? 0 : 1, order.get());
+    }
+    ord = order.get();
+  }
+  unsigned g = (unsigned)((nq + 127) / 128);
+  if (kind == RQ_RADIUS) {
+    double thr = radius_threshold(radius);
+    k_range_count<0><<<g, 128, 0, c.stream>>>(t.nodes, t.n, preds, t.dim, ord, nq, thr, cap, counts);
+  } else if (kind == RQ_SPHERES) {
+    k_range_count<1><<<g, 128, 0, c.stream>>>(t.nodes, t.n, preds, t.dim, ord, nq, 0.0, cap, counts);
+  } else {
+    k_range_count<2><<<g, 128, 0, c.stream>>>(t.nodes, t.n, preds, t.dim, ord, nq, 0.0, cap, counts);
+  }
+  SPB_LAUNCHED();
+}
+
+// ---------------------------------------------------------------------------
+// exclusive scan int32 -> int64 (offsets[n+1]); three kernels
+// ---------------------------------------------------------------------------
+constexpr int SCAN_BLOCK = 1024;
+
+__device__ __forceinline__ int64_t block_incl_scan(int64_t v, int64_t *wsum) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int d = 1; d < 32; d <<= 1) {
+    int64_t y = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v += y;
+  }
+  if (lane == 31) wsum[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t s = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+    for (int d = 1; d < 32; d <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, s, d);
+      if (lane >= d) s += y;
+    }
+    wsum[lane] = s;
+  }
+  __syncthreads();
+  if (warp > 0) v += wsum[warp - 1];
+  return v;
+}
+
+__global__ void k_scan_blocks(const int32_t *__restrict__ in, int64_t n, int64_t *__restrict__ out,
+                              int64_t *__restrict__ bsum) {
+  __shared__ int64_t wsum[32];
+  const int64_t i = (int64_t)blockIdx.x * SCAN_BLOCK + threadIdx.x;
+  int64_t v = i < n ? in[i] : 0;
+  int64_t incl = block_incl_scan(v, wsum);
+  if (i < n) out[i + 1] = incl;
+  if (threadIdx.x == SCAN_BLOCK - 1) bsum[blockIdx.x] = incl;
+}
+
+__global__ void k_scan_sums(int64_t *bsum, int64_t nb) {
+  __shared__ int64_t wsum[32];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nb; base += SCAN_BLOCK) {
+    int64_t i = base + threadIdx.x;
+    int64_t v = i < nb ? bsum[i] : 0;
+    int64_t incl = block_incl_scan(v, wsum);
+    int64_t c0 = carry;
+    if (i < nb) bsum[i] = c0 + incl - v;  // exclusive
+    __syncthreads();
+    if (threadIdx.x == SCAN_BLOCK - 1) carry = c0 + incl;
+    __syncthreads();
+  }
+}
+
+__global__ void k_scan_add(int64_t *out, int64_t n, const int64_t *__restrict__ bsum) {
+  const int64_t i = (int64_t)blockIdx.x * SCAN_BLOCK + threadIdx.x;
+  if (i < n) out[i + 1] += bsum[blockIdx.x];
+  if (i == 0) out[0] = 0;
+}
+
+void exclusive_scan(Ctx &c, const int32_t *in, int64_t n, int64_t *out) {
+  if (n <= 0) {
+    SPB_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), c.stream));
+    return;
+  }
+  const int64_t nb = (n + SCAN_BLOCK - 1) / SCAN_BLOCK;
+  DevBuf<int64_t> bsum((size_t)nb, c.stream);
+  k_scan_blocks<<<(unsigned)nb, SCAN_BLOCK, 0, c.stream>>>(in, n, out, bsum.get());
+  SPB_LAUNCHED();
+  k_scan_sums<<<1, SCAN_BLOCK, 0, c.stream>>>(bsum.get(), nb);
+  SPB_LAUNCHED();
+  k_scan_add<<<(unsigned)nb, SCAN_BLOCK, 0, c.stream>>>(out, n, bsum.get());
+  SPB_LAUNCHED();
+}
+
+// ---------------------------------------------------------------------------
+// CRS fill (query_crs second pass, traversal.hpp:254-260) and row sort
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(128) k_range_fill(const float4 *__restrict__ nodes, int64_t n,
+                                                    const float *__restrict__ preds, int dim,
+                                                    const int32_t *__restrict__ order, int64_t nq,
+                                                    const int64_t *__restrict__ offsets,
+                                                    uint64_t *__restrict__ keyed) {
+  const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (qi >= nq) return;
+  const int64_t q = order[qi];
+  int64_t w = offsets[q];
+  float b[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float cx = 0.f, cy = 0.f, cz = 0.f;
+  double thr = 0.0;
+  if (MODE == 1) {
+    const float *p = preds + q * (dim + 1);
+    cx = p[0]; cy = p[1]; cz = dim == 3 ? p[2] : 0.f;
+    thr = radius_threshold(p[dim]);
+  } else {
+    for (int k = 0; k < dim; ++k) {
+      b[k] = preds[q * 2 * dim + k];
+      b[3 + k] = preds[q * 2 * dim + dim + k];
+    }
+  }
+  int32_t cur = 0;
+  while (cur != kSentinel) {
+    const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
+    const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+    const bool hit = MODE == 1 ? (gap2(cx, cy, cz, lo, hi) <= thr) : box_touch(lo, hi, b);
+    if (cur >= n - 1) {
+      // key = (query << 32) | object; sorting the keys orders each row by object
+      if (hit) keyed[w++] = ((uint64_t)q << 32) | (uint32_t)node_link(lo);
+      cur = node_rope(hi);
+    } else {
+      cur = hit ? node_link(lo) : node_rope(hi);
+    }
+  }
+}
+
+__global__ void k_low_words(const uint64_t *__restrict__ keys, int64_t m, int32_t *__restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) out[i] = (int32_t)(uint32_t)keys[i];
+}
+
+int64_t range_crs(Ctx &c, const Tree &t, int kind, const float *preds, int64_t nq, int64_t *offsets, int32_t *values,
+                  int64_t capacity) {
+  if (nq <= 0) {
+    SPB_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int64_t), c.stream));
+    return 0;
+  }
+  DevBuf<int32_t> order((size_t)nq, c.stream), counts((size_t)nq, c.stream);
+  query_order(c, preds, nq, t.dim, kind == RQ_SPHERES ? 0 : 1, order.get());
+  range_count(c, t, kind, preds, nq, 0.f, 0, counts.get(), order.get());
+  exclusive_scan(c, counts.get(), nq, offsets);
+  int64_t total = 0;
+  SPB_CUDA(cudaMemcpyAsync(&total, offsets + nq, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  if (total > capacity) return total;
+  if (total == 0 || t.n == 0) return total;
+  DevBuf<uint64_t> k0((size_t)total, c.stream), k1((size_t)total, c.stream);
+  DevBuf<uint32_t> v0((size_t)total, c.stream), v1((size_t)total, c.stream);
+  unsigned g = (unsigned)((nq + 127) / 128);
+  if (kind == RQ_SPHERES)
+    k_range_fill<1><<<g, 128, 0, c.stream>>>(t.nodes, t.n, preds, t.dim, order.get(), nq, offsets, k0.get());
+  else
+    k_range_fill<2><<<g, 128, 0, c.stream>>>(t.nodes, t.n, preds, t.dim, order.get(), nq, offsets, k0.get());
+  SPB_LAUNCHED();
+  int qbits = 1;
+  while (qbits < 31 && (1LL << qbits) < nq) ++qbits;
+  uint64_t *ka = k0.get(), *kb = k1.get();
+  uint32_t *va = v0.get(), *vb = v1.get();
+  radix_sort_pairs(c, &ka, &va, &kb, &vb, total, 32 + qbits, true);
+  k_low_words<<<grid_for(total, 256, 148 * 16), 256, 0, c.stream>>>(ka, total, values);
+  SPB_LAUNCHED();
+  return total;
+}
+
+// ---------------------------------------------------------------------------
+// pair_traversal (traversal.hpp:162-184): leaf p walks from its own rope, so
+// only later leaves are examined and each close pair appears exactly once.
+// ---------------------------------------------------------------------------
+template <bool FILL>
+__global__ void __launch_bounds__(128) k_pairs(const float4 *__restrict__ nodes, int64_t n, double thr,
+                                               int32_t *__restrict__ counts, const int64_t *__restrict__ offsets,
+                                               int32_t *__restrict__ pairs) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int64_t self = n - 1 + p;
+  const float4 me = ld_node(nodes, 2 * self);
+  int32_t cur = node_rope(ld_node(nodes, 2 * self + 1));
+  int64_t w = FILL ? offsets[p] : 0;
+  int32_t c = 0;
+  while (cur != kSentinel) {
+    const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
+    const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+    const bool hit = gap2(me.x, me.y, me.z, lo, hi) <= thr;
+    if (cur >= n - 1) {
+      if (hit) {
+        if (FILL) {
+          pairs[2 * w] = node_link(me);
+          pairs[2 * w + 1] = node_link(lo);
+          ++w;
+        } else {
+          ++c;
+        }
+      }
+      cur = node_rope(hi);
+    } else {
+      cur = hit ? node_link(lo) : node_rope(hi);
+    }
+  }
+  if (!FILL) counts[p] = c;
+}
+
+int64_t pair_list(Ctx &c, const Tree &t, float eps, int32_t *pairs, int64_t capacity) {
+  if (t.n < 2) return 0;
+  const double thr = radius_threshold(eps);
+  DevBuf<int32_t> counts((size_t)t.n, c.stream);
+  DevBuf<int64_t> offsets((size_t)t.n + 1, c.stream);
+  unsigned g = (unsigned)((t.n + 127) / 128);
+  k_pairs<false><<<g, 128, 0, c.stream>>>(t.nodes, t.n, thr, counts.get(), nullptr, nullptr);
+  SPB_LAUNCHED();
+  exclusive_scan(c, counts.get(), t.n, offsets.get());
+  int64_t total = 0;
+  SPB_CUDA(cudaMemcpyAsync(&total, offsets.get() + t.n, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  if (total > capacity || total == 0) return total;
+  k_pairs<true><<<g, 128, 0, c.stream>>>(t.nodes, t.n, thr, nullptr, offsets.get(), pairs);
+  SPB_LAUNCHED();
+  return total;
+}
+
+// ---------------------------------------------------------------------------
+// k nearest neighbours (nearest_query, traversal.hpp:93-156).
+// Results are the min(k, n) smallest (float distance, object) pairs, which any
+// exact pruning order reproduces; this kernel keeps the reference's explicit
+// stack (near child popped first) and its strict `dist > worst` pruning, with
+// the candidate max-heap in local memory.
+// ---------------------------------------------------------------------------
+constexpr int KNN_STACK = 100;  // tree depth <= 96 prefix bits + 1
+
+__device__ __forceinline__ float box_dist(float x, float y, float z, const float4 &lo, const float4 &hi) {
+  return __double2float_rn(__dsqrt_rn(gap2(x, y, z, lo, hi)));
+}
+
+__device__ __forceinline__ bool cand_less(float da, int32_t ia, float db, int32_t ib) {
+  return da < db || (da == db && ia < ib);
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(128) k_knn(const float4 *__restrict__ nodes, int64_t n,
+                                             const float *__restrict__ origins, int dim,
+                                             const int32_t *__restrict__ order, int64_t nq, int32_t k,
+                                             float *__restrict__ gdist, int32_t *__restrict__ gidx,
+                                             int32_t *__restrict__ out_idx, float *__restrict__ out_dist) {
+  const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (qi >= nq) return;
+  const int64_t q = order[qi];
+  const float x = origins[q * dim], y = origins[q * dim + 1], z = dim == 3 ? origins[q * dim + 2] : 0.f;
+  const int32_t kk = (int32_t)((int64_t)k < n ? (int64_t)k : n);
+  // heap storage: registers/local for KMAX > 0, else global scratch rows
+  float hd_local[KMAX > 0 ? KMAX : 1];
+  int32_t hi_local[KMAX > 0 ? KMAX : 1];
+  float *hd = KMAX > 0 ? hd_local : gdist + qi * (int64_t)kk;
+  int32_t *hx = KMAX > 0 ? hi_local : gidx + qi * (int64_t)kk;
+  int32_t size = 0;
+
+  float sd[KNN_STACK];
+  int32_t sr[KNN_STACK];
+  int top = 0;
+  {
+    const float4 lo = ld_node(nodes, 0), hi = ld_node(nodes, 1);
+    sd[0] = box_dist(x, y, z, lo, hi);
+    sr[0] = 0;
+    top = 1;
+  }
+  while (top > 0) {
+    --top;
+    const float d = sd[top];
+    const int32_t ref = sr[top];
+    if (size == kk && d > hd[0]) continue;
+    if (ref >= n - 1) {
+      const int32_t obj = node_link(ld_node(nodes, 2 * (int64_t)ref));
+      if (size < kk) {  // push + sift up
+        int32_t i = size++;
+        while (i > 0) {
+          int32_t pa = (i - 1) >> 1;
+          if (!cand_less(hd[pa], hx[pa], d, obj)) break;
+          hd[i] = hd[pa];
+          hx[i] = hx[pa];
+          i = pa;
+        }
+        hd[i] = d;
+        hx[i] = obj;
+      } else if (cand_less(d, obj, hd[0], hx[0])) {  // replace top + sift down
+        int32_t i = 0;
+        while (true) {
+          int32_t l = 2 * i + 1, r = l + 1, m = i;
+          float md = d;
+          int32_t mi = obj;
+          if (l < size && cand_less(md, mi, hd[l], hx[l])) { m = l; md = hd[l]; mi = hx[l]; }
+          if (r < size && cand_less(md, mi, hd[r], hx[r])) { m = r; md = hd[r]; mi = hx[r]; }
+          if (m == i) break;
+          hd[i] = hd[m];
+          hx[i] = hx[m];
+          i = m;
+        }
+        hd[i] = d;
+        hx[i] = obj;
+      }
+      continue;
+    }
+    const float4 lo = ld_node(nodes, 2 * (int64_t)ref);
+    const int32_t left = node_link(lo);
+    const float4 llo = ld_node(nodes, 2 * (int64_t)left), lhi = ld_node(nodes, 2 * (int64_t)left + 1);
+    const int32_t right = node_rope(lhi);
+    const float4 rlo = ld_node(nodes, 2 * (int64_t)right), rhi = ld_node(nodes, 2 * (int64_t)right + 1);
+    float dn = box_dist(x, y, z, llo, lhi), df = box_dist(x, y, z, rlo, rhi);
+    int32_t rn = left, rf = right;
+    if (df < dn) {
+      float td = dn; dn = df; df = td;
+      int32_t tr = rn; rn = rf; rf = tr;
+    }
+    const bool full = size == kk;
+    if (!(full && df > hd[0]) && top < KNN_STACK) { sd[top] = df; sr[top] = rf; ++top; }
+    if (!(full && dn > hd[0]) && top < KNN_STACK) { sd[top] = dn; sr[top] = rn; ++top; }
+  }
+  // heap -> ascending order: repeatedly move the max to the end
+  for (int32_t end = size - 1; end > 0; --end) {
+    float td = hd[0]; int32_t tx = hx[0];
+    float ld = hd[end]; int32_t lx = hx[end];
+    int32_t i = 0;
+    while (true) {
+      int32_t l = 2 * i + 1, r = l + 1, m = i;
+      float md = ld; int32_t mi = lx;
+      if (l < end && cand_less(md, mi, hd[l], hx[l])) { m = l; md = hd[l]; mi = hx[l]; }
+      if (r < end && cand_less(md, mi, hd[r], hx[r])) { m = r; md = hd[r]; mi = hx[r]; }
+      if (m == i) break;
+      hd[i] = hd[m]; hx[i] = hx[m];
+      i = m;
+    }
+    hd[i] = ld; hx[i] = lx;
+    hd[end] = td; hx[end] = tx;
+  }
+  for (int32_t j = 0; j < k; ++j) {
+    const int64_t o = q * (int64_t)k + j;
+    out_idx[o] = j < size ? hx[j] : -1;
+    if (out_dist) out_dist[o] = j < size ? hd[j] : __int_as_float(0x7f800000);
+  }
+}
+
+void knn(Ctx &c, const Tree &t, const float *origins, int64_t nq, int32_t k, int32_t *idx, float *dist) {
+  if (nq <= 0 || k <= 0) return;
+  if (t.n == 0) {
+    SPB_CUDA(cudaMemsetAsync(idx, 0xff, (size_t)nq * k * sizeof(int32_t), c.stream));
+    return;
+  }
+  DevBuf<int32_t> order((size_t)nq, c.stream);
+  sort_points(c, origins, nq, t.dim, order.get());
+  unsigned g = (unsigned)((nq + 127) / 128);
+  const int64_t kk = std::min<int64_t>(k, t.n);
+  if (kk <= 16) {
+    k_knn<16><<<g, 128, 0, c.stream>>>(t.nodes, t.n, origins, t.dim, order.get(), nq, k, nullptr, nullptr, idx, dist);
+  } else if (kk <= 64) {
+    k_knn<64><<<g, 128, 0, c.stream>>>(t.nodes, t.n, origins, t.dim, order.get(), nq, k, nullptr, nullptr, idx, dist);
+  } else {
+    if ((double)nq * (double)kk * 8.0 > 8e9) throw CapacityError();
+    DevBuf<float> gd((size_t)(nq * kk), c.stream);
+    DevBuf<int32_t> gi((size_t)(nq * kk), c.stream);
+    k_knn<0><<<g, 128, 0, c.stream>>>(t.nodes, t.n, origins, t.dim, order.get(), nq, k, gd.get(), gi.get(), idx, dist);
+  }
+  SPB_LAUNCHED();
+}
+
+}  // namespace spb
