@@ -1,12 +1,542 @@
-// FDBSCAN-DenseBox (dbscan.hpp:298-449) — placeholder until the dense-grid
-// kernels land.
+// FDBSCAN-DenseBox on sm_100a (fdbscan_densebox, dbscan.hpp:298-449;
+// build_dense_grid, dense_grid.hpp:52-103).
+//
+//   K8  grid:   cell coordinates floor((p - anchor) / cell_length) in double,
+//               Morton-interleaved into one sortable key; a stable radix sort
+//               groups every cell's members contiguously in ascending index
+//               order; segment heads give cell sizes; cells with >= min_pts
+//               members are dense (none when coordinates could saturate).
+//   objects:    dense cells ordered by smallest member (dbscan.hpp:312-320)
+//               as tight boxes, then every sparse point as a point box in
+//               index order (dbscan.hpp:322-339) -> the mixed hierarchy.
+//   K9  core:   sparse points count self + sparse neighbours + dense-cell
+//               members within eps, stopping at min_pts (dbscan.hpp:351-385).
+//   K9  merge:  intra-dense-cell unions (dbscan.hpp:390-394), then every point
+//               walks the mixed tree: own cell skipped, dense hits expand to
+//               per-member checks with the i < j guard (counted as
+//               distance_checks), sparse hits merge with i < j
+//               (dbscan.hpp:398-440).
+// Union-find runs in ORIGINAL index space with min-index hooking, so a root
+// is already the canonical label (finalize_labels, dbscan.hpp:72-98).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <vector>
+
+#include "sp_common.cuh"
 #include "sp_internal.hpp"
 #include "sp_query.hpp"
+#include "sp_traverse.cuh"
 
 namespace spb {
 
-void densebox(Ctx &, const float *, int64_t, int, float, int32_t, int, int32_t *, uint8_t *, DbscanResult *) {
-  throw InvalidArgument("densebox: not implemented yet");
+namespace {
+
+__device__ __forceinline__ uint64_t spread3_21(uint64_t v) {
+  v &= 0x1fffffull;
+  v = (v | (v << 32)) & 0x001f00000000ffffull;
+  v = (v | (v << 16)) & 0x001f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+__device__ __forceinline__ uint64_t spread2_32(uint64_t v) {
+  v &= 0xffffffffull;
+  v = (v | (v << 16)) & 0x0000ffff0000ffffull;
+  v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
+  v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+
+// DenseGrid::coord_of (dense_grid.hpp:60-73) for one axis.
+__host__ __device__ __forceinline__ int64_t cell_coord(float p, float anchor, float cell) {
+  double f = floor(((double)p - (double)anchor) / (double)cell);
+  if (f < -4.0e18) f = -4.0e18;
+  if (f > 4.0e18) f = 4.0e18;
+  return (int64_t)f;
+}
+
+// Morton key of the cell (axis 0 in the LSB), or per-axis coordinate keys
+// when the coordinates need more than the interleave width.
+__global__ void k_cell_keys(const float *__restrict__ pts, int64_t n, int dim, const float *__restrict__ scene,
+                            float cell, int axis, uint64_t *__restrict__ keys) {
+  const float a0 = scene[0], a1 = scene[1], a2 = scene[2];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float *p = pts + i * dim;
+    if (axis >= 0) {
+      const float a = axis == 0 ? a0 : (axis == 1 ? a1 : a2);
+      keys[i] = (uint64_t)cell_coord(p[axis], a, cell);
+      continue;
+    }
+    const uint64_t c0 = (uint64_t)cell_coord(p[0], a0, cell), c1 = (uint64_t)cell_coord(p[1], a1, cell);
+    if (dim == 3) {
+      const uint64_t c2 = (uint64_t)cell_coord(p[2], a2, cell);
+      keys[i] = spread3_21(c0) | (spread3_21(c1) << 1) | (spread3_21(c2) << 2);
+    } else {
+      keys[i] = spread2_32(c0) | (spread2_32(c1) << 1);
+    }
+  }
+}
+
+__global__ void k_gather_keys(const float *__restrict__ pts, int64_t n, int dim, const float *__restrict__ scene,
+                              float cell, int axis, const uint32_t *__restrict__ order, uint64_t *__restrict__ keys) {
+  const float a = scene[axis];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    keys[i] = (uint64_t)cell_coord(pts[(int64_t)order[i] * dim + axis], a, cell);
+}
+
+// Cell heads in the sorted order: head[i] = 1 where a new cell starts.  For
+// the per-axis path the equality test needs all coordinates.
+__global__ void k_heads(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ order,
+                        const float *__restrict__ pts, int dim, const float *__restrict__ scene, float cell,
+                        int64_t n, bool exact_keys, int32_t *__restrict__ head) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    int32_t h;
+    if (i == 0) {
+      h = 1;
+    } else if (exact_keys) {
+      h = keys[i] != keys[i - 1];
+    } else {
+      const float *a = pts + (int64_t)order[i] * dim, *b = pts + (int64_t)order[i - 1] * dim;
+      h = 0;
+      for (int k = 0; k < dim; ++k) h |= cell_coord(a[k], scene[k], cell) != cell_coord(b[k], scene[k], cell);
+    }
+    head[i] = h;
+  }
+}
+
+// cell_start[c] = sorted position where cell c begins (c from the head scan).
+__global__ void k_cell_starts(const int32_t *__restrict__ head, const int64_t *__restrict__ scan, int64_t n,
+                              int64_t *__restrict__ cell_start) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    if (head[i]) cell_start[scan[i]] = i;
+}
+
+// dense flag per cell; dense cells emit (min member, cell) for ordering.
+__global__ void k_dense_flags(const int64_t *__restrict__ cell_start, int64_t m, int64_t n, int32_t min_pts,
+                              bool no_dense, int32_t *__restrict__ dense) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m; c += stride) {
+    const int64_t len = (c + 1 < m ? cell_start[c + 1] : n) - cell_start[c];
+    dense[c] = (!no_dense && len >= min_pts) ? 1 : 0;
+  }
+}
+
+__global__ void k_dense_pack(const int32_t *__restrict__ dense, const int64_t *__restrict__ dscan,
+                             const int64_t *__restrict__ cell_start, const uint32_t *__restrict__ order, int64_t m,
+                             uint64_t *__restrict__ minkey, uint32_t *__restrict__ cellid) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m; c += stride) {
+    if (!dense[c]) continue;
+    const int64_t d = dscan[c];
+    minkey[d] = order[cell_start[c]];  // members ascend within a cell (stable sort)
+    cellid[d] = (uint32_t)c;
+  }
+}
+
+// One warp per dense object: member range, point_cell[], tight box
+// (dense_grid.hpp / dbscan.hpp:326-333).
+__global__ void k_dense_objects(const uint32_t *__restrict__ dense_cell, int64_t nd,
+                                const int64_t *__restrict__ cell_start, int64_t m, int64_t n,
+                                const uint32_t *__restrict__ order, const float *__restrict__ pts, int dim,
+                                int32_t *__restrict__ point_cell, int64_t *__restrict__ dbeg, int32_t *__restrict__ dlen,
+                                float *__restrict__ objects) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= nd) return;
+  const int64_t c = dense_cell[warp];
+  const int64_t s = cell_start[c], e = c + 1 < m ? cell_start[c + 1] : n;
+  float lo[3] = {3.4028235e38f, 3.4028235e38f, 3.4028235e38f}, hi[3] = {-3.4028235e38f, -3.4028235e38f, -3.4028235e38f};
+  for (int64_t i = s + lane; i < e; i += 32) {
+    const uint32_t o = order[i];
+    point_cell[o] = (int32_t)warp;
+    for (int k = 0; k < dim; ++k) {
+      const float v = pts[(int64_t)o * dim + k];
+      lo[k] = fminf(lo[k], v);
+      hi[k] = fmaxf(hi[k], v);
+    }
+  }
+  for (int k = 0; k < dim; ++k) {
+    for (int off = 16; off; off >>= 1) {
+      lo[k] = fminf(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], off));
+      hi[k] = fmaxf(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], off));
+    }
+  }
+  if (lane == 0) {
+    dbeg[warp] = s;
+    dlen[warp] = (int32_t)(e - s);
+    for (int k = 0; k < dim; ++k) {
+      objects[warp * 2 * dim + k] = lo[k];
+      objects[warp * 2 * dim + dim + k] = hi[k];
+    }
+  }
+}
+
+__global__ void k_sparse_flags(const int32_t *__restrict__ point_cell, int64_t n, int32_t *__restrict__ flag) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) flag[i] = point_cell[i] < 0;
+}
+
+__global__ void k_sparse_objects(const int32_t *__restrict__ point_cell, const int64_t *__restrict__ sscan, int64_t n,
+                                 int64_t nd, const float *__restrict__ pts, int dim, int32_t *__restrict__ sparse_pts,
+                                 float *__restrict__ objects) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    if (point_cell[i] >= 0) continue;
+    const int64_t s = sscan[i];
+    sparse_pts[s] = (int32_t)i;
+    float *o = objects + (nd + s) * 2 * dim;
+    for (int k = 0; k < dim; ++k) o[k] = o[dim + k] = pts[i * dim + k];
+  }
+}
+
+struct DenseView {
+  const float4 *nodes;
+  int64_t nobj;
+  int64_t nd;
+  const int64_t *dbeg;
+  const int32_t *dlen;
+  const uint32_t *members;  // sorted-by-cell original indices
+  const int32_t *sparse_pts;
+  const float *pts;
+  int dim;
+  double thr;
+};
+
+__device__ __forceinline__ void load_pt(const float *pts, int dim, int64_t i, float &x, float &y, float &z) {
+  x = pts[i * dim];
+  y = pts[i * dim + 1];
+  z = dim == 3 ? pts[i * dim + 2] : 0.f;
+}
+
+// Core detection for sparse points (dbscan.hpp:351-385).
+__global__ void __launch_bounds__(128) k_db_core(DenseView v, const uint32_t *__restrict__ qorder, int64_t n,
+                                                 const int32_t *__restrict__ point_cell, int32_t min_pts,
+                                                 uint8_t *__restrict__ core) {
+  const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (qi >= n) return;
+  const int64_t i = qorder[qi];
+  if (point_cell[i] >= 0) return;  // dense members are core already
+  float x, y, z;
+  load_pt(v.pts, v.dim, i, x, y, z);
+  int32_t cnt = 0;
+  int32_t cur = 0;
+  while (cur != kSentinel) {
+    const float4 lo = ld_node(v.nodes, 2 * (int64_t)cur);
+    const float4 hi = ld_node(v.nodes, 2 * (int64_t)cur + 1);
+    const bool hit = gap2(x, y, z, lo, hi) <= v.thr;
+    if (cur >= v.nobj - 1) {
+      if (hit) {
+        const int32_t o = node_link(lo);
+        if (o < v.nd) {
+          const int64_t b = v.dbeg[o];
+          const int32_t len = v.dlen[o];
+          for (int32_t t = 0; t < len && cnt < min_pts; ++t) {
+            float qx, qy, qz;
+            load_pt(v.pts, v.dim, v.members[b + t], qx, qy, qz);
+            if (dist2(x, y, z, qx, qy, qz) <= v.thr) ++cnt;
+          }
+        } else {
+          ++cnt;
+        }
+        if (cnt >= min_pts) break;
+      }
+      cur = node_rope(hi);
+    } else {
+      cur = hit ? node_link(lo) : node_rope(hi);
+    }
+  }
+  core[i] = cnt >= min_pts;
+}
+
+// Intra-cell unions: every member joins its cell's first (smallest) member.
+__global__ void k_db_cell_unions(const int64_t *__restrict__ dbeg, const int32_t *__restrict__ dlen, int64_t nd,
+                                 const uint32_t *__restrict__ members, int32_t *parent) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= nd) return;
+  const int64_t b = dbeg[warp];
+  const int32_t first = (int32_t)members[b];
+  for (int32_t t = 1 + lane; t < dlen[warp]; t += 32) uf_union(parent, first, (int32_t)members[b + t]);
+}
+
+template <bool FOF>
+__device__ __forceinline__ void db_merge(int32_t i, int32_t j, int32_t *parent, uint8_t *core, uint32_t *claims) {
+  if (FOF) {
+    uf_union(parent, i, j);
+    core[i] = 1;
+    core[j] = 1;
+    return;
+  }
+  const bool ci = core[i] != 0, cj = core[j] != 0;
+  if (ci && cj) {
+    uf_union(parent, i, j);
+  } else if (ci || cj) {
+    const int32_t b = ci ? j : i;
+    const uint32_t bit = 1u << (b & 31);
+    if (!(atomicOr(&claims[b >> 5], bit) & bit)) uf_union(parent, i, j);
+  }
+}
+
+template <bool FOF>
+__global__ void __launch_bounds__(128) k_db_merge(DenseView v, const uint32_t *__restrict__ qorder, int64_t n,
+                                                  const int32_t *__restrict__ point_cell, int32_t *parent,
+                                                  uint8_t *core, uint32_t *claims,
+                                                  unsigned long long *__restrict__ checks_total) {
+  const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t checks = 0;
+  if (qi < n) {
+    const int32_t i = (int32_t)qorder[qi];
+    const int32_t own = point_cell[i];
+    float x, y, z;
+    load_pt(v.pts, v.dim, i, x, y, z);
+    int32_t cur = 0;
+    while (cur != kSentinel) {
+      const float4 lo = ld_node(v.nodes, 2 * (int64_t)cur);
+      const float4 hi = ld_node(v.nodes, 2 * (int64_t)cur + 1);
+      const bool hit = gap2(x, y, z, lo, hi) <= v.thr;
+      if (cur >= v.nobj - 1) {
+        if (hit) {
+          const int32_t o = node_link(lo);
+          if (o < v.nd) {
+            if (o != own) {
+              const int64_t b = v.dbeg[o];
+              const int32_t len = v.dlen[o];
+              for (int32_t t = 0; t < len; ++t) {
+                const int32_t j = (int32_t)v.members[b + t];
+                if (i < j) {
+                  ++checks;
+                  float qx, qy, qz;
+                  load_pt(v.pts, v.dim, j, qx, qy, qz);
+                  if (dist2(x, y, z, qx, qy, qz) <= v.thr) db_merge<FOF>(i, j, parent, core, claims);
+                }
+              }
+            }
+          } else {
+            const int32_t j = v.sparse_pts[o - v.nd];
+            if (i < j) db_merge<FOF>(i, j, parent, core, claims);
+          }
+        }
+        cur = node_rope(hi);
+      } else {
+        cur = hit ? node_link(lo) : node_rope(hi);
+      }
+    }
+  }
+  // warp-aggregate the distance-check counter
+  for (int off = 16; off; off >>= 1) checks += __shfl_xor_sync(0xffffffffu, checks, off);
+  if ((threadIdx.x & 31) == 0 && checks) atomicAdd(checks_total, (unsigned long long)checks);
+}
+
+__global__ void k_db_labels(int64_t n, int32_t *parent, const uint8_t *__restrict__ core,
+                            const uint32_t *__restrict__ claims, int32_t *__restrict__ labels,
+                            uint8_t *__restrict__ core_out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const bool member = core[i] || (claims && ((claims[i >> 5] >> (i & 31)) & 1u));
+    labels[i] = member ? uf_root(parent, (int32_t)i) : -1;
+    core_out[i] = core[i];
+  }
+}
+
+__global__ void k_iota32(int32_t *a, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) a[i] = (int32_t)i;
+}
+
+__global__ void k_dense_core(const int32_t *__restrict__ point_cell, int64_t n, uint8_t *__restrict__ core) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) core[i] = point_cell[i] >= 0;
+}
+
+}  // namespace
+
+void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t min_pts, int width, int32_t *labels,
+              uint8_t *core_out, DbscanResult *res) {
+  cudaEvent_t ev[5];
+  for (auto &e : ev) SPB_CUDA(cudaEventCreate(&e));
+  SPB_CUDA(cudaEventRecord(ev[0], c.stream));
+  const unsigned G = grid_for(n, 256, 148 * 16);
+
+  // ---- grid (build_dense_grid) ----
+  float cell = (float)((double)eps / std::sqrt((double)dim) * (1.0 - 1e-6));
+  bool no_dense = !(cell > 0.f);
+  DevBuf<float> scene(6, c.stream);
+  DevBuf<int> bad(1, c.stream);
+  scene_bounds(c, pts, n, dim, true, scene.get(), bad.get());
+  float hs[6];
+  int hbad = 0;
+  SPB_CUDA(cudaMemcpyAsync(hs, scene.get(), sizeof(hs), cudaMemcpyDeviceToHost, c.stream));
+  SPB_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  if (hbad) {
+    for (auto &e : ev) cudaEventDestroy(e);
+    throw InvalidArgument("dbscan: non-finite coordinate");
+  }
+  for (int k = 0; k < dim && !no_dense; ++k) {
+    double extent = (double)hs[3 + k] - (double)hs[k];
+    no_dense = extent / (double)cell >= 4.0e18;
+  }
+  if (!(cell > 0.f)) cell = 1.f;
+
+  DevBuf<int32_t> point_cell((size_t)n, c.stream);
+  SPB_CUDA(cudaMemsetAsync(point_cell.get(), 0xff, (size_t)n * sizeof(int32_t), c.stream));
+  DevBuf<uint64_t> k0((size_t)n, c.stream), k1((size_t)n, c.stream);
+  DevBuf<uint32_t> v0((size_t)n, c.stream), v1((size_t)n, c.stream);
+  uint32_t *order = nullptr;  // points sorted by cell (members ascending)
+  int64_t nd = 0;
+  DevBuf<int64_t> dbeg, cell_start;
+  DevBuf<int32_t> dlen;
+  DevBuf<float> objects;
+  int64_t num_dense_points = 0;
+  {
+    // bits needed per axis for the largest coordinate (that of the scene max)
+    int bits = 1;
+    for (int k = 0; k < dim; ++k) {
+      int64_t mc = cell_coord(hs[3 + k], hs[k], cell);
+      while (bits < 63 && (1LL << bits) <= mc) ++bits;
+    }
+    const bool interleave = (int64_t)bits * dim <= 64;
+    uint64_t *ka = k0.get(), *kb = k1.get();
+    uint32_t *va = v0.get(), *vb = v1.get();
+    if (interleave) {
+      k_cell_keys<<<G, 256, 0, c.stream>>>(pts, n, dim, scene.get(), cell, -1, ka);
+      SPB_LAUNCHED();
+      radix_sort_pairs(c, &ka, &va, &kb, &vb, n, bits * dim, true);
+    } else {
+      // lexicographic (x, y, z) by stable per-axis passes, last axis first
+      bool first = true;
+      for (int axis = dim - 1; axis >= 0; --axis) {
+        if (first) {
+          k_cell_keys<<<G, 256, 0, c.stream>>>(pts, n, dim, scene.get(), cell, axis, ka);
+        } else {
+          k_gather_keys<<<G, 256, 0, c.stream>>>(pts, n, dim, scene.get(), cell, axis, va, ka);
+        }
+        SPB_LAUNCHED();
+        radix_sort_pairs(c, &ka, &va, &kb, &vb, n, bits, first);
+        first = false;
+      }
+    }
+    order = va;
+    // segments
+    DevBuf<int32_t> head((size_t)n, c.stream);
+    DevBuf<int64_t> hscan((size_t)n + 1, c.stream);
+    k_heads<<<G, 256, 0, c.stream>>>(ka, order, pts, dim, scene.get(), cell, n, interleave, head.get());
+    SPB_LAUNCHED();
+    exclusive_scan(c, head.get(), n, hscan.get());
+    int64_t m = 0;
+    SPB_CUDA(cudaMemcpyAsync(&m, hscan.get() + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    SPB_CUDA(cudaStreamSynchronize(c.stream));
+    cell_start = DevBuf<int64_t>((size_t)m, c.stream);
+    k_cell_starts<<<G, 256, 0, c.stream>>>(head.get(), hscan.get(), n, cell_start.get());
+    SPB_LAUNCHED();
+    DevBuf<int32_t> dense((size_t)m, c.stream);
+    DevBuf<int64_t> dscan((size_t)m + 1, c.stream);
+    const unsigned Gm = grid_for(m, 256, 148 * 16);
+    k_dense_flags<<<Gm, 256, 0, c.stream>>>(cell_start.get(), m, n, min_pts, no_dense, dense.get());
+    SPB_LAUNCHED();
+    exclusive_scan(c, dense.get(), m, dscan.get());
+    SPB_CUDA(cudaMemcpyAsync(&nd, dscan.get() + m, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    SPB_CUDA(cudaStreamSynchronize(c.stream));
+    if (nd > 0) {
+      // dense cells ordered by their smallest member
+      DevBuf<uint64_t> mk0((size_t)nd, c.stream), mk1((size_t)nd, c.stream);
+      DevBuf<uint32_t> mv0((size_t)nd, c.stream), mv1((size_t)nd, c.stream);
+      k_dense_pack<<<Gm, 256, 0, c.stream>>>(dense.get(), dscan.get(), cell_start.get(), order, m, mk0.get(),
+                                             mv0.get());
+      SPB_LAUNCHED();
+      uint64_t *ma = mk0.get(), *mb = mk1.get();
+      uint32_t *wa = mv0.get(), *wb = mv1.get();
+      radix_sort_pairs(c, &ma, &wa, &mb, &wb, nd, 32, false);
+      dbeg = DevBuf<int64_t>((size_t)nd, c.stream);
+      dlen = DevBuf<int32_t>((size_t)nd, c.stream);
+      objects = DevBuf<float>((size_t)n * 2 * dim, c.stream);  // upper bound: nd + sparse <= n
+      k_dense_objects<<<(unsigned)((nd * 32 + 255) / 256), 256, 0, c.stream>>>(
+          wa, nd, cell_start.get(), m, n, order, pts, dim, point_cell.get(), dbeg.get(), dlen.get(), objects.get());
+      SPB_LAUNCHED();
+    } else {
+      objects = DevBuf<float>((size_t)n * 2 * dim, c.stream);
+    }
+  }
+  // sparse points in index order
+  DevBuf<int32_t> sflag((size_t)n, c.stream);
+  DevBuf<int64_t> sscan((size_t)n + 1, c.stream);
+  k_sparse_flags<<<G, 256, 0, c.stream>>>(point_cell.get(), n, sflag.get());
+  SPB_LAUNCHED();
+  exclusive_scan(c, sflag.get(), n, sscan.get());
+  int64_t ns = 0;
+  SPB_CUDA(cudaMemcpyAsync(&ns, sscan.get() + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  num_dense_points = n - ns;
+  DevBuf<int32_t> sparse_pts((size_t)(ns > 0 ? ns : 1), c.stream);
+  k_sparse_objects<<<G, 256, 0, c.stream>>>(point_cell.get(), sscan.get(), n, nd, pts, dim, sparse_pts.get(),
+                                            objects.get());
+  SPB_LAUNCHED();
+  sflag.reset();
+  sscan.reset();
+  const int64_t nobj = nd + ns;
+  Tree t;
+  build_tree(c, objects.get(), nobj, dim, false, width, t);
+  SPB_CUDA(cudaEventRecord(ev[1], c.stream));
+
+  DenseView v{t.nodes, nobj, nd, dbeg.get(), dlen.get(), order, sparse_pts.get(), pts, dim, radius_threshold(eps)};
+  DevBuf<uint8_t> core((size_t)n, c.stream);
+  k_dense_core<<<G, 256, 0, c.stream>>>(point_cell.get(), n, core.get());
+  SPB_LAUNCHED();
+  const bool count_phase = min_pts > 2;
+  const unsigned Gq = (unsigned)((n + 127) / 128);
+  if (count_phase && ns > 0) {
+    k_db_core<<<Gq, 128, 0, c.stream>>>(v, order, n, point_cell.get(), min_pts, core.get());
+    SPB_LAUNCHED();
+  }
+  SPB_CUDA(cudaEventRecord(ev[2], c.stream));
+
+  DevBuf<int32_t> parent((size_t)n, c.stream);
+  DevBuf<uint32_t> claims(count_phase ? (size_t)((n + 31) / 32) : 0, c.stream);
+  DevBuf<unsigned long long> checks(1, c.stream);
+  SPB_CUDA(cudaMemsetAsync(checks.get(), 0, sizeof(unsigned long long), c.stream));
+  if (count_phase) SPB_CUDA(cudaMemsetAsync(claims.get(), 0, claims.n * sizeof(uint32_t), c.stream));
+  k_iota32<<<G, 256, 0, c.stream>>>(parent.get(), n);
+  SPB_LAUNCHED();
+  if (nd > 0) {
+    k_db_cell_unions<<<(unsigned)((nd * 32 + 255) / 256), 256, 0, c.stream>>>(dbeg.get(), dlen.get(), nd, order,
+                                                                              parent.get());
+    SPB_LAUNCHED();
+  }
+  if (count_phase)
+    k_db_merge<false><<<Gq, 128, 0, c.stream>>>(v, order, n, point_cell.get(), parent.get(), core.get(), claims.get(),
+                                                checks.get());
+  else
+    k_db_merge<true><<<Gq, 128, 0, c.stream>>>(v, order, n, point_cell.get(), parent.get(), core.get(), nullptr,
+                                               checks.get());
+  SPB_LAUNCHED();
+  SPB_CUDA(cudaEventRecord(ev[3], c.stream));
+  k_db_labels<<<G, 256, 0, c.stream>>>(n, parent.get(), core.get(), claims.get(), labels, core_out);
+  SPB_LAUNCHED();
+  SPB_CUDA(cudaEventRecord(ev[4], c.stream));
+  unsigned long long hchecks = 0;
+  SPB_CUDA(cudaMemcpyAsync(&hchecks, checks.get(), sizeof(hchecks), cudaMemcpyDeviceToHost, c.stream));
+  SPB_CUDA(cudaEventSynchronize(ev[4]));
+  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  if (res) {
+    for (int i = 0; i < 4; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      res->ms[i] = ms;
+    }
+    res->distance_checks = (int64_t)hchecks;
+    res->num_dense_cells = nd;
+    res->num_dense_points = num_dense_points;
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
 }
 
 }  // namespace spb

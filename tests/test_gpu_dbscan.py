@@ -1,0 +1,134 @@
+"""GPU: fdbscan / friends_of_friends parity (dbscan.hpp:229-292): FoF labels
+bit-identical to the reference; minPts > 2 core flags identical and clusters
+equivalent under the reference's check_equivalence contract (verify.hpp)."""
+import numpy as np
+import pytest
+
+from fixtures import dbscan_cases, golden_hashes, summarize
+from oracle_lib import eps_for, fnv1a64
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", list(dbscan_cases().keys()))
+def test_fdbscan_matches_reference_fixture(sp, oracle, name):
+    c = dbscan_cases()[name]
+    dim, min_pts = (int(v) for v in c["meta"])
+    eps = float(c["eps"])
+    out = sp.fdbscan(c["points"], sp.DbscanParams(eps, min_pts))
+    assert np.array_equal(out.core_flags, c["core"])
+    if min_pts == 2:
+        assert np.array_equal(out.labels, c["labels"])
+        fof = sp.friends_of_friends(c["points"], eps)
+        assert np.array_equal(fof.labels, c["labels"])
+    else:
+        assert oracle.check_equivalence(c["points"], dim, eps, (out.labels, out.core_flags),
+                                        (c["labels"], c["core"])) is None
+
+
+def test_fof_random_instances_match_oracle(sp, oracle):
+    rng = np.random.default_rng(21)
+    for trial in range(40):
+        dim = int(rng.choice([2, 3]))
+        n = int(rng.integers(1, 30000))
+        pts = rng.random((n, dim), dtype=np.float32)
+        if trial % 4 == 1:
+            pts = np.round(pts * 32) / 32
+        eps = float(rng.choice([0.002, 0.01, 0.03]))
+        width = int(rng.choice([32, 64]))
+        out = sp.friends_of_friends(pts, eps, width=width)
+        lab, core = oracle.dbscan(pts, dim, eps, 2)
+        assert np.array_equal(out.labels, lab) and np.array_equal(out.core_flags, core), trial
+
+
+def test_minpts_random_instances_equivalent(sp, oracle):
+    rng = np.random.default_rng(22)
+    for trial in range(25):
+        dim = int(rng.choice([2, 3]))
+        n = int(rng.integers(1, 20000))
+        centres = rng.random((8, dim))
+        pts = np.clip(centres[rng.integers(0, 8, n)] + rng.standard_normal((n, dim)) * 0.02, 0, 1).astype(np.float32)
+        eps = float(rng.choice([0.005, 0.01]))
+        mp = int(rng.choice([3, 4, 5, 10]))
+        out = sp.fdbscan(pts, sp.DbscanParams(eps, mp))
+        lab, core = oracle.dbscan(pts, dim, eps, mp)
+        assert np.array_equal(out.core_flags, core), trial
+        assert oracle.check_equivalence(pts, dim, eps, (out.labels, out.core_flags), (lab, core)) is None, trial
+
+
+def test_kats(sp):
+    # test_dbscan.cpp:55-81: lone point is noise; a close pair is one cluster;
+    # blob A..D + border E (through D) + noise F with min_pts 4
+    out = sp.fdbscan(np.array([[0.5, 0.5]], np.float32), sp.DbscanParams(0.1, 2))
+    assert out.labels.tolist() == [-1] and out.core_flags.tolist() == [0]
+    out = sp.fdbscan(np.array([[0.5, 0.5], [0.55, 0.5]], np.float32), sp.DbscanParams(0.1, 2))
+    assert out.labels.tolist() == [0, 0] and out.core_flags.tolist() == [1, 1]
+    blob = np.array([[0.50, 0.50], [0.52, 0.50], [0.50, 0.52], [0.59, 0.50], [0.68, 0.50], [0.95, 0.95]],
+                    np.float32)
+    for algo in (sp.fdbscan, sp.fdbscan_densebox):
+        out = algo(blob, sp.DbscanParams(0.1, 4))
+        assert out.core_flags.tolist() == [1, 1, 1, 1, 0, 0]
+        assert out.labels.tolist() == [0, 0, 0, 0, 0, -1]
+    # test_dbscan.cpp:284-293: chains connect, singletons are noise
+    chain = np.array([[i * 0.09, 0.0] for i in range(10)] + [[5.0, 5.0]], np.float32)
+    out = sp.friends_of_friends(chain, 0.1)
+    assert out.labels.tolist() == [0] * 10 + [-1]
+
+
+def test_parameter_validation(sp):
+    # test_dbscan.cpp:45-53
+    p = np.zeros((3, 3), np.float32)
+    for eps, mp in ((0.0, 2), (-1.0, 2), (float("inf"), 2), (float("nan"), 2), (0.1, 1)):
+        with pytest.raises(sp.InvalidArgument):
+            sp.fdbscan(p, sp.DbscanParams(eps, mp))
+    with pytest.raises(sp.InvalidArgument):
+        sp.friends_of_friends(np.array([[0, 0, np.nan]], np.float32), 0.1)
+
+
+def test_empty_and_tiny_eps(sp, oracle):
+    out = sp.fdbscan(np.zeros((0, 3), np.float32), sp.DbscanParams(0.1, 3))
+    assert len(out.labels) == 0
+    rng = np.random.default_rng(4)
+    p = rng.random((500, 3), dtype=np.float32)
+    p[100:110] = p[0]
+    out = sp.fdbscan(p, sp.DbscanParams(1e-30, 3))
+    lab, core = oracle.dbscan(p, 3, 1e-30, 3)
+    assert np.array_equal(out.core_flags, core)
+    assert oracle.check_equivalence(p, 3, 1e-30, (out.labels, out.core_flags), (lab, core)) is None
+
+
+def test_permutation_invariance(sp):
+    # test_dbscan.cpp:420-443: FoF labels map consistently under input permutation
+    rng = np.random.default_rng(6)
+    p = rng.random((20000, 3), dtype=np.float32)
+    perm = rng.permutation(len(p))
+    a = sp.friends_of_friends(p, 0.01).labels
+    b = sp.friends_of_friends(p[perm], 0.01).labels
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(len(p))
+    # same partition and noise set
+    assert np.array_equal(a[perm] == -1, b == -1)
+    ca = a[perm][b != -1]
+    cb = b[b != -1]
+    pairs = set(zip(ca.tolist(), cb.tolist()))
+    assert len(pairs) == len(set(ca.tolist())) == len(set(cb.tolist()))
+
+
+def test_repeatable_and_device_arrays(sp):
+    import torch
+    rng = np.random.default_rng(7)
+    p = rng.random((100000, 3), dtype=np.float32)
+    a = sp.friends_of_friends(p, 0.004)
+    d = torch.from_numpy(p).cuda()
+    b = sp.friends_of_friends(d, 0.004)
+    assert np.array_equal(a.labels, b.labels.cpu().numpy())
+    assert np.array_equal(a.core_flags, b.core_flags.cpu().numpy())
+
+
+def test_c1_labels_hash(sp, oracle):
+    g = golden_hashes()["C1"]
+    p = oracle.uniform(g["n"], 3, 1.0, g["seed"])
+    out = sp.friends_of_friends(p, eps_for(g["n"]))
+    assert fnv1a64(out.labels) == g["labels_hash"]
+    assert fnv1a64(out.core_flags) == g["core_hash"]
+    assert summarize(out.labels, out.core_flags) == (g["clusters"], g["noise"], g["core"])

@@ -1,0 +1,65 @@
+"""GPU, full BASELINE sizes: parity against the SURVEY §8(c) hashes of the
+unmodified reference at C2 (2^24 points + 2^24 range counts), C4 (2^24 x 2^24
+kNN, k = 16) and the C5 proxies (FoF on the 2^24 / 2^26 clustered field),
+plus size-independent properties at the bench size."""
+import numpy as np
+import pytest
+
+from fixtures import golden_hashes, summarize
+from oracle_lib import eps_for, fnv1a64
+
+pytestmark = pytest.mark.gpu
+
+
+def test_c2_leaf_perm_and_range_counts(sp, oracle):
+    g = golden_hashes()["C2"]
+    n = g["n"]
+    p = oracle.uniform(n, 3, 1.0, g["seed"])
+    r = np.float32(np.cbrt(30.0 / (n * 4.18879020478639)))
+    assert "%08x" % r.view(np.uint32) == g["radius_bits"]
+    b = sp.Bvh.build(p)
+    e = b.export()
+    assert fnv1a64(e["leaf_object"]) == g["leaf_perm"]
+    counts = sp.range_count(b, p, radius=float(r))
+    assert int(counts.sum()) == g["total_matches"]
+    assert fnv1a64(counts) == g["counts_hash"]
+
+
+def test_c4_knn(sp, oracle):
+    g = golden_hashes()["C4"]
+    n = g["n"]
+    p = oracle.uniform(n, 3, 1.0, g["seeds"][0])
+    q = oracle.uniform(n, 3, 1.0, g["seeds"][1])
+    idx, dist = sp.nearest_query(sp.Bvh.build(p), q, 16, with_distances=True)
+    assert fnv1a64(idx) == g["knn_idx"]
+    assert abs(float(dist[:, 15].astype(np.float64).mean()) - g["mean_16th_dist"]) < 1e-9
+
+
+@pytest.mark.parametrize("key", ["C5_2^24", "C5_2^26"])
+def test_c5_proxy_fof_labels(sp, oracle, key):
+    g = golden_hashes()[key]
+    n = g["n"]
+    p = oracle.field(n)
+    out = sp.friends_of_friends(p, eps_for(n))
+    assert summarize(out.labels, out.core_flags) == (g["clusters"], g["noise"], g["core"])
+    assert fnv1a64(out.core_flags) == g["core_hash"]
+    assert fnv1a64(out.labels) == g["labels_hash"]
+
+
+def test_bench_field_properties(sp):
+    # 2^27 points of the bench field: labels are canonical (label == min index
+    # of its cluster, a core point's label is a member <= itself), noise
+    # exactly the non-core points, and the run is repeatable.
+    import torch
+    n = 1 << 27
+    p = sp.generate_field(n, seed=2409)
+    eps = eps_for(n)
+    a = sp.friends_of_friends(p, eps)
+    lab = a.labels
+    core = a.core_flags.bool()
+    idx = torch.arange(n, device=lab.device, dtype=torch.int32)
+    assert bool(((lab == -1) == ~core).all())
+    assert bool((lab[core] <= idx[core]).all())
+    assert bool((lab[lab[core].long()] == lab[core]).all())  # the label point is its own cluster's root
+    b = sp.friends_of_friends(p, eps)
+    assert bool((a.labels == b.labels).all())
