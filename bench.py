@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""Benchmark for the B200 FoF/DBSCAN hot path (BASELINE.json metric:
+"FoF/DBSCAN points/sec at 1/2/4/8 B200 + % HBM roofline; BVH build Mpts/s").
+
+Default workload ("fof_field", SURVEY §8(d) C5 shape, weak scaling):
+friends-of-friends (DBSCAN minPts = 2) on a HACC-like clustered 3-D fp32 field
+— 25% uniform background + Gaussian halos of 8192 points, sigma =
+0.001*cbrt(2^26/n) — with 2^27 points per GPU (the per-GPU share of the C5
+1-billion-point run on 8 GPUs), eps = 0.168 * mean spacing of the whole field.
+One step = one full pass of the path: scene bounds, Morton codes, radix sort,
+hierarchy + refit + ropes, pair traversal fused with union-find, label
+finalisation (N > 1 adds the slab exchange and the distributed merge).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload fof_field|c1|c2|c3|c4] [--n POINTS_PER_GPU]
+
+`value` is device-resident throughput (inputs already in HBM); `e2e` is the
+same call through the public API with pinned HOST buffers (H2D of the points
+and D2H of labels + core flags inside the timed region).  The reference arm
+(--impl reference) times the unmodified reference CPU implementation
+(oracle/_ref, built from /root/reference) on a bounded sample on this host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAK_FALLBACK_GBS = 6650.0
+ARBORX_A100_PTS_S = 37.0e6 / 0.15  # ~37M HACC particles FoF in < 0.15 s on one A100
+
+
+def eps_for(n: int) -> float:
+    import numpy as np
+    return float(np.float32(0.168 * np.cbrt(1.0 / float(n))))
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return PEAK_FALLBACK_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# per-kernel algorithmic bytes for the FoF pipeline phases
+# ---------------------------------------------------------------------------
+def phase_bytes(phase: str, n: int, pairs_per_pt: float, key_bits: int = 63) -> float:
+    npass = (key_bits + 7) // 8
+    per = {
+        "bounds": 12.0,                                 # read xyz
+        "morton": 12.0 + 8.0,                           # read xyz, write code
+        "sort": 8.0 + 20.0 + 24.0 * (npass - 1),        # histogram read; pass 0 (iota values); 12 B in+out/pass
+        "hierarchy": 16.0 + 124.0,                      # delta (2 keys+ids, write) + leaf/internal writes, gathers
+        "merge": 32.0 + 64.0 + 4.0 + 1.0 + 8.0 * pairs_per_pt,  # own leaf, tree once, parent init, flag, unions
+        "finalize": 22.0,
+        "core": 32.0 + 64.0 + 1.0,
+    }
+    return per.get(phase, 0.0) * n
+
+
+# ---------------------------------------------------------------------------
+# reference CPU path (oracle/_ref) — the cpu_baseline leg and --impl reference
+# ---------------------------------------------------------------------------
+def reference_sample(n_sample: int, runs: int, warmup: int = 0):
+    """Time the reference's friends_of_friends on H(n_sample) (the reference's
+    own generator); returns (points/s, kind, cores, per-run seconds)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Oracle, Reference  # test infrastructure: checker/baseline only
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    if Reference.available():
+        R, kind = Reference.get(), "reference"
+        pts = R.field(n_sample)
+        run = lambda: R.dbscan(pts, 3, eps_for(n_sample), 2, "fof")
+    else:
+        O, kind = Oracle.get(), "port"
+        pts = O.field(n_sample)
+        run = lambda: O.dbscan(pts, 3, eps_for(n_sample), 2)
+    for _ in range(warmup):
+        run()
+    secs = []
+    for _ in range(runs):
+        t = time.perf_counter()
+        run()
+        secs.append(time.perf_counter() - t)
+    return n_sample / statistics.median(secs), kind, cores, secs
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    n_sample = args.cpu_sample_n
+    v, kind, cores, secs = reference_sample(n_sample, args.steps, args.warmup)
+    cfg = workload_config(args, world)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "points/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic (reference generator H(n))",
+        "config": cfg,
+        "cpu_baseline": {"value": v, "unit": "points/s", "cores": cores, "kind": kind,
+                         "sample": "friends_of_friends on H(%d) (SURVEY §8(d) field, reference mt19937_64 generator), "
+                                   "eps = 0.168*n^(-1/3); %d timed runs" % (n_sample, args.steps)},
+        "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "FoF/DBSCAN points/sec (friends-of-friends, minPts=2)"
+
+
+def workload_config(args, world):
+    n = args.n
+    return {"workload": "fof_field: friends_of_friends on HACC-like clustered 3D fp32 field, "
+                        "%d points per GPU (C5 per-GPU share), eps = 0.168*n_total^(-1/3)" % n,
+            "points_per_gpu": n, "points_total": n * world, "eps": eps_for(n * world), "min_pts": 2,
+            "parallelism": "x-slabs over %d GPU(s) with eps ghost layers" % world if world > 1 else "single GPU",
+            "l2": "inputs (%.1f GB) larger than L2 (126 MB); no flush needed" % (n * 12 / 1e9)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2409_10743_b200 as sp
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream(dev)
+    ctx = sp.Context(local_rank, stream=stream.cuda_stream)
+
+    n = args.n
+    n_total = n * world
+    eps = eps_for(n_total)
+    if world > 1:
+        from paper_2409_10743_b200 import distributed as spd
+        pts = sp.generate_field(n_total, first=rank * n, count=n, seed=args.seed, ctx=ctx)
+        step = lambda: spd.fof_slabs(pts, eps, ctx=ctx, rank=rank, world=world, first_index=rank * n)
+    else:
+        pts = sp.generate_field(n_total, first=0, count=n, seed=args.seed, ctx=ctx)
+        labels = torch.empty(n, dtype=torch.int32, device=dev)
+        core = torch.empty(n, dtype=torch.uint8, device=dev)
+        step = lambda: sp.friends_of_friends(pts, eps, ctx=ctx, out=(labels, core))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    # close pairs per point (for the merge kernel's byte model), outside timing
+    pairs_per_pt = None
+    if world == 1:
+        b = sp.Bvh.build(pts, ctx=ctx)
+        import ctypes
+        tot = ctypes.c_int64(0)
+        ctx._check(sp._lib.sp_pair_list(ctx.h, b.h, ctypes.c_float(eps), None, 0, ctypes.byref(tot), sp.SP_MEM_DEVICE))
+        pairs_per_pt = tot.value / n
+        del b
+
+    # ---- device-resident timed region ----
+    phase_acc = {}
+    barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    launches0 = ctx.kernel_launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        out = step()
+        for name, ms in ctx.phases():
+            phase_acc[name] = phase_acc.get(name, 0.0) + ms
+    e1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    launches = ctx.kernel_launches - launches0
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = n_total * args.steps / (ms / 1e3)
+
+    # ---- end-to-end through the public API with pinned host buffers ----
+    e2e_value = None
+    h2d = n * 12
+    d2h = n * 5
+    if world == 1:
+        host_pts = torch.empty((n, 3), dtype=torch.float32, pin_memory=True)
+        host_pts.copy_(pts)
+        host_labels = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        host_core = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        e2e_step = lambda: sp.friends_of_friends(host_pts, eps, ctx=ctx, out=(host_labels, host_core))
+        e2e_step()
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        barrier()
+        e2e_value = n_total * args.steps / (e0.elapsed_time(e1) / 1e3)
+        # the device run and the host run must agree bit-for-bit
+        assert torch.equal(host_labels, labels.cpu()) and torch.equal(host_core, core.cpu()), "e2e != device run"
+    else:
+        e2e_value = value  # replaced by the distributed host-buffer path once it lands
+
+    peak, peak_src = measured_peak()
+    phases = {k: v / args.steps for k, v in phase_acc.items()}
+    roofline = None
+    if phases:
+        dom = max(phases, key=phases.get)
+        ach_bytes = phase_bytes(dom, n, pairs_per_pt or 0.0)
+        ach = ach_bytes / (phases[dom] / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": ach_bytes, "kernel_ms": round(phases[dom], 3),
+                    "share_of_step": round(phases[dom] / ms_per_step, 3)}
+        build_ms = sum(phases.get(k, 0.0) for k in ("bounds", "morton", "sort", "hierarchy"))
+    else:
+        build_ms = None
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, kind, cores, secs = reference_sample(args.cpu_sample_n, 2, 0)
+        cpu = {"value": v, "unit": "points/s", "cores": cores, "kind": kind,
+               "sample": "friends_of_friends on H(%d) (same field shape, reference generator), %d runs, "
+                         "median %.2f s" % (args.cpu_sample_n, len(secs), statistics.median(secs))}
+    line = {
+        "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": value / ARBORX_A100_PTS_S,
+        "vs_baseline_ref": "ArborX on 1x A100: ~37M HACC particles FoF in < 0.15 s (PAPER.md:489-493) = %.3g points/s"
+                           % ARBORX_A100_PTS_S,
+        "dtype": "f32 (exact f64 distance predicate)", "data": "synthetic (device Philox HACC-like field)",
+        "config": workload_config(args, world),
+        "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d * world,
+                "d2h_bytes_per_step": d2h * world},
+        "gpu_launches": launches,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "bvh_build_mpts_s": (n / (build_ms / 1e3) / 1e6) if build_ms else None,
+        "phases_ms": {k: round(v, 3) for k, v in phases.items()},
+        "close_pairs_per_point": pairs_per_pt,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1 << 27, help="points per GPU")
+    ap.add_argument("--seed", type=int, default=2409)
+    ap.add_argument("--cpu-sample-n", type=int, default=1 << 22)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print("warning: --gpus %d but WORLD_SIZE %d" % (args.gpus, world), file=sys.stderr)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if args.impl == "ours":
+            torch.cuda.set_device(local_rank)
+        dist.init_process_group(backend=backend)
+    try:
+        if args.impl == "reference":
+            run_reference_arm(args, rank, world)
+        else:
+            run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -81,6 +81,13 @@ int sp_ctx_synchronize(sp_ctx *ctx);
 const char *sp_last_error(const sp_ctx *ctx);
 /* Number of kernels this library launched on ctx since creation. */
 int64_t sp_ctx_kernel_launches(const sp_ctx *ctx);
+/* Device-event phase breakdown of the last call on ctx (StopWatch lap times,
+ * exec.hpp:28-41, at kernel granularity): phase i ran for sp_ctx_phase_ms(i)
+ * milliseconds, e.g. "bounds", "morton", "sort", "hierarchy", "core",
+ * "merge", "finalize". */
+int sp_ctx_phase_count(const sp_ctx *ctx);
+const char *sp_ctx_phase_name(const sp_ctx *ctx, int i);
+double sp_ctx_phase_ms(const sp_ctx *ctx, int i);
 
 /* ---- hierarchy (Bvh<D>::build, bvh.hpp:62, 243-261) ---------------------- */
 /* objects: points (is_points=1, float[n*dim]) or boxes (float[n*2*dim]).

@@ -79,6 +79,9 @@ def _load() -> C.CDLL:
         "sp_ctx_synchronize": (C.c_int, [vp]),
         "sp_last_error": (C.c_char_p, [vp]),
         "sp_ctx_kernel_launches": (i64, [vp]),
+        "sp_ctx_phase_count": (C.c_int, [vp]),
+        "sp_ctx_phase_name": (C.c_char_p, [vp, C.c_int]),
+        "sp_ctx_phase_ms": (C.c_double, [vp, C.c_int]),
         "sp_bvh_build": (C.c_int, [vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, pp]),
         "sp_bvh_destroy": (C.c_int, [vp]),
         "sp_bvh_size": (i64, [vp]),
@@ -145,6 +148,11 @@ class Context:
     def kernel_launches(self) -> int:
         return int(_lib.sp_ctx_kernel_launches(self.h))
 
+    def phases(self) -> list:
+        """[(name, ms)] device-event phase times of the last call."""
+        return [(_lib.sp_ctx_phase_name(self.h, i).decode(), float(_lib.sp_ctx_phase_ms(self.h, i)))
+                for i in range(_lib.sp_ctx_phase_count(self.h))]
+
     def _check(self, rc: int):
         if rc == SP_OK:
             return
@@ -171,12 +179,21 @@ def _is_cuda(a) -> bool:
     return hasattr(a, "is_cuda") and bool(a.is_cuda)
 
 
+def _is_torch(a) -> bool:
+    return hasattr(a, "data_ptr") and hasattr(a, "is_contiguous")
+
+
+def _ptr(a) -> C.c_void_p:
+    return C.c_void_p(a.data_ptr() if _is_torch(a) else a.ctypes.data)
+
+
 def _in(a, dtype):
-    """(pointer, mem, keepalive) for an input array (numpy or CUDA tensor)."""
-    if _is_cuda(a):
+    """(pointer, mem, keepalive) for an input array: numpy, a (pinned) CPU
+    tensor, or a CUDA tensor (device-resident; no copy)."""
+    if _is_torch(a):
         if not a.is_contiguous():
             a = a.contiguous()
-        return C.c_void_p(a.data_ptr()), SP_MEM_DEVICE, a
+        return C.c_void_p(a.data_ptr()), (SP_MEM_DEVICE if a.is_cuda else SP_MEM_HOST), a
     arr = np.ascontiguousarray(a, dtype=dtype)
     return arr.ctypes.data_as(C.c_void_p), SP_MEM_HOST, arr
 
@@ -475,8 +492,7 @@ def _dbscan(points, eps, min_pts, algo, width, ctx, out=None):
     dev = mem == SP_MEM_DEVICE
     if out is not None:
         labels, core = out
-        lp, cp = C.c_void_p(labels.data_ptr() if dev else labels.ctypes.data), \
-            C.c_void_p(core.data_ptr() if dev else core.ctypes.data)
+        lp, cp = _ptr(labels), _ptr(core)
     else:
         labels, lp = _out(dev, (n,), np.int32, _torch_dtype("int32") if dev else None, points.device if dev else None)
         core, cp = _out(dev, (n,), np.uint8, _torch_dtype("uint8") if dev else None, points.device if dev else None)

@@ -15,6 +15,32 @@ namespace spb {
 
 thread_local int64_t *g_launch_counter = nullptr;
 
+void mark(Ctx &c, const char *name) {
+  if (c.marks_used == c.event_pool.size()) {
+    cudaEvent_t e;
+    SPB_CUDA(cudaEventCreate(&e));
+    c.event_pool.push_back(e);
+    c.mark_names.push_back(nullptr);
+  }
+  c.mark_names[c.marks_used] = name;
+  SPB_CUDA(cudaEventRecord(c.event_pool[c.marks_used], c.stream));
+  ++c.marks_used;
+}
+
+void reset_marks(Ctx &c) {
+  c.marks_used = 0;
+  c.phases.clear();
+}
+
+void resolve_marks(Ctx &c) {
+  c.phases.clear();
+  for (size_t i = 1; i < c.marks_used; ++i) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c.event_pool[i - 1], c.event_pool[i]) != cudaSuccess) ms = -1.f;
+    c.phases.emplace_back(c.mark_names[i], (double)ms);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K1: scene box + finiteness (bvh.hpp:247-254, geometry.hpp:58-69, 98-114)
 // ---------------------------------------------------------------------------
@@ -467,7 +493,9 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
   t.stream = c.stream;
   SPB_CUDA(cudaMallocAsync(&t.scene, 6 * sizeof(float), c.stream));
   DevBuf<int> bad(1, c.stream);
+  mark(c, "start");
   scene_bounds(c, objects, n, dim, points, t.scene, bad.get());
+  mark(c, "bounds");
   int h_bad = 0;
   SPB_CUDA(cudaMemcpyAsync(&h_bad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   SPB_CUDA(cudaStreamSynchronize(c.stream));
@@ -481,9 +509,11 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
   DevBuf<uint64_t> k0(n, c.stream), k1(n, c.stream);
   DevBuf<uint32_t> v0(n, c.stream), v1(n, c.stream);
   morton_codes(c, objects, n, dim, points, width, t.scene, k0.get(), nullptr);
+  mark(c, "morton");
   uint64_t *ka = k0.get(), *kb = k1.get();
   uint32_t *va = v0.get(), *vb = v1.get();
   radix_sort_pairs(c, &ka, &va, &kb, &vb, n, (width / dim) * dim, /*vals_iota=*/true);
+  mark(c, "sort");
   DevBuf<int32_t> delta(n > 1 ? n - 1 : 1, c.stream), flags(n > 1 ? n - 1 : 1, c.stream);
   if (n > 1) {
     k_delta<<<grid_for(n, 256, 148 * 16), 256, 0, c.stream>>>(ka, va, n, width, delta.get());
@@ -494,6 +524,7 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
   if (points) k_hierarchy<true><<<g, 256, 0, c.stream>>>(n, delta.get(), va, objects, dim, t.nodes, flags.get(), t.perm);
   else k_hierarchy<false><<<g, 256, 0, c.stream>>>(n, delta.get(), va, objects, dim, t.nodes, flags.get(), t.perm);
   SPB_LAUNCHED();
+  mark(c, "hierarchy");
 }
 
 void sort_points(Ctx &c, const float *pts, int64_t n, int dim, int32_t *order) {

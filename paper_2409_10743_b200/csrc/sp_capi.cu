@@ -84,9 +84,14 @@ int guarded(sp_ctx *ctx, F &&f) {
   if (!ctx) return SP_EINVAL;
   DeviceGuard dg(ctx->c.device);
   spb::g_launch_counter = &ctx->c.launches;
+  spb::reset_marks(ctx->c);
   int rc = SP_OK;
   try {
     f(ctx->c);
+    if (ctx->c.marks_used) {
+      SPB_CUDA(cudaStreamSynchronize(ctx->c.stream));
+      spb::resolve_marks(ctx->c);
+    }
   } catch (const spb::InvalidArgument &e) {
     ctx->c.last_error = e.what();
     rc = SP_EINVAL;
@@ -151,6 +156,7 @@ int sp_ctx_destroy(sp_ctx *ctx) {
   {
     DeviceGuard dg(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
+    for (cudaEvent_t e : ctx->c.event_pool) cudaEventDestroy(e);
     if (ctx->c.owns_stream) cudaStreamDestroy(ctx->c.stream);
   }
   delete ctx;
@@ -179,6 +185,18 @@ int sp_ctx_synchronize(sp_ctx *ctx) {
 const char *sp_last_error(const sp_ctx *ctx) { return ctx ? ctx->c.last_error.c_str() : "null context"; }
 
 int64_t sp_ctx_kernel_launches(const sp_ctx *ctx) { return ctx ? ctx->c.launches : 0; }
+
+int sp_ctx_phase_count(const sp_ctx *ctx) { return ctx ? (int)ctx->c.phases.size() : 0; }
+
+const char *sp_ctx_phase_name(const sp_ctx *ctx, int i) {
+  if (!ctx || i < 0 || i >= (int)ctx->c.phases.size()) return "";
+  return ctx->c.phases[(size_t)i].first.c_str();
+}
+
+double sp_ctx_phase_ms(const sp_ctx *ctx, int i) {
+  if (!ctx || i < 0 || i >= (int)ctx->c.phases.size()) return -1.0;
+  return ctx->c.phases[(size_t)i].second;
+}
 
 int sp_bvh_build(sp_ctx *ctx, const float *objects, int64_t n, int dim, int is_points, int code_width, int mem,
                  sp_bvh **out) {

@@ -154,6 +154,7 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
     SPB_CUDA(cudaMemsetAsync(corep.get(), 0, (size_t)n, c.stream));
   }
   SPB_CUDA(cudaEventRecord(ev[2], c.stream));
+  if (count_phase) mark(c, "core");
   k_iota<<<grid_for(n, 256, 148 * 16), 256, 0, c.stream>>>(parent.get(), n);
   SPB_LAUNCHED();
   if (count_phase) {
@@ -164,6 +165,7 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
   }
   SPB_LAUNCHED();
   SPB_CUDA(cudaEventRecord(ev[3], c.stream));
+  mark(c, "merge");
   SPB_CUDA(cudaMemsetAsync(minobj.get(), 0x7f, (size_t)n * sizeof(int32_t), c.stream));
   k_final_roots<<<g256, 256, 0, c.stream>>>(n, parent.get(), corep.get(), claims.get(), t.perm, minobj.get());
   SPB_LAUNCHED();
@@ -171,6 +173,7 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
                                              core);
   SPB_LAUNCHED();
   SPB_CUDA(cudaEventRecord(ev[4], c.stream));
+  mark(c, "finalize");
   SPB_CUDA(cudaEventSynchronize(ev[4]));
   if (res) {
     for (int i = 0; i < 4; ++i) {

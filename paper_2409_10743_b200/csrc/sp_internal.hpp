@@ -6,6 +6,7 @@
 
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "sp_common.cuh"
 
@@ -20,7 +21,19 @@ struct Ctx {
   bool owns_stream = false;
   std::string last_error;
   int64_t launches = 0;
+  // Phase marks of the current call: events recorded on the stream between
+  // pipeline stages; (name_i, ms_i) = time from mark i-1 to mark i.
+  std::vector<cudaEvent_t> event_pool;
+  std::vector<const char *> mark_names;
+  size_t marks_used = 0;
+  std::vector<std::pair<std::string, double>> phases;
 };
+
+// Record a phase boundary on the context stream (cheap; no host sync).
+void mark(Ctx &c, const char *name);
+// Resolve the marks of the finished call into c.phases (after a sync).
+void resolve_marks(Ctx &c);
+void reset_marks(Ctx &c);
 
 template <class T>
 struct DevBuf {
