@@ -428,33 +428,14 @@ struct HierView {
   }
 };
 
-// Thread p writes leaf p, then climbs: the first child to arrive at a parent
-// records its far bound in flags[split] and stops; the second knows the
-// parent's full range [l, r] and split, recovers its Karras index (r for a
-// left child, l for a right child, 0 for the root), joins the two child boxes
-// left-first and writes {box, left, rope}.
-template <bool POINTS>
-__global__ void __launch_bounds__(256) k_hierarchy(int64_t n, const int32_t *__restrict__ delta,
-                                                   const uint32_t *__restrict__ perm, const float *__restrict__ obj,
-                                                   int dim, float4 *nodes, int32_t *flags,
-                                                   int32_t *__restrict__ perm_out) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  HierView H{n, delta};
-  const uint32_t oi = perm[p];
-  perm_out[p] = (int32_t)oi;
-  const int sz = POINTS ? dim : 2 * dim;
-  const float *o = obj + (int64_t)oi * sz;
-  float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f};
-  for (int k = 0; k < dim; ++k) {
-    lo[k] = o[k];
-    hi[k] = POINTS ? lo[k] : o[dim + k];
-  }
-  const int64_t leaf = n - 1 + p;
-  nodes[2 * leaf] = make_float4(lo[0], lo[1], lo[2], __int_as_float((int)oi));
-  nodes[2 * leaf + 1] = make_float4(hi[0], hi[1], hi[2], __int_as_float(H.rope(p)));
-  if (n == 1) return;
-
+// The climb from leaf p (leaf box in lo/hi, already written): the first child
+// to arrive at a parent records its far bound in flags[split] and stops; the
+// second knows the parent's full range [l, r] and split, recovers its Karras
+// index (r for a left child, l for a right child, 0 for the root), joins the
+// two child boxes left-first and writes {box, left, rope}.
+__device__ __forceinline__ void climb(const HierView &H, int64_t p, float lo[3], float hi[3], float4 *nodes,
+                                      int32_t *flags) {
+  const int64_t n = H.n;
   int64_t l = p, r = p;
   while (true) {
     const bool L = H.is_left(l, r);
@@ -485,6 +466,32 @@ __global__ void __launch_bounds__(256) k_hierarchy(int64_t n, const int32_t *__r
   }
 }
 
+template <bool POINTS>
+__global__ void __launch_bounds__(256) k_hierarchy(int64_t n, const int32_t *__restrict__ delta,
+                                                   const uint32_t *__restrict__ perm, const float *__restrict__ obj,
+                                                   int dim, float4 *nodes, int32_t *flags,
+                                                   int32_t *__restrict__ perm_out, float4 *__restrict__ leafpt) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  HierView H{n, delta};
+  const uint32_t oi = perm[p];
+  perm_out[p] = (int32_t)oi;
+  const int sz = POINTS ? dim : 2 * dim;
+  const float *o = obj + (int64_t)oi * sz;
+  float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f};
+  for (int k = 0; k < dim; ++k) {
+    lo[k] = o[k];
+    hi[k] = POINTS ? lo[k] : o[dim + k];
+  }
+  const int64_t leaf = n - 1 + p;
+  nodes[2 * leaf] = make_float4(lo[0], lo[1], lo[2], __int_as_float((int)oi));
+  const int32_t leaf_rope = H.rope(p);
+  nodes[2 * leaf + 1] = make_float4(hi[0], hi[1], hi[2], __int_as_float(leaf_rope));
+  if (POINTS) leafpt[p] = make_float4(lo[0], lo[1], lo[2], __int_as_float(leaf_rope));
+  if (n == 1) return;
+  climb(H, p, lo, hi, nodes, flags);
+}
+
 void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, int width, Tree &t) {
   t.n = n;
   t.dim = dim;
@@ -505,6 +512,7 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
   const int64_t num_nodes = 2 * n - 1;
   SPB_CUDA(cudaMallocAsync(&t.nodes, (size_t)num_nodes * 2 * sizeof(float4), c.stream));
   SPB_CUDA(cudaMallocAsync(&t.perm, (size_t)n * sizeof(int32_t), c.stream));
+  if (points) SPB_CUDA(cudaMallocAsync(&t.leafpt, (size_t)n * sizeof(float4), c.stream));
 
   DevBuf<uint64_t> k0(n, c.stream), k1(n, c.stream);
   DevBuf<uint32_t> v0(n, c.stream), v1(n, c.stream);
@@ -521,8 +529,12 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
     SPB_CUDA(cudaMemsetAsync(flags.get(), 0xff, (size_t)(n - 1) * sizeof(int32_t), c.stream));
   }
   unsigned g = (unsigned)((n + 255) / 256);
-  if (points) k_hierarchy<true><<<g, 256, 0, c.stream>>>(n, delta.get(), va, objects, dim, t.nodes, flags.get(), t.perm);
-  else k_hierarchy<false><<<g, 256, 0, c.stream>>>(n, delta.get(), va, objects, dim, t.nodes, flags.get(), t.perm);
+  if (points)
+    k_hierarchy<true><<<g, 256, 0, c.stream>>>(n, delta.get(), va, objects, dim, t.nodes, flags.get(), t.perm,
+                                               t.leafpt);
+  else
+    k_hierarchy<false><<<g, 256, 0, c.stream>>>(n, delta.get(), va, objects, dim, t.nodes, flags.get(), t.perm,
+                                                nullptr);
   SPB_LAUNCHED();
   mark(c, "hierarchy");
 }

@@ -2,9 +2,11 @@
 // fused with lock-free union-find (K6), capped core counting (K5 with early
 // termination), the border claim latch, and label finalisation (K7).
 // Reference: dbscan.hpp:72-292, union_find.hpp:17-82, traversal.hpp:162-184.
+//
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "sp_common.cuh"
@@ -14,70 +16,100 @@
 
 namespace spb {
 
-// Union-find lives in LEAF-POSITION space: leaf p's neighbours in Morton order
-// are its neighbours in memory, so parent[] accesses stay local.  Canonical
-// labels (the smallest ORIGINAL index of each set, finalize_labels,
-// dbscan.hpp:72-98) are recovered in the finalisation pass.
+// Union-find lives in SORTED-POSITION space: Morton neighbours are memory
+// neighbours, so parent[] accesses stay local.  Canonical labels (the smallest
+// ORIGINAL index of each set, finalize_labels, dbscan.hpp:72-98) are recovered
+// in the finalisation pass.
 
 __global__ void k_iota(int32_t *a, int64_t n) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) a[i] = (int32_t)i;
 }
 
-// Capped neighbour counts for every point (detect_core_counts,
-// dbscan.hpp:146-182); queries run in leaf order, which is the order
-// sort_queries gives the same points (traversal.hpp:209-218).
-__global__ void __launch_bounds__(128) k_core_flags(const float4 *__restrict__ nodes, int64_t n, double thr,
+// Capped neighbour counts (detect_core_counts, dbscan.hpp:146-182); queries
+// run in leaf order, which is the order sort_queries gives the same points
+// (traversal.hpp:209-218).  Counts include the point itself and stop at
+// min_pts, so count = min(hits, min_pts) whatever the visiting order.
+__global__ void __launch_bounds__(128) k_core_flags(const float4 *__restrict__ nodes,
+                                                    const float4 *__restrict__ leafpt, int64_t n, Radius R,
                                                     int32_t min_pts, uint8_t *__restrict__ corep) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
-  const float4 me = ld_node(nodes, 2 * (n - 1 + p));
-  corep[p] = count_sphere(nodes, n, me.x, me.y, me.z, thr, min_pts) >= min_pts;
+  const float4 me = ld_node(leafpt, p);
+  corep[p] = count_sphere(nodes, leafpt, n, me.x, me.y, me.z, R, min_pts) >= min_pts;
 }
 
-// Pair traversal fused with the merge rule.  FOF: every close pair unions and
-// marks both ends as having a partner (core <=> set size > 1,
+// The merge rule for one close pair (p's leaf precedes q's).  FOF: every
+// close pair unions (core <=> set size > 1 is derived at finalisation,
 // dbscan.hpp:102-110, 259-263).  Otherwise merge_close_pair
 // (dbscan.hpp:123-137): core-core unions; core-noncore unions iff the
 // non-core side wins its one-shot claim latch (union_find.hpp:63-82).
+// root_p is a hint for p's root: if q already points at it the pair is in one
+// set (true even for a stale hint, which is still a member of p's set), else a
+// union costs one find on q.
 template <bool FOF>
-__global__ void __launch_bounds__(128) k_merge_pairs(const float4 *__restrict__ nodes, int64_t n, double thr,
-                                                     int32_t *parent, uint8_t *corep, uint32_t *claims) {
+__device__ __forceinline__ void merge_pair(int32_t p, int32_t q, bool core_p, int32_t &root_p, int32_t *parent,
+                                           const uint8_t *corep, uint32_t *claims) {
+  if (FOF) {
+    if (parent[q] == root_p) return;
+    root_p = uf_union(parent, root_p, q);
+    return;
+  }
+  const bool core_q = corep[q] != 0;
+  if (core_p && core_q) {
+    if (parent[q] == root_p) return;
+    root_p = uf_union(parent, root_p, q);
+  } else if (core_p || core_q) {
+    const int32_t b = core_p ? q : p;  // the non-core side
+    const uint32_t bit = 1u << (b & 31);
+    if (!(atomicOr(&claims[b >> 5], bit) & bit)) root_p = uf_union(parent, root_p, q);
+  }
+}
+
+// Pair traversal fused with the merge rule (traversal.hpp:162-184 +
+// dbscan.hpp:252-263): leaf p walks the ropes from its own rope, so only later
+// leaves are examined and each close pair is seen exactly once.  Leaves are
+// read as one 16-byte {x,y,z,rope}; internal nodes take the conservative
+// fp32 test, leaves the exact one.
+template <bool FOF>
+__global__ void __launch_bounds__(128) k_merge_pairs(const float4 *__restrict__ nodes,
+                                                     const float4 *__restrict__ leafpt, int64_t n, Radius R,
+                                                     int32_t *parent, const uint8_t *__restrict__ corep,
+                                                     uint32_t *claims) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int64_t first_leaf = n - 1;
-  const float4 me = ld_node(nodes, 2 * (first_leaf + p));
-  int32_t cur = node_rope(ld_node(nodes, 2 * (first_leaf + p) + 1));
-  bool any = false;
+  const float4 me = ld_node(leafpt, p);
+  int32_t cur = __float_as_int(me.w);
+  int32_t root_p = (int32_t)p;
   const bool core_p = FOF ? true : corep[p] != 0;
   while (cur != kSentinel) {
-    const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
-    const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
-    const bool hit = gap2(me.x, me.y, me.z, lo, hi) <= thr;
     if (cur >= first_leaf) {
-      if (hit) {
-        const int32_t q = (int32_t)(cur - first_leaf);
-        if (FOF) {
-          uf_union(parent, (int32_t)p, q);
-          corep[q] = 1;
-          any = true;
-        } else {
-          const bool core_q = corep[q] != 0;
-          if (core_p && core_q) {
-            uf_union(parent, (int32_t)p, q);
-          } else if (core_p || core_q) {
-            const int32_t b = core_p ? q : (int32_t)p;  // the non-core side
-            const uint32_t bit = 1u << (b & 31);
-            if (!(atomicOr(&claims[b >> 5], bit) & bit)) uf_union(parent, (int32_t)p, q);
-          }
-        }
-      }
-      cur = node_rope(hi);
+      const int32_t q = (int32_t)(cur - first_leaf);
+      const float4 L = ld_node(leafpt, q);
+      if (hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z))
+        merge_pair<FOF>((int32_t)p, q, core_p, root_p, parent, corep, claims);
+      cur = __float_as_int(L.w);
     } else {
-      cur = hit ? node_link(lo) : node_rope(hi);
+      const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
+      const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+      cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
     }
   }
-  if (FOF && any) corep[p] = 1;
+}
+
+// FoF core flags: a point is core iff its set has another member, i.e. it is
+// not a root, or it is a root somebody points at (mark_core_by_set_size,
+// dbscan.hpp:102-110).  Compresses every point to its root.
+__global__ void __launch_bounds__(256) k_fof_core(int64_t n, int32_t *parent, uint8_t *corep) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int32_t r = uf_root(parent, (int32_t)p);
+  if (r != p) {
+    parent[p] = r;
+    corep[p] = 1;
+    corep[r] = 1;
+  }
 }
 
 __device__ __forceinline__ bool is_member(const uint8_t *corep, const uint32_t *claims, int64_t p) {
@@ -132,40 +164,50 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
   }
   cudaEvent_t ev[5];
   for (auto &e : ev) SPB_CUDA(cudaEventCreate(&e));
+  struct EvGuard {
+    cudaEvent_t *e;
+    ~EvGuard() {
+      for (int i = 0; i < 5; ++i) cudaEventDestroy(e[i]);
+    }
+  } guard{ev};
   SPB_CUDA(cudaEventRecord(ev[0], c.stream));
   Tree t;
   try {
     build_tree(c, points, n, dim, true, width, t);
   } catch (const InvalidArgument &) {
-    for (auto &e : ev) cudaEventDestroy(e);
     throw InvalidArgument("dbscan: non-finite coordinate");
   }
   SPB_CUDA(cudaEventRecord(ev[1], c.stream));
-  const double thr = radius_threshold(eps);
+  const Radius R = make_radius(eps);
   const bool count_phase = min_pts > 2;
   const unsigned g128 = (unsigned)((n + 127) / 128), g256 = (unsigned)((n + 255) / 256);
   DevBuf<uint8_t> corep((size_t)n, c.stream);
   DevBuf<int32_t> parent((size_t)n, c.stream), minobj((size_t)n, c.stream);
   DevBuf<uint32_t> claims(count_phase ? (size_t)((n + 31) / 32) : 0, c.stream);
   if (count_phase) {
-    k_core_flags<<<g128, 128, 0, c.stream>>>(t.nodes, n, thr, min_pts, corep.get());
+    k_core_flags<<<g128, 128, 0, c.stream>>>(t.nodes, t.leafpt, n, R, min_pts, corep.get());
     SPB_LAUNCHED();
+    mark(c, "core");
   } else {
     SPB_CUDA(cudaMemsetAsync(corep.get(), 0, (size_t)n, c.stream));
   }
   SPB_CUDA(cudaEventRecord(ev[2], c.stream));
-  if (count_phase) mark(c, "core");
   k_iota<<<grid_for(n, 256, 148 * 16), 256, 0, c.stream>>>(parent.get(), n);
   SPB_LAUNCHED();
   if (count_phase) {
     SPB_CUDA(cudaMemsetAsync(claims.get(), 0, claims.n * sizeof(uint32_t), c.stream));
-    k_merge_pairs<false><<<g128, 128, 0, c.stream>>>(t.nodes, n, thr, parent.get(), corep.get(), claims.get());
+    k_merge_pairs<false><<<g128, 128, 0, c.stream>>>(t.nodes, t.leafpt, n, R, parent.get(), corep.get(),
+                                                     claims.get());
   } else {
-    k_merge_pairs<true><<<g128, 128, 0, c.stream>>>(t.nodes, n, thr, parent.get(), corep.get(), nullptr);
+    k_merge_pairs<true><<<g128, 128, 0, c.stream>>>(t.nodes, t.leafpt, n, R, parent.get(), corep.get(), nullptr);
   }
   SPB_LAUNCHED();
   SPB_CUDA(cudaEventRecord(ev[3], c.stream));
   mark(c, "merge");
+  if (!count_phase) {
+    k_fof_core<<<g256, 256, 0, c.stream>>>(n, parent.get(), corep.get());
+    SPB_LAUNCHED();
+  }
   SPB_CUDA(cudaMemsetAsync(minobj.get(), 0x7f, (size_t)n * sizeof(int32_t), c.stream));
   k_final_roots<<<g256, 256, 0, c.stream>>>(n, parent.get(), corep.get(), claims.get(), t.perm, minobj.get());
   SPB_LAUNCHED();
@@ -182,12 +224,6 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
       res->ms[i] = ms;
     }
   }
-  for (auto &e : ev) cudaEventDestroy(e);
-  corep.reset();
-  parent.reset();
-  minobj.reset();
-  claims.reset();
-  t.free_all();
 }
 
 }  // namespace spb

@@ -208,7 +208,7 @@ struct DenseView {
   const int32_t *sparse_pts;
   const float *pts;
   int dim;
-  double thr;
+  Radius R;
 };
 
 __device__ __forceinline__ void load_pt(const float *pts, int dim, int64_t i, float &x, float &y, float &z) {
@@ -232,7 +232,8 @@ __global__ void __launch_bounds__(128) k_db_core(DenseView v, const uint32_t *__
   while (cur != kSentinel) {
     const float4 lo = ld_node(v.nodes, 2 * (int64_t)cur);
     const float4 hi = ld_node(v.nodes, 2 * (int64_t)cur + 1);
-    const bool hit = gap2(x, y, z, lo, hi) <= v.thr;
+    const bool leaf = cur >= v.nobj - 1;
+    const bool hit = leaf ? hit_box(v.R, x, y, z, lo, hi) : maybe_box(v.R, x, y, z, lo, hi);
     if (cur >= v.nobj - 1) {
       if (hit) {
         const int32_t o = node_link(lo);
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(128) k_db_core(DenseView v, const uint32_t *__
           for (int32_t t = 0; t < len && cnt < min_pts; ++t) {
             float qx, qy, qz;
             load_pt(v.pts, v.dim, v.members[b + t], qx, qy, qz);
-            if (dist2(x, y, z, qx, qy, qz) <= v.thr) ++cnt;
+            if (hit_point(v.R, x, y, z, qx, qy, qz)) ++cnt;
           }
         } else {
           ++cnt;
@@ -302,7 +303,8 @@ __global__ void __launch_bounds__(128) k_db_merge(DenseView v, const uint32_t *_
     while (cur != kSentinel) {
       const float4 lo = ld_node(v.nodes, 2 * (int64_t)cur);
       const float4 hi = ld_node(v.nodes, 2 * (int64_t)cur + 1);
-      const bool hit = gap2(x, y, z, lo, hi) <= v.thr;
+      const bool leaf = cur >= v.nobj - 1;
+      const bool hit = leaf ? hit_box(v.R, x, y, z, lo, hi) : maybe_box(v.R, x, y, z, lo, hi);
       if (cur >= v.nobj - 1) {
         if (hit) {
           const int32_t o = node_link(lo);
@@ -316,7 +318,7 @@ __global__ void __launch_bounds__(128) k_db_merge(DenseView v, const uint32_t *_
                   ++checks;
                   float qx, qy, qz;
                   load_pt(v.pts, v.dim, j, qx, qy, qz);
-                  if (dist2(x, y, z, qx, qy, qz) <= v.thr) db_merge<FOF>(i, j, parent, core, claims);
+                  if (hit_point(v.R, x, y, z, qx, qy, qz)) db_merge<FOF>(i, j, parent, core, claims);
                 }
               }
             }
@@ -487,7 +489,7 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
   build_tree(c, objects.get(), nobj, dim, false, width, t);
   SPB_CUDA(cudaEventRecord(ev[1], c.stream));
 
-  DenseView v{t.nodes, nobj, nd, dbeg.get(), dlen.get(), order, sparse_pts.get(), pts, dim, radius_threshold(eps)};
+  DenseView v{t.nodes, nobj, nd, dbeg.get(), dlen.get(), order, sparse_pts.get(), pts, dim, make_radius(eps)};
   DevBuf<uint8_t> core((size_t)n, c.stream);
   k_dense_core<<<G, 256, 0, c.stream>>>(point_cell.get(), n, core.get());
   SPB_LAUNCHED();

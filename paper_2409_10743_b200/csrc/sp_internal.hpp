@@ -79,6 +79,7 @@ struct Tree {
   float4 *nodes = nullptr;  // 2 float4 per node, 2n-1 nodes (NodeRef order)
   int32_t *perm = nullptr;  // leaf position -> object index
   float *scene = nullptr;   // device float[6]: min xyz, max xyz
+  float4 *leafpt = nullptr; // point trees: leaf p as {x, y, z, rope} (16 B)
   cudaStream_t stream = nullptr;
   Tree() = default;
   Tree(const Tree &) = delete;
@@ -88,6 +89,8 @@ struct Tree {
     if (nodes) cudaFreeAsync(nodes, stream);
     if (perm) cudaFreeAsync(perm, stream);
     if (scene) cudaFreeAsync(scene, stream);
+    if (leafpt) cudaFreeAsync(leafpt, stream);
+    leafpt = nullptr;
     nodes = nullptr;
     perm = nullptr;
     scene = nullptr;

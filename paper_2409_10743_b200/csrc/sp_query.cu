@@ -49,9 +49,10 @@ void query_order(Ctx &c, const float *preds, int64_t nq, int dim, int kind, int3
 // mode 1: spheres with per-query radius float[nq*(dim+1)]
 // mode 2: boxes float[nq*2*dim]
 template <int MODE>
-__global__ void __launch_bounds__(128) k_range_count(const float4 *__restrict__ nodes, int64_t n,
+__global__ void __launch_bounds__(128) k_range_count(const float4 *__restrict__ nodes,
+                                                     const float4 *__restrict__ leafpt, int64_t n,
                                                      const float *__restrict__ preds, int dim,
-                                                     const int32_t *__restrict__ order, int64_t nq, double thr0,
+                                                     const int32_t *__restrict__ order, int64_t nq, Radius R0,
                                                      int32_t cap, int32_t *__restrict__ counts) {
   const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (qi >= nq) return;
@@ -61,8 +62,8 @@ __global__ void __launch_bounds__(128) k_range_count(const float4 *__restrict__ 
     const int stride = MODE == 0 ? dim : dim + 1;
     const float *p = preds + q * stride;
     float cx = p[0], cy = p[1], cz = dim == 3 ? p[2] : 0.f;
-    double thr = MODE == 0 ? thr0 : radius_threshold(p[dim]);
-    c = count_sphere(nodes, n, cx, cy, cz, thr, cap);
+    const Radius R = MODE == 0 ? R0 : make_radius(p[dim]);
+    c = count_sphere(nodes, leafpt, n, cx, cy, cz, R, cap);
   } else {
     float b[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int k = 0; k < dim; ++k) {
@@ -105,13 +106,13 @@ void range_count(Ctx &c, const Tree &t, int kind, const float *preds, int64_t nq
     ord = order.get();
   }
   unsigned g = (unsigned)((nq + 127) / 128);
+  const Radius R = make_radius(radius);
   if (kind == RQ_RADIUS) {
-    double thr = radius_threshold(radius);
-    k_range_count<0><<<g, 128, 0, c.stream>>>(t.nodes, t.n, preds, t.dim, ord, nq, thr, cap, counts);
+    k_range_count<0><<<g, 128, 0, c.stream>>>(t.nodes, t.leafpt, t.n, preds, t.dim, ord, nq, R, cap, counts);
   } else if (kind == RQ_SPHERES) {
-    k_range_count<1><<<g, 128, 0, c.stream>>>(t.nodes, t.n, preds, t.dim, ord, nq, 0.0, cap, counts);
+    k_range_count<1><<<g, 128, 0, c.stream>>>(t.nodes, t.leafpt, t.n, preds, t.dim, ord, nq, R, cap, counts);
   } else {
-    k_range_count<2><<<g, 128, 0, c.stream>>>(t.nodes, t.n, preds, t.dim, ord, nq, 0.0, cap, counts);
+    k_range_count<2><<<g, 128, 0, c.stream>>>(t.nodes, t.leafpt, t.n, preds, t.dim, ord, nq, R, cap, counts);
   }
   SPB_LAUNCHED();
 }
@@ -205,11 +206,11 @@ __global__ void __launch_bounds__(128) k_range_fill(const float4 *__restrict__ n
   int64_t w = offsets[q];
   float b[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   float cx = 0.f, cy = 0.f, cz = 0.f;
-  double thr = 0.0;
+  Radius R{0.0, 0.f, 0.f, 0};
   if (MODE == 1) {
     const float *p = preds + q * (dim + 1);
     cx = p[0]; cy = p[1]; cz = dim == 3 ? p[2] : 0.f;
-    thr = radius_threshold(p[dim]);
+    R = make_radius(p[dim]);
   } else {
     for (int k = 0; k < dim; ++k) {
       b[k] = preds[q * 2 * dim + k];
@@ -220,8 +221,10 @@ __global__ void __launch_bounds__(128) k_range_fill(const float4 *__restrict__ n
   while (cur != kSentinel) {
     const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
     const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
-    const bool hit = MODE == 1 ? (gap2(cx, cy, cz, lo, hi) <= thr) : box_touch(lo, hi, b);
-    if (cur >= n - 1) {
+    const bool leaf = cur >= n - 1;
+    const bool hit = MODE == 1 ? (leaf ? hit_box(R, cx, cy, cz, lo, hi) : maybe_box(R, cx, cy, cz, lo, hi))
+                               : box_touch(lo, hi, b);
+    if (leaf) {
       // key = (query << 32) | object; sorting the keys orders each row by object
       if (hit) keyed[w++] = ((uint64_t)q << 32) | (uint32_t)node_link(lo);
       cur = node_rope(hi);
@@ -274,7 +277,7 @@ int64_t range_crs(Ctx &c, const Tree &t, int kind, const float *preds, int64_t n
 // only later leaves are examined and each close pair appears exactly once.
 // ---------------------------------------------------------------------------
 template <bool FILL>
-__global__ void __launch_bounds__(128) k_pairs(const float4 *__restrict__ nodes, int64_t n, double thr,
+__global__ void __launch_bounds__(128) k_pairs(const float4 *__restrict__ nodes, int64_t n, Radius R,
                                                int32_t *__restrict__ counts, const int64_t *__restrict__ offsets,
                                                int32_t *__restrict__ pairs) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -287,8 +290,9 @@ __global__ void __launch_bounds__(128) k_pairs(const float4 *__restrict__ nodes,
   while (cur != kSentinel) {
     const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
     const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
-    const bool hit = gap2(me.x, me.y, me.z, lo, hi) <= thr;
-    if (cur >= n - 1) {
+    const bool leaf = cur >= n - 1;
+    const bool hit = leaf ? hit_box(R, me.x, me.y, me.z, lo, hi) : maybe_box(R, me.x, me.y, me.z, lo, hi);
+    if (leaf) {
       if (hit) {
         if (FILL) {
           pairs[2 * w] = node_link(me);
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(128) k_pairs(const float4 *__restrict__ nodes,
 
 int64_t pair_list(Ctx &c, const Tree &t, float eps, int32_t *pairs, int64_t capacity) {
   if (t.n < 2) return 0;
-  const double thr = radius_threshold(eps);
+  const Radius thr = make_radius(eps);
   DevBuf<int32_t> counts((size_t)t.n, c.stream);
   DevBuf<int64_t> offsets((size_t)t.n + 1, c.stream);
   unsigned g = (unsigned)((t.n + 127) / 128);
