@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "sp_common.cuh"
 #include "sp_internal.hpp"
@@ -190,11 +191,13 @@ void morton_codes(Ctx &c, const float *objects, int64_t n, int dim, bool points,
 // ---------------------------------------------------------------------------
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_ITEMS = 16;
-constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096
 constexpr int RS_BINS = 256;
 constexpr int RS_WH = RS_BINS + 1;  // + one slot for out-of-range items
-constexpr size_t RS_SMEM = (size_t)RS_TILE * 8 + (size_t)RS_TILE * 4 + (size_t)RS_WARPS * RS_WH * 4;
+
+template <int ITEMS>
+constexpr size_t rs_smem_bytes() {
+  return (size_t)RS_THREADS * ITEMS * 12 + (size_t)RS_WARPS * RS_WH * 4;
+}
 
 __global__ void __launch_bounds__(256) k_rs_hist(const uint64_t *__restrict__ keys, int64_t n, int npass,
                                                  uint32_t *__restrict__ ghist) {
@@ -237,16 +240,16 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
   return v;
 }
 
-__global__ void __launch_bounds__(RS_THREADS) k_rs_onesweep(const uint64_t *__restrict__ kin,
-                                                            const uint32_t *__restrict__ vin,
-                                                            uint64_t *__restrict__ kout, uint32_t *__restrict__ vout,
-                                                            int64_t n, int shift, const uint32_t *__restrict__ binbase,
-                                                            unsigned long long *lookback, uint32_t *tile_ctr,
-                                                            uint32_t tag) {
+template <int ITEMS>
+__global__ void __launch_bounds__(RS_THREADS, ITEMS <= 8 ? 4 : 2) k_rs_onesweep(
+    const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
+    uint32_t *__restrict__ vout, int64_t n, int shift, const uint32_t *__restrict__ binbase,
+    unsigned long long *lookback, uint32_t *tile_ctr, uint32_t tag) {
+  constexpr int TILE = RS_THREADS * ITEMS;
   extern __shared__ __align__(16) unsigned char rs_smem[];
   uint64_t *skeys = reinterpret_cast<uint64_t *>(rs_smem);
-  uint32_t *svals = reinterpret_cast<uint32_t *>(skeys + RS_TILE);
-  uint32_t *whist = svals + RS_TILE;
+  uint32_t *svals = reinterpret_cast<uint32_t *>(skeys + TILE);
+  uint32_t *whist = svals + TILE;
   __shared__ uint32_t s_dstart[RS_BINS];
   __shared__ uint32_t s_gbase[RS_BINS];
   __shared__ uint32_t s_wsum[RS_WARPS];
@@ -257,41 +260,46 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_onesweep(const uint64_t *__re
   if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
-  const int64_t base = (int64_t)tile * RS_TILE;
+  const int64_t base = (int64_t)tile * TILE;
 
-  uint64_t key[RS_ITEMS];
-  uint32_t val[RS_ITEMS];
-  uint32_t dig[RS_ITEMS];
-  uint32_t rk[RS_ITEMS];
-  const int64_t wbase = base + (int64_t)warp * (RS_ITEMS * 32);
+  uint64_t key[ITEMS];
+  uint32_t val[ITEMS];
+  uint16_t rk[ITEMS];
+  const int64_t wbase = base + (int64_t)warp * (ITEMS * 32);
+  if (base + TILE <= n) {  // full tile: unconditional loads, all in flight together
 #pragma unroll
-  for (int i = 0; i < RS_ITEMS; ++i) {
-    int64_t idx = wbase + i * 32 + lane;
-    if (idx < n) {
-      key[i] = kin[idx];
-      val[i] = vin ? vin[idx] : (uint32_t)idx;
-      dig[i] = (uint32_t)(key[i] >> shift) & 0xffu;
+    for (int i = 0; i < ITEMS; ++i) key[i] = kin[wbase + i * 32 + lane];
+    if (vin) {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) val[i] = vin[wbase + i * 32 + lane];
     } else {
-      key[i] = 0;
-      val[i] = 0;
-      dig[i] = RS_BINS;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) val[i] = (uint32_t)(wbase + i * 32 + lane);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int64_t idx = wbase + i * 32 + lane;
+      key[i] = idx < n ? kin[idx] : ~0ull;
+      val[i] = idx < n ? (vin ? vin[idx] : (uint32_t)idx) : 0u;
     }
   }
+  auto digit = [&](int i) -> uint32_t {
+    return (wbase + i * 32 + lane < n) ? ((uint32_t)(key[i] >> shift) & 0xffu) : (uint32_t)RS_BINS;
+  };
   // Warp-local stable ranks: items are visited in original order (item i of
   // lane l is element i*32 + l of the warp's slice).
   uint32_t *wh = whist + warp * RS_WH;
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
-  for (int i = 0; i < RS_ITEMS; ++i) {
-    uint32_t peers = __match_any_sync(0xffffffffu, dig[i]);
-    uint32_t cnt = __popc(peers);
-    uint32_t below = __popc(peers & lt);
-    int leader = __ffs(peers) - 1;
-    uint32_t b = wh[dig[i]];
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint32_t d = digit(i);
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t b = wh[d];
     __syncwarp();
-    if (lane == leader) wh[dig[i]] = b + cnt;
+    if (lane == __ffs(peers) - 1) wh[d] = b + __popc(peers);
     __syncwarp();
-    rk[i] = b + below;
+    rk[i] = (uint16_t)(b + __popc(peers & lt));
   }
   __syncthreads();
 
@@ -299,7 +307,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_onesweep(const uint64_t *__re
   uint32_t tot = 0;
 #pragma unroll
   for (int w = 0; w < RS_WARPS; ++w) {
-    uint32_t cw = whist[w * RS_WH + tid];
+    const uint32_t cw = whist[w * RS_WH + tid];
     whist[w * RS_WH + tid] = tot;
     tot += cw;
   }
@@ -313,8 +321,8 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_onesweep(const uint64_t *__re
     st_volatile_u64(mine, agg_tag | tot);
     int64_t j = (int64_t)tile - 1;
     while (true) {
-      unsigned long long v = ld_volatile_u64(lookback + (size_t)j * RS_BINS + tid);
-      unsigned long long st = v & 0xffffffff00000000ull;
+      const unsigned long long v = ld_volatile_u64(lookback + (size_t)j * RS_BINS + tid);
+      const unsigned long long st = v & 0xffffffff00000000ull;
       if (st == inc_tag) {
         excl += (uint32_t)v;
         break;
@@ -331,7 +339,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_onesweep(const uint64_t *__re
   // Tile-local digit starts: exclusive scan of tot over the 256 digits.
   uint32_t x = tot;
   for (int d = 1; d < 32; d <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
     if (lane >= d) x += y;
   }
   if (lane == 31) s_wsum[warp] = x;
@@ -342,37 +350,36 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_onesweep(const uint64_t *__re
   __syncthreads();
 
 #pragma unroll
-  for (int i = 0; i < RS_ITEMS; ++i) {
-    if (dig[i] < RS_BINS) {
-      uint32_t pos = s_dstart[dig[i]] + wh[dig[i]] + rk[i];
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint32_t d = digit(i);
+    if (d < RS_BINS) {
+      const uint32_t pos = s_dstart[d] + wh[d] + rk[i];
       skeys[pos] = key[i];
       svals[pos] = val[i];
     }
   }
   __syncthreads();
-  const int valid = (int)((n - base) < (int64_t)RS_TILE ? (n - base) : (int64_t)RS_TILE);
+  const int valid = (int)((n - base) < (int64_t)TILE ? (n - base) : (int64_t)TILE);
   for (int pos = tid; pos < valid; pos += RS_THREADS) {
-    uint64_t k = skeys[pos];
-    uint32_t d = (uint32_t)(k >> shift) & 0xffu;
-    uint32_t o = s_gbase[d] + (uint32_t)pos - s_dstart[d];
+    const uint64_t k = skeys[pos];
+    const uint32_t d = (uint32_t)(k >> shift) & 0xffu;
+    const uint32_t o = s_gbase[d] + (uint32_t)pos - s_dstart[d];
     kout[o] = k;
     vout[o] = svals[pos];
   }
 }
 
-void radix_sort_pairs(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_alt, uint32_t **vals_alt, int64_t n,
-                      int key_bits, bool vals_iota) {
-  if (n <= 1) {
-    if (n == 1 && vals_iota) SPB_CUDA(cudaMemsetAsync(*vals, 0, sizeof(uint32_t), c.stream));
-    return;
-  }
+template <int ITEMS>
+void onesweep_passes(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_alt, uint32_t **vals_alt, int64_t n,
+                     int npass, bool vals_iota) {
+  constexpr int TILE = RS_THREADS * ITEMS;
+  constexpr size_t SMEM = rs_smem_bytes<ITEMS>();
   static bool attr_set = false;
   if (!attr_set) {
-    SPB_CUDA(cudaFuncSetAttribute(k_rs_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RS_SMEM));
+    SPB_CUDA(cudaFuncSetAttribute(k_rs_onesweep<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
     attr_set = true;
   }
-  const int npass = std::max(1, (key_bits + 7) / 8);
-  const int64_t ntiles = (n + RS_TILE - 1) / RS_TILE;
+  const int64_t ntiles = (n + TILE - 1) / TILE;
   DevBuf<uint32_t> hist((size_t)npass * RS_BINS + npass, c.stream);
   DevBuf<unsigned long long> lookback((size_t)ntiles * RS_BINS, c.stream);
   SPB_CUDA(cudaMemsetAsync(hist.get(), 0, hist.n * sizeof(uint32_t), c.stream));
@@ -383,13 +390,26 @@ void radix_sort_pairs(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_
   SPB_LAUNCHED();
   uint32_t *ctr = hist.get() + (size_t)npass * RS_BINS;
   for (int p = 0; p < npass; ++p) {
-    k_rs_onesweep<<<(unsigned)ntiles, RS_THREADS, RS_SMEM, c.stream>>>(
-        *keys, (p == 0 && vals_iota) ? nullptr : *vals, *keys_alt, *vals_alt, n, 8 * p, hist.get() + (size_t)p * RS_BINS, lookback.get(), ctr + p,
-        (uint32_t)(2 * p + 1));
+    k_rs_onesweep<ITEMS><<<(unsigned)ntiles, RS_THREADS, SMEM, c.stream>>>(
+        *keys, (p == 0 && vals_iota) ? nullptr : *vals, *keys_alt, *vals_alt, n, 8 * p,
+        hist.get() + (size_t)p * RS_BINS, lookback.get(), ctr + p, (uint32_t)(2 * p + 1));
     SPB_LAUNCHED();
     std::swap(*keys, *keys_alt);
     std::swap(*vals, *vals_alt);
   }
+}
+
+void radix_sort_pairs(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_alt, uint32_t **vals_alt, int64_t n,
+                      int key_bits, bool vals_iota) {
+  if (n <= 1) {
+    if (n == 1 && vals_iota) SPB_CUDA(cudaMemsetAsync(*vals, 0, sizeof(uint32_t), c.stream));
+    return;
+  }
+  const int npass = std::max(1, (key_bits + 7) / 8);
+  static const int items = getenv("SPB_RS_ITEMS") ? atoi(getenv("SPB_RS_ITEMS")) : 16;
+  if (items >= 16) onesweep_passes<16>(c, keys, vals, keys_alt, vals_alt, n, npass, vals_iota);
+  else if (items >= 12) onesweep_passes<12>(c, keys, vals, keys_alt, vals_alt, n, npass, vals_iota);
+  else onesweep_passes<8>(c, keys, vals, keys_alt, vals_alt, n, npass, vals_iota);
 }
 
 // ---------------------------------------------------------------------------
