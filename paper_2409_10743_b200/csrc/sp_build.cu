@@ -460,10 +460,16 @@ __device__ __forceinline__ void climb(const HierView &H, int64_t p, float lo[3],
   while (true) {
     const bool L = H.is_left(l, r);
     const int64_t a = L ? r : l - 1;  // the parent's split position
-    __threadfence();
-    const int32_t other = atomicExch(&flags[a], (int32_t)(L ? l : r));
+    // Release-exchange: this node's box stores are performed before the flag
+    // changes hands.  The second arrival reads the sibling box with L2-coherent
+    // loads whose addresses depend on the exchanged value, so no acquire
+    // fence (and no L1 invalidation) is needed.
+    int32_t other;
+    asm volatile("atom.release.gpu.global.exch.b32 %0, [%1], %2;"
+                 : "=r"(other)
+                 : "l"(flags + a), "r"((int32_t)(L ? l : r))
+                 : "memory");
     if (other < 0) return;  // first arrival
-    __threadfence();
     if (L) r = other;
     else l = other;
     const int64_t left = (a == l) ? n - 1 + l : a;
