@@ -194,7 +194,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         from paper_2409_10743_b200 import distributed as spd
         pts = sp.generate_field(n_total, first=rank * n, count=n, seed=args.seed, ctx=ctx)
-        step = lambda: spd.fof_slabs(pts, eps, ctx=ctx, rank=rank, world=world, first_index=rank * n)
+        step = lambda: spd.fof_slabs(pts, eps, first_index=rank * n, ctx=ctx)
     else:
         pts = sp.generate_field(n_total, first=0, count=n, seed=args.seed, ctx=ctx)
         labels = torch.empty(n, dtype=torch.int32, device=dev)
