@@ -77,7 +77,15 @@ typedef struct {
 int sp_ctx_create(int device, void *stream, sp_ctx **out);
 int sp_ctx_destroy(sp_ctx *ctx);
 int sp_ctx_set_stream(sp_ctx *ctx, void *stream);
+/* Wait for all work on ctx; reports (SP_EINVAL) input errors that calls made
+ * with SP_FLAG_ASYNC found on the device. */
 int sp_ctx_synchronize(sp_ctx *ctx);
+/* SP_FLAG_ASYNC: sp_dbscan / sp_bvh_build only ENQUEUE work on the context
+ * stream (host<->device copies included) and return; host buffers must stay
+ * valid and untouched until sp_ctx_synchronize.  Two contexts on two streams
+ * then pipeline consecutive calls (one call's copies overlap the other's
+ * kernels).  Timings are not collected in this mode. */
+int sp_ctx_set_flags(sp_ctx *ctx, int flags);
 const char *sp_last_error(const sp_ctx *ctx);
 /* Number of kernels this library launched on ctx since creation. */
 int64_t sp_ctx_kernel_launches(const sp_ctx *ctx);

@@ -77,6 +77,7 @@ def _load() -> C.CDLL:
         "sp_ctx_destroy": (C.c_int, [vp]),
         "sp_ctx_set_stream": (C.c_int, [vp, vp]),
         "sp_ctx_synchronize": (C.c_int, [vp]),
+        "sp_ctx_set_flags": (C.c_int, [vp, C.c_int]),
         "sp_last_error": (C.c_char_p, [vp]),
         "sp_ctx_kernel_launches": (i64, [vp]),
         "sp_ctx_phase_count": (C.c_int, [vp]),
@@ -143,6 +144,11 @@ class Context:
 
     def synchronize(self):
         self._check(_lib.sp_ctx_synchronize(self.h))
+
+    def set_async(self, on: bool = True):
+        """SP_FLAG_ASYNC: calls only enqueue work; call synchronize() before
+        reading outputs or reusing host buffers."""
+        self._check(_lib.sp_ctx_set_flags(self.h, 1 if on else 0))
 
     @property
     def kernel_launches(self) -> int:

@@ -91,6 +91,10 @@ __global__ void k_bounds_final(const int32_t *ord6, int dim, int64_t n, float *s
   }
 }
 
+__global__ void k_flag_or(const int *src, int *dst) {
+  if (*src) *dst = 1;
+}
+
 void scene_bounds(Ctx &c, const float *objects, int64_t n, int dim, bool points, float *scene, int *bad) {
   DevBuf<int32_t> ord(6, c.stream);
   k_bounds_init<<<1, 32, 0, c.stream>>>(ord.get(), bad);
@@ -529,10 +533,16 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
   mark(c, "start");
   scene_bounds(c, objects, n, dim, points, t.scene, bad.get());
   mark(c, "bounds");
-  int h_bad = 0;
-  SPB_CUDA(cudaMemcpyAsync(&h_bad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  SPB_CUDA(cudaStreamSynchronize(c.stream));
-  if (h_bad) throw InvalidArgument("bvh: non-finite object bounds");
+  if (c.async()) {
+    // no host round trip: fold the flag into the context's deferred error
+    k_flag_or<<<1, 1, 0, c.stream>>>(bad.get(), c.d_err);
+    SPB_LAUNCHED();
+  } else {
+    int h_bad = 0;
+    SPB_CUDA(cudaMemcpyAsync(&h_bad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    SPB_CUDA(cudaStreamSynchronize(c.stream));
+    if (h_bad) throw InvalidArgument("bvh: non-finite object bounds");
+  }
   if (n == 0) return;
 
   const int64_t num_nodes = 2 * n - 1;

@@ -88,7 +88,7 @@ int guarded(sp_ctx *ctx, F &&f) {
   int rc = SP_OK;
   try {
     f(ctx->c);
-    if (ctx->c.marks_used) {
+    if (ctx->c.marks_used && !ctx->c.async()) {
       SPB_CUDA(cudaStreamSynchronize(ctx->c.stream));
       spb::resolve_marks(ctx->c);
     }
@@ -117,7 +117,9 @@ void check_dim(int dim) {
   if (dim != 2 && dim != 3) throw spb::InvalidArgument("dimension must be 2 or 3");
 }
 
-void finish(spb::Ctx &c) { SPB_CUDA(cudaStreamSynchronize(c.stream)); }
+void finish(spb::Ctx &c) {
+  if (!c.async()) SPB_CUDA(cudaStreamSynchronize(c.stream));
+}
 
 }  // namespace
 
@@ -141,6 +143,11 @@ int sp_ctx_create(int device, void *stream, sp_ctx **out) {
     }
     ctx->c.owns_stream = true;
   }
+  if (cudaMalloc(&ctx->c.d_err, sizeof(int)) != cudaSuccess || cudaMemset(ctx->c.d_err, 0, sizeof(int)) != cudaSuccess) {
+    if (ctx->c.owns_stream) cudaStreamDestroy(ctx->c.stream);
+    delete ctx;
+    return SP_ECUDA;
+  }
   // Keep freed stream-ordered allocations reserved: a caching allocator.
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -157,6 +164,7 @@ int sp_ctx_destroy(sp_ctx *ctx) {
     DeviceGuard dg(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
     for (cudaEvent_t e : ctx->c.event_pool) cudaEventDestroy(e);
+    if (ctx->c.d_err) cudaFree(ctx->c.d_err);
     if (ctx->c.owns_stream) cudaStreamDestroy(ctx->c.stream);
   }
   delete ctx;
@@ -179,7 +187,26 @@ int sp_ctx_set_stream(sp_ctx *ctx, void *stream) {
 }
 
 int sp_ctx_synchronize(sp_ctx *ctx) {
-  return guarded(ctx, [&](spb::Ctx &c) { finish(c); });
+  return guarded(ctx, [&](spb::Ctx &c) {
+    SPB_CUDA(cudaStreamSynchronize(c.stream));
+    int err = 0;
+    SPB_CUDA(cudaMemcpy(&err, c.d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err) {
+      SPB_CUDA(cudaMemset(c.d_err, 0, sizeof(int)));
+      throw spb::InvalidArgument("non-finite coordinate in an asynchronous call");
+    }
+  });
+}
+
+int sp_ctx_set_flags(sp_ctx *ctx, int flags) {
+  if (!ctx) return SP_EINVAL;
+  if (ctx->c.async() && !(flags & SP_FLAG_ASYNC)) {
+    int rc = sp_ctx_synchronize(ctx);
+    ctx->c.flags = flags;
+    return rc;
+  }
+  ctx->c.flags = flags;
+  return SP_OK;
 }
 
 const char *sp_last_error(const sp_ctx *ctx) { return ctx ? ctx->c.last_error.c_str() : "null context"; }

@@ -216,6 +216,7 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
   SPB_LAUNCHED();
   SPB_CUDA(cudaEventRecord(ev[4], c.stream));
   mark(c, "finalize");
+  if (c.async()) return;  // timings need a host wait; async calls skip them
   SPB_CUDA(cudaEventSynchronize(ev[4]));
   if (res) {
     for (int i = 0; i < 4; ++i) {

@@ -27,6 +27,12 @@ struct Ctx {
   std::vector<const char *> mark_names;
   size_t marks_used = 0;
   std::vector<std::pair<std::string, double>> phases;
+  // SP_FLAG_ASYNC: calls only enqueue work (no host synchronisation); input
+  // validity errors found on the device accumulate in d_err and are reported
+  // by the next sp_ctx_synchronize.
+  int flags = 0;
+  int *d_err = nullptr;
+  bool async() const { return (flags & 1) != 0; }
 };
 
 // Record a phase boundary on the context stream (cheap; no host sync).
