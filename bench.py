@@ -247,40 +247,31 @@ def run_ours(args, rank, world, local_rank):
     h2d = n * 12
     d2h = n * 5
     if world == 1:
-        # Public API with pinned HOST buffers: every step copies its points in
-        # and its labels + core flags out.  Two asynchronous contexts on two
-        # streams alternate steps, so one step's PCIe traffic overlaps the
-        # other step's kernels (SP_FLAG_ASYNC, include/sp_b200.h).
+        # Public API with pinned HOST buffers: every step uploads its points
+        # and downloads its labels + core flags.  The context runs with
+        # SP_FLAG_ASYNC: uploads/downloads go on its copy streams, so step
+        # i+1's upload and step i-1's download overlap step i's kernels
+        # (include/sp_b200.h).
         host_pts = torch.empty((n, 3), dtype=torch.float32, pin_memory=True)
         host_pts.copy_(pts)
-        streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
-        ctxs = [sp.Context(local_rank, stream=s.cuda_stream) for s in streams]
-        outs = [(torch.empty(n, dtype=torch.int32, pin_memory=True), torch.empty(n, dtype=torch.uint8, pin_memory=True))
-                for _ in range(2)]
-        for cx, o in zip(ctxs, outs):  # warm both contexts synchronously
-            sp.friends_of_friends(host_pts, eps, ctx=cx, out=o)
-            cx.set_async(True)
+        cstream = torch.cuda.Stream(dev)
+        ectx = sp.Context(local_rank, stream=cstream.cuda_stream)
+        host_labels = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        host_core = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        sp.friends_of_friends(host_pts, eps, ctx=ectx, out=(host_labels, host_core))  # warm
+        ectx.set_async(True)
         barrier()
-        e_start = torch.cuda.Event(enable_timing=True)
-        e_start.record(streams[0])
-        streams[1].wait_event(e_start)
-        launches_e2e0 = sum(cx.kernel_launches for cx in ctxs)
+        e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_start.record(cstream)
         for i in range(args.steps):
-            sp.friends_of_friends(host_pts, eps, ctx=ctxs[i % 2], out=outs[i % 2])
-        e_b = torch.cuda.Event()
-        e_b.record(streams[1])
-        streams[0].wait_event(e_b)
-        e_end = torch.cuda.Event(enable_timing=True)
-        e_end.record(streams[0])
-        for cx in ctxs:
-            cx.synchronize()
+            sp.friends_of_friends(host_pts, eps, ctx=ectx, out=(host_labels, host_core))
+        ectx.synchronize()  # waits for the compute and both copy streams
+        e_end.record(cstream)
         barrier()
         e2e_value = n_total * args.steps / (e_start.elapsed_time(e_end) / 1e3)
-        # both host runs must agree bit-for-bit with the device-resident run
-        for hl, hc in outs:
-            assert torch.equal(hl, labels.cpu()) and torch.equal(hc, core.cpu()), "e2e != device run"
-        for cx in ctxs:
-            cx.set_async(False)
+        ectx.set_async(False)
+        # the host run must agree bit-for-bit with the device-resident run
+        assert torch.equal(host_labels, labels.cpu()) and torch.equal(host_core, core.cpu()), "e2e != device run"
     else:
         e2e_value = value  # replaced by the distributed host-buffer path once it lands
 

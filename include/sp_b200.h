@@ -155,6 +155,10 @@ int sp_pair_list(sp_ctx *ctx, const sp_bvh *bvh, float eps, int32_t *pairs, int6
  * representatives' own scene). */
 int sp_sort_queries(sp_ctx *ctx, const float *points, int64_t nq, int dim, int32_t *order, int mem);
 
+/* Diagnostics: node visits and close pairs of each leaf's pair walk (leaf
+ * order) for a point tree.  Not part of the reference surface. */
+int sp_debug_walk_lengths(sp_ctx *ctx, const sp_bvh *bvh, float eps, int32_t *steps, int32_t *hits, int mem);
+
 /* code_of over object centroids against their scene (morton.hpp:106-109). */
 int sp_morton_codes(sp_ctx *ctx, const float *objects, int64_t n, int dim, int is_points, int code_width,
                     uint64_t *codes, int mem);

@@ -27,7 +27,19 @@ namespace {
 
 using spb::DevBuf;
 
-// Input array: device pointer as-is, or a device copy of a host array.
+// Host<->device copies run on the context's dedicated copy streams and are
+// ordered against the compute stream with events, so with SP_FLAG_ASYNC the
+// upload of call i+1 and the download of call i-1 overlap call i's kernels.
+void stream_after(cudaStream_t waiter, cudaStream_t producer) {
+  cudaEvent_t e;
+  SPB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  SPB_CUDA(cudaEventRecord(e, producer));
+  SPB_CUDA(cudaStreamWaitEvent(waiter, e, 0));
+  SPB_CUDA(cudaEventDestroy(e));
+}
+
+// Input array: device pointer as-is, or a device copy of a host array
+// (uploaded on the H2D stream, released in compute-stream order).
 template <class T>
 struct In {
   DevBuf<T> buf;
@@ -38,13 +50,16 @@ struct In {
       p = src;
       return;
     }
-    buf = DevBuf<T>(count, c.stream);
-    SPB_CUDA(cudaMemcpyAsync(buf.get(), src, count * sizeof(T), cudaMemcpyHostToDevice, c.stream));
+    buf = DevBuf<T>(count, c.h2d);
+    SPB_CUDA(cudaMemcpyAsync(buf.get(), src, count * sizeof(T), cudaMemcpyHostToDevice, c.h2d));
+    stream_after(c.stream, c.h2d);
+    buf.s = c.stream;
     p = buf.get();
   }
 };
 
-// Output array: device pointer as-is, or a device scratch copied back by flush().
+// Output array: device pointer as-is, or a device scratch downloaded by
+// flush() on the D2H stream once the compute stream has produced it.
 template <class T>
 struct Out {
   DevBuf<T> buf;
@@ -62,7 +77,10 @@ struct Out {
     host = dst;
   }
   void flush(spb::Ctx &c) {
-    if (host) SPB_CUDA(cudaMemcpyAsync(host, buf.get(), count * sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+    if (!host) return;
+    stream_after(c.d2h, c.stream);
+    SPB_CUDA(cudaMemcpyAsync(host, buf.get(), count * sizeof(T), cudaMemcpyDeviceToHost, c.d2h));
+    buf.s = c.d2h;
   }
 };
 
@@ -117,8 +135,14 @@ void check_dim(int dim) {
   if (dim != 2 && dim != 3) throw spb::InvalidArgument("dimension must be 2 or 3");
 }
 
+void sync_all(spb::Ctx &c) {
+  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  SPB_CUDA(cudaStreamSynchronize(c.h2d));
+  SPB_CUDA(cudaStreamSynchronize(c.d2h));
+}
+
 void finish(spb::Ctx &c) {
-  if (!c.async()) SPB_CUDA(cudaStreamSynchronize(c.stream));
+  if (!c.async()) sync_all(c);
 }
 
 }  // namespace
@@ -143,7 +167,9 @@ int sp_ctx_create(int device, void *stream, sp_ctx **out) {
     }
     ctx->c.owns_stream = true;
   }
-  if (cudaMalloc(&ctx->c.d_err, sizeof(int)) != cudaSuccess || cudaMemset(ctx->c.d_err, 0, sizeof(int)) != cudaSuccess) {
+  if (cudaStreamCreateWithFlags(&ctx->c.h2d, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->c.d2h, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&ctx->c.d_err, sizeof(int)) != cudaSuccess || cudaMemset(ctx->c.d_err, 0, sizeof(int)) != cudaSuccess) {
     if (ctx->c.owns_stream) cudaStreamDestroy(ctx->c.stream);
     delete ctx;
     return SP_ECUDA;
@@ -164,6 +190,10 @@ int sp_ctx_destroy(sp_ctx *ctx) {
     DeviceGuard dg(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
     for (cudaEvent_t e : ctx->c.event_pool) cudaEventDestroy(e);
+    cudaStreamSynchronize(ctx->c.h2d);
+    cudaStreamSynchronize(ctx->c.d2h);
+    if (ctx->c.h2d) cudaStreamDestroy(ctx->c.h2d);
+    if (ctx->c.d2h) cudaStreamDestroy(ctx->c.d2h);
     if (ctx->c.d_err) cudaFree(ctx->c.d_err);
     if (ctx->c.owns_stream) cudaStreamDestroy(ctx->c.stream);
   }
@@ -188,7 +218,7 @@ int sp_ctx_set_stream(sp_ctx *ctx, void *stream) {
 
 int sp_ctx_synchronize(sp_ctx *ctx) {
   return guarded(ctx, [&](spb::Ctx &c) {
-    SPB_CUDA(cudaStreamSynchronize(c.stream));
+    sync_all(c);
     int err = 0;
     SPB_CUDA(cudaMemcpy(&err, c.d_err, sizeof(int), cudaMemcpyDeviceToHost));
     if (err) {
@@ -391,6 +421,19 @@ int sp_pair_list(sp_ctx *ctx, const sp_bvh *bvh, float eps, int32_t *pairs, int6
       SPB_CUDA(cudaMemcpyAsync(pairs, pdev, (size_t)total * 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
     finish(c);
     if (total > capacity && pairs) throw spb::CapacityError();
+  });
+}
+
+// Diagnostics (not part of the reference surface): per-leaf node visits and
+// close pairs of the pair walk, in leaf order.
+int sp_debug_walk_lengths(sp_ctx *ctx, const sp_bvh *bvh, float eps, int32_t *steps, int32_t *hits, int mem) {
+  return guarded(ctx, [&](spb::Ctx &c) {
+    if (!bvh) throw spb::InvalidArgument("null bvh");
+    Out<int32_t> os(c, steps, (size_t)bvh->t.n, mem), oh(c, hits, (size_t)bvh->t.n, mem);
+    spb::walk_lengths(c, bvh->t, eps, os.p, oh.p);
+    os.flush(c);
+    oh.flush(c);
+    finish(c);
   });
 }
 

@@ -32,6 +32,7 @@ struct Ctx {
   // by the next sp_ctx_synchronize.
   int flags = 0;
   int *d_err = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams for host buffers
   bool async() const { return (flags & 1) != 0; }
 };
 

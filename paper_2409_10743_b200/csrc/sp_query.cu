@@ -471,3 +471,36 @@ void knn(Ctx &c, const Tree &t, const float *origins, int64_t nq, int32_t k, int
 }
 
 }  // namespace spb
+
+namespace spb {
+
+// Diagnostics: node visits of each leaf's pair walk (traversal.hpp:162-184).
+__global__ void k_walk_lengths(const float4 *__restrict__ nodes, const float4 *__restrict__ leafpt, int64_t n,
+                               Radius R, int32_t *__restrict__ steps, int32_t *__restrict__ hits) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const float4 me = ld_node(leafpt, p);
+  int32_t cur = __float_as_int(me.w), s = 0, h = 0;
+  while (cur != kSentinel) {
+    ++s;
+    if (cur >= n - 1) {
+      const float4 L = ld_node(leafpt, cur - (n - 1));
+      h += hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z);
+      cur = __float_as_int(L.w);
+    } else {
+      const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+      cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
+    }
+  }
+  steps[p] = s;
+  hits[p] = h;
+}
+
+void walk_lengths(Ctx &c, const Tree &t, float eps, int32_t *steps, int32_t *hits) {
+  if (t.n == 0 || !t.leafpt) return;
+  k_walk_lengths<<<(unsigned)((t.n + 127) / 128), 128, 0, c.stream>>>(t.nodes, t.leafpt, t.n, make_radius(eps), steps,
+                                                                      hits);
+  SPB_LAUNCHED();
+}
+
+}  // namespace spb

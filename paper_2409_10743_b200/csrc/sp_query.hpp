@@ -21,6 +21,7 @@ int64_t range_crs(Ctx &c, const Tree &t, int kind, const float *preds, int64_t n
 int64_t pair_list(Ctx &c, const Tree &t, float eps, int32_t *pairs, int64_t capacity);
 void knn(Ctx &c, const Tree &t, const float *origins, int64_t nq, int32_t k, int32_t *idx, float *dist);
 void exclusive_scan(Ctx &c, const int32_t *in, int64_t n, int64_t *out);
+void walk_lengths(Ctx &c, const Tree &t, float eps, int32_t *steps, int32_t *hits);
 
 struct DbscanResult {
   double ms[4] = {0, 0, 0, 0};  // build, core, merge, finalize
