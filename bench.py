@@ -319,6 +319,147 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# the other BASELINE configs; same JSON contract, one line each
+# ---------------------------------------------------------------------------
+CONFIGS = {
+    # name: (points, description)
+    "c1": (1000000, "C1: friends_of_friends on 10^6 uniform points, eps = 0.168*n^(-1/3)"),
+    "c2": (1 << 24, "C2: Bvh::build + sort_queries + range count, 2^24 uniform points, 2^24 sphere queries "
+                    "centred on them, r = cbrt(30/(n*4pi/3)) (~30.7 neighbours)"),
+    "c3": (1 << 26, "C3: fdbscan_densebox min_pts = 5 on the 2^26-point clustered field, eps = 0.168*n^(-1/3)"),
+    "c4": (1 << 24, "C4: Bvh::build + nearest_query k = 16, 2^24 uniform points, 2^24 uniform queries"),
+}
+
+
+def run_config(args):
+    import numpy as np
+    import torch
+    import paper_2409_10743_b200 as sp
+
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream(dev)
+    ctx = sp.Context(0, stream=stream.cuda_stream)
+    w = args.workload
+    n = args.n if args.n != (1 << 27) else CONFIGS[w][0]
+    if w in ("c1", "c2", "c4"):
+        pts = sp.generate_uniform(n, 3, seed=args.seed, ctx=ctx)
+    else:
+        pts = sp.generate_field(n, seed=args.seed, ctx=ctx)
+    qs = sp.generate_uniform(n, 3, seed=args.seed + 1, ctx=ctx) if w == "c4" else pts
+    eps = eps_for(n)
+    r2 = float(np.float32(np.cbrt(30.0 / (n * 4.18879020478639))))
+    times = {}
+
+    def timed(name, fn):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        out = fn()
+        b.record(stream)
+        times.setdefault(name, []).append((a, b))
+        return out
+
+    if w == "c1":
+        step = lambda: timed("fof", lambda: sp.friends_of_friends(pts, eps, ctx=ctx))
+        unit, per_step = "points/s", n
+    elif w == "c3":
+        step = lambda: timed("densebox", lambda: sp.fdbscan_densebox(pts, sp.DbscanParams(eps, 5), ctx=ctx))
+        unit, per_step = "points/s", n
+    elif w == "c2":
+        def step():
+            b = timed("build", lambda: sp.Bvh.build(pts, ctx=ctx))
+            timed("query", lambda: sp.range_count(b, qs, radius=r2))
+        unit, per_step = "queries/s", n
+    else:
+        def step():
+            b = timed("build", lambda: sp.Bvh.build(pts, ctx=ctx))
+            timed("query", lambda: sp.nearest_query(b, qs, 16))
+        unit, per_step = "queries/s", n
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    times.clear()
+    sampler = ClockSampler(0)
+    sampler.start()
+    launches0 = ctx.kernel_launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+    launches = ctx.kernel_launches - launches0
+    ms = e0.elapsed_time(e1)
+    parts = {k: sum(a.elapsed_time(b) for a, b in v) / args.steps for k, v in times.items()}
+
+    # e2e: the same calls with host (pinned) inputs and outputs, synchronous
+    host_pts = torch.empty((n, 3), dtype=torch.float32, pin_memory=True)
+    host_pts.copy_(pts)
+    host_qs = host_pts
+    if w == "c4":
+        host_qs = torch.empty((n, 3), dtype=torch.float32, pin_memory=True)
+        host_qs.copy_(qs)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        if w == "c1":
+            sp.friends_of_friends(host_pts, eps, ctx=ctx)
+        elif w == "c3":
+            sp.fdbscan_densebox(host_pts, sp.DbscanParams(eps, 5), ctx=ctx)
+        elif w == "c2":
+            sp.range_count(sp.Bvh.build(host_pts, ctx=ctx), host_qs, radius=r2)
+        else:
+            sp.nearest_query(sp.Bvh.build(host_pts, ctx=ctx), host_qs, 16)
+    torch.cuda.synchronize(dev)
+    e2e = per_step * args.steps / (time.perf_counter() - t0)
+    h2d = n * 12 * (2 if w == "c4" else 1)
+    d2h = {"c1": n * 5, "c3": n * 5, "c2": n * 4, "c4": n * 16 * 4}[w]
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from oracle_lib import Reference  # the reference CPU path (baseline only)
+        if Reference.available():
+            R = Reference.get()
+            if w == "c1":
+                sample = 1000000
+                p = R.uniform(sample, 3, 1.0, 2409)
+                t = time.perf_counter(); R.dbscan(p, 3, eps_for(sample), 2, "fof"); dt = time.perf_counter() - t
+            elif w == "c3":
+                sample = 1 << 21
+                p = R.field(sample)
+                t = time.perf_counter(); R.dbscan(p, 3, eps_for(sample), 5, "densebox"); dt = time.perf_counter() - t
+            elif w == "c2":
+                sample = 1 << 20
+                p = R.uniform(sample, 3, 1.0, 2409)
+                rr = float(np.float32(np.cbrt(30.0 / (sample * 4.18879020478639))))
+                t = time.perf_counter(); R.range_count(p, p, rr); dt = time.perf_counter() - t
+            else:
+                sample = 1 << 20
+                p = R.uniform(sample, 3, 1.0, 2409)
+                q = R.uniform(sample, 3, 1.0, 2410)
+                t = time.perf_counter(); R.knn(p, q, 16); dt = time.perf_counter() - t
+            cpu = {"value": sample / dt, "unit": unit, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": "%s at n = %d (reference generator), one run, %.2f s" % (w, sample, dt)}
+    line = {
+        "metric": {"c1": METRIC, "c3": "FDBSCAN-DenseBox points/sec (min_pts=5)",
+                   "c2": "BVH build + range-count queries/sec", "c4": "BVH build + kNN (k=16) queries/sec"}[w],
+        "value": per_step * args.steps / (ms / 1e3), "unit": unit, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (exact f64 distance predicate)", "data": "synthetic (device Philox)",
+        "config": {"workload": CONFIGS[w][1], "points": n,
+                   "l2": "inputs larger than L2" if n * 12 > 126e6 else "inputs smaller than L2 (C1 as specified)"},
+        "e2e": {"value": e2e, "unit": unit, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "note": "synchronous calls with pinned host buffers"},
+        "gpu_launches": launches, "cpu_baseline": cpu, "clocks": clocks,
+        "parts_ms": {k: round(v, 3) for k, v in parts.items()},
+    }
+    if w in ("c2", "c4"):
+        line["bvh_build_mpts_s"] = n / (parts["build"] / 1e3) / 1e6
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -329,6 +470,8 @@ def main():
     ap.add_argument("--seed", type=int, default=2409)
     ap.add_argument("--cpu-sample-n", type=int, default=1 << 22)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="fof_field", choices=["fof_field"] + sorted(CONFIGS),
+                    help="fof_field is the headline; c1..c4 are the other SURVEY §8(d) configs (1 GPU)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -345,6 +488,8 @@ def main():
     try:
         if args.impl == "reference":
             run_reference_arm(args, rank, world)
+        elif args.workload != "fof_field":
+            run_config(args)
         else:
             run_ours(args, rank, world, local_rank)
     finally:

@@ -209,7 +209,30 @@ struct DenseView {
   const float *pts;
   int dim;
   Radius R;
+  const float4 *cpts;  // points in sorted-by-cell order {x, y, z, bits(original index)}
 };
+
+// first position in members [b, b+len) (ascending original indices) whose
+// original index exceeds i
+__device__ __forceinline__ int32_t first_above(const float4 *cpts, int64_t b, int32_t len, int32_t i) {
+  int32_t lo = 0, hi = len;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (__float_as_int(cpts[b + mid].w) > i) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+__global__ void k_cell_points(const uint32_t *__restrict__ order, const float *__restrict__ pts, int64_t n, int dim,
+                              float4 *__restrict__ cpts) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    const uint32_t o = order[k];
+    const float *q = pts + (int64_t)o * dim;
+    cpts[k] = make_float4(q[0], q[1], dim == 3 ? q[2] : 0.f, __int_as_float((int)o));
+  }
+}
 
 __device__ __forceinline__ void load_pt(const float *pts, int dim, int64_t i, float &x, float &y, float &z) {
   x = pts[i * dim];
@@ -223,10 +246,10 @@ __global__ void __launch_bounds__(128) k_db_core(DenseView v, const uint32_t *__
                                                  uint8_t *__restrict__ core) {
   const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (qi >= n) return;
-  const int64_t i = qorder[qi];
+  const float4 me = v.cpts[qi];
+  const int64_t i = __float_as_int(me.w);
   if (point_cell[i] >= 0) return;  // dense members are core already
-  float x, y, z;
-  load_pt(v.pts, v.dim, i, x, y, z);
+  const float x = me.x, y = me.y, z = me.z;
   int32_t cnt = 0;
   int32_t cur = 0;
   while (cur != kSentinel) {
@@ -241,9 +264,8 @@ __global__ void __launch_bounds__(128) k_db_core(DenseView v, const uint32_t *__
           const int64_t b = v.dbeg[o];
           const int32_t len = v.dlen[o];
           for (int32_t t = 0; t < len && cnt < min_pts; ++t) {
-            float qx, qy, qz;
-            load_pt(v.pts, v.dim, v.members[b + t], qx, qy, qz);
-            if (hit_point(v.R, x, y, z, qx, qy, qz)) ++cnt;
+            const float4 q = v.cpts[b + t];
+            if (hit_point(v.R, x, y, z, q.x, q.y, q.z)) ++cnt;
           }
         } else {
           ++cnt;
@@ -295,10 +317,10 @@ __global__ void __launch_bounds__(128) k_db_merge(DenseView v, const uint32_t *_
   const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   uint64_t checks = 0;
   if (qi < n) {
-    const int32_t i = (int32_t)qorder[qi];
+    const float4 me = v.cpts[qi];
+    const int32_t i = __float_as_int(me.w);
     const int32_t own = point_cell[i];
-    float x, y, z;
-    load_pt(v.pts, v.dim, i, x, y, z);
+    const float x = me.x, y = me.y, z = me.z;
     int32_t cur = 0;
     while (cur != kSentinel) {
       const float4 lo = ld_node(v.nodes, 2 * (int64_t)cur);
@@ -310,16 +332,15 @@ __global__ void __launch_bounds__(128) k_db_merge(DenseView v, const uint32_t *_
           const int32_t o = node_link(lo);
           if (o < v.nd) {
             if (o != own) {
+              // members ascend by original index: only j > i are checked
               const int64_t b = v.dbeg[o];
               const int32_t len = v.dlen[o];
-              for (int32_t t = 0; t < len; ++t) {
-                const int32_t j = (int32_t)v.members[b + t];
-                if (i < j) {
-                  ++checks;
-                  float qx, qy, qz;
-                  load_pt(v.pts, v.dim, j, qx, qy, qz);
-                  if (hit_point(v.R, x, y, z, qx, qy, qz)) db_merge<FOF>(i, j, parent, core, claims);
-                }
+              const int32_t t0 = first_above(v.cpts, b, len, i);
+              checks += (uint64_t)(len - t0);
+              for (int32_t t = t0; t < len; ++t) {
+                const float4 q = v.cpts[b + t];
+                if (hit_point(v.R, x, y, z, q.x, q.y, q.z))
+                  db_merge<FOF>(i, __float_as_int(q.w), parent, core, claims);
               }
             }
           } else {
@@ -485,11 +506,15 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
   sflag.reset();
   sscan.reset();
   const int64_t nobj = nd + ns;
+  DevBuf<float4> cpts((size_t)n, c.stream);
+  k_cell_points<<<G, 256, 0, c.stream>>>(order, pts, n, dim, cpts.get());
+  SPB_LAUNCHED();
   Tree t;
   build_tree(c, objects.get(), nobj, dim, false, width, t);
   SPB_CUDA(cudaEventRecord(ev[1], c.stream));
 
-  DenseView v{t.nodes, nobj, nd, dbeg.get(), dlen.get(), order, sparse_pts.get(), pts, dim, make_radius(eps)};
+  DenseView v{t.nodes, nobj, nd, dbeg.get(), dlen.get(), order, sparse_pts.get(), pts, dim, make_radius(eps),
+              cpts.get()};
   DevBuf<uint8_t> core((size_t)n, c.stream);
   k_dense_core<<<G, 256, 0, c.stream>>>(point_cell.get(), n, core.get());
   SPB_LAUNCHED();
