@@ -10,7 +10,7 @@ for r in rows[hi + 1:]:
     if len(r) <= vi:
         continue
     v = float(r[vi].replace(',', ''))
-    v *= {'nsecond': 1e-6, 'usecond': 1e-3, 'msecond': 1.0, 'second': 1e3}.get(r[ui], 1.0)
+    v *= {'nsecond': 1e-6, 'ns': 1e-6, 'usecond': 1e-3, 'us': 1e-3, 'msecond': 1.0, 'ms': 1.0, 'second': 1e3, 's': 1e3}.get(r[ui].strip(), 1.0)
     name = r[ki].split('(')[0].replace('void ', '').replace('spb::', '')[:50]
     agg[name] += v
     cnt[name] += 1

@@ -1,0 +1,30 @@
+"""One-screen summary of an ncu --set full report (for profiles/)."""
+import csv, subprocess, sys, json
+METRICS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "dram read"),
+    ("dram__bytes_write.sum", "dram write"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram % of peak"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit rate"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 hit rate"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active"),
+    ("smsp__thread_inst_executed_per_inst_executed.ratio", "threads per warp instruction"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall long-scoreboard / issue"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %"),
+]
+def summarize(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    h, units, v = rows[0], rows[1], rows[2]
+    res = {"kernel": v[h.index("Kernel Name")][:80]}
+    for m, name in METRICS:
+        if m in h:
+            i = h.index(m)
+            res[name] = "%s %s" % (v[i], units[i])
+    return res
+if __name__ == "__main__":
+    for rep in sys.argv[1:]:
+        print(json.dumps(summarize(rep), indent=1))
