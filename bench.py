@@ -116,6 +116,28 @@ def phase_bytes(phase: str, n: int, pairs_per_pt: float, key_bits: int = 63) -> 
     return per.get(phase, 0.0) * n
 
 
+PROFILED = {"merge": "merge_2p27", "sort": "sort_2p27", "hierarchy": "hier_2p27"}
+
+
+def profiled_traffic(phase: str, n: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the phase's
+    kernel from the committed ncu --set full capture (profiles/r01), for the
+    headline size only; None otherwise."""
+    if n != (1 << 27) or phase not in PROFILED:
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", PROFILED[phase] + ".summary.json")) as f:
+            d = json.load(f)
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = 0.0
+        for key in ("dram read", "dram write"):
+            v, u = d[key].split()
+            tot += float(v) * scale[u]
+        return tot
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------------------
 # reference CPU path (oracle/_ref) — the cpu_baseline leg and --impl reference
 # ---------------------------------------------------------------------------
@@ -283,7 +305,7 @@ def run_ours(args, rank, world, local_rank):
         ach_bytes = phase_bytes(dom, n, pairs_per_pt or 0.0)
         ach = ach_bytes / (phases[dom] / 1e3) / 1e9
         roofline = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_src,
+                    "frac": round(ach / peak, 4), "traffic": profiled_traffic(dom, n), "peak_source": peak_src,
                     "algorithmic_bytes_per_launch": ach_bytes, "kernel_ms": round(phases[dom], 3),
                     "share_of_step": round(phases[dom] / ms_per_step, 3)}
         build_ms = sum(phases.get(k, 0.0) for k in ("bounds", "morton", "sort", "hierarchy"))

@@ -171,6 +171,21 @@ int sp_morton_codes(sp_ctx *ctx, const float *objects, int64_t n, int dim, int i
 int sp_dbscan(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, int32_t min_pts, int algo,
               int code_width, int32_t *labels, uint8_t *core, sp_timings *timings, sp_stats *stats, int mem);
 
+/* adjacency_graph_dbscan (dbscan.hpp:456-504): the legacy min_pts = 2
+ * baseline that materialises the eps-neighbourhood CRS; SP_ECAPACITY when
+ * the total exceeds max_adjacency (its CapacityError). */
+int sp_dbscan_adjacency(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, int code_width,
+                        int64_t max_adjacency, int32_t *labels, uint8_t *core, sp_timings *timings, int mem);
+
+/* check_equivalence (verify.hpp:21-61): *violation = -1 when `got` is an
+ * equivalent clustering of `want`, else the index of the first violating
+ * point with *kind = 1 core flag, 2 noise, 3 core partition split, 4 core
+ * clusters merged, 5 border point without an in-cluster core point within
+ * eps.  The border test is a tree walk, not the reference's O(n^2) scan. */
+int sp_check_equivalence(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, const int32_t *got_labels,
+                         const uint8_t *got_core, const int32_t *want_labels, const uint8_t *want_core,
+                         int64_t *violation, int *kind, int mem);
+
 /* ---- synthetic input (for benchmarks; no reference counterpart) ---------- */
 /* HACC-like clustered field of SURVEY §8(d) shape — 25% uniform background
  * plus Gaussian halos of 8192 points, sigma = 0.001*cbrt(2^26/n_total),

@@ -37,7 +37,8 @@ from . import build as _build
 __all__ = [
     "Bvh", "DbscanOutput", "DbscanParams", "DbscanTimings", "DbscanStats", "InvalidArgument", "CapacityError",
     "CudaError", "range_count", "query_crs", "nearest_query", "pair_traversal", "sort_queries", "morton_codes",
-    "fdbscan", "friends_of_friends", "fdbscan_densebox", "generate_field", "generate_uniform", "Context",
+    "fdbscan", "friends_of_friends", "fdbscan_densebox", "adjacency_graph_dbscan", "check_equivalence", "generate_field", "generate_uniform",
+    "Context",
     "default_context", "library_path",
 ]
 
@@ -95,6 +96,9 @@ def _load() -> C.CDLL:
         "sp_sort_queries": (C.c_int, [vp, vp, i64, C.c_int, vp, C.c_int]),
         "sp_morton_codes": (C.c_int, [vp, vp, i64, C.c_int, C.c_int, C.c_int, vp, C.c_int]),
         "sp_dbscan": (C.c_int, [vp, vp, i64, C.c_int, f32, i32, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int]),
+        "sp_dbscan_adjacency": (C.c_int, [vp, vp, i64, C.c_int, f32, C.c_int, i64, vp, vp, vp, C.c_int]),
+        "sp_check_equivalence": (C.c_int, [vp, vp, i64, C.c_int, f32, vp, vp, vp, vp, C.POINTER(i64),
+                                           C.POINTER(C.c_int), C.c_int]),
         "sp_generate_field": (C.c_int, [vp, i64, i64, i64, C.c_uint64, vp, C.c_int]),
         "sp_generate_uniform": (C.c_int, [vp, i64, C.c_int, C.c_uint64, vp, C.c_int]),
     }
@@ -523,6 +527,54 @@ def fdbscan_densebox(points, params: DbscanParams, width: int = 64, ctx: Optiona
                      out=None) -> DbscanOutput:
     """fdbscan_densebox (dbscan.hpp:298-449)."""
     return _dbscan(points, params.eps, params.min_pts, SP_ALGO_DENSEBOX, width, ctx, out)
+
+
+def adjacency_graph_dbscan(points, eps: float, width: int = 64, max_adjacency: Optional[int] = None,
+                           ctx: Optional[Context] = None) -> DbscanOutput:
+    """adjacency_graph_dbscan (dbscan.hpp:456-504): the historical baseline
+    that materialises the neighbour CRS; raises CapacityError past
+    max_adjacency."""
+    ctx = ctx or default_context()
+    dim = _dim_of(points)
+    n = int(points.shape[0])
+    p, mem, keep = _in(points, np.float32)
+    dev = mem == SP_MEM_DEVICE
+    labels, lp = _out(dev, (n,), np.int32, _torch_dtype("int32") if dev else None, points.device if dev else None)
+    core, cp = _out(dev, (n,), np.uint8, _torch_dtype("uint8") if dev else None, points.device if dev else None)
+    t = _Timings()
+    cap = (1 << 62) if max_adjacency is None else int(max_adjacency)
+    ctx._check(_lib.sp_dbscan_adjacency(ctx.h, p, n, dim, C.c_float(eps), int(width), cap, lp, cp, C.byref(t), mem))
+    return DbscanOutput(labels, core, DbscanTimings(t.build_ms, t.core_ms, t.merge_ms, t.finalize_ms))
+
+
+def check_equivalence(points, eps: float, got: DbscanOutput, want: DbscanOutput, ctx: Optional[Context] = None):
+    """check_equivalence (verify.hpp:21-61): None when equivalent, else a
+    message naming the first violating point."""
+    ctx = ctx or default_context()
+    dim = _dim_of(points)
+    n = int(points.shape[0])
+    p, mem, keep = _in(points, np.float32)
+    arrs = []
+    for a, dt in ((got.labels, np.int32), (got.core_flags, np.uint8), (want.labels, np.int32),
+                  (want.core_flags, np.uint8)):
+        if mem == SP_MEM_DEVICE:
+            a = a if _is_torch(a) and a.is_cuda else _torch_from(a, points.device)
+        else:
+            a = np.ascontiguousarray(a.cpu().numpy() if _is_torch(a) else a, dtype=dt)
+        arrs.append(a)
+    v, k = C.c_int64(-1), C.c_int(0)
+    ctx._check(_lib.sp_check_equivalence(ctx.h, p, n, dim, C.c_float(eps), _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]),
+                                         _ptr(arrs[3]), C.byref(v), C.byref(k), mem))
+    if v.value < 0:
+        return None
+    what = {1: "core flag mismatch", 2: "noise mismatch", 3: "core partition mismatch", 4: "core clusters merged",
+            5: "border point has no in-cluster core point within eps"}[k.value]
+    return "%s at point %d" % (what, v.value)
+
+
+def _torch_from(a, device):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(a)).to(device)
 
 
 # ---- synthetic inputs ---------------------------------------------------------------

@@ -424,6 +424,21 @@ int sp_pair_list(sp_ctx *ctx, const sp_bvh *bvh, float eps, int32_t *pairs, int6
   });
 }
 
+int sp_check_equivalence(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, const int32_t *got_labels,
+                         const uint8_t *got_core, const int32_t *want_labels, const uint8_t *want_core,
+                         int64_t *violation, int *kind, int mem) {
+  return guarded(ctx, [&](spb::Ctx &c) {
+    check_dim(dim);
+    In<float> p(c, points, (size_t)n * dim, mem);
+    In<int32_t> gl(c, got_labels, (size_t)n, mem), wl(c, want_labels, (size_t)n, mem);
+    In<uint8_t> gc(c, got_core, (size_t)n, mem), wc(c, want_core, (size_t)n, mem);
+    int k = 0;
+    const int64_t v = spb::check_equivalence(c, p.p, n, dim, eps, gl.p, gc.p, wl.p, wc.p, &k);
+    if (violation) *violation = v;
+    if (kind) *kind = k;
+  });
+}
+
 // Diagnostics (not part of the reference surface): per-leaf node visits and
 // close pairs of the pair walk, in leaf order.
 int sp_debug_walk_lengths(sp_ctx *ctx, const sp_bvh *bvh, float eps, int32_t *steps, int32_t *hits, int mem) {
@@ -496,6 +511,35 @@ int sp_dbscan(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, i
       stats->distance_checks = res.distance_checks;
       stats->num_dense_cells = res.num_dense_cells;
       stats->num_dense_points = res.num_dense_points;
+    }
+  });
+}
+
+int sp_dbscan_adjacency(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, int code_width,
+                        int64_t max_adjacency, int32_t *labels, uint8_t *core, sp_timings *timings, int mem) {
+  return guarded(ctx, [&](spb::Ctx &c) {
+    check_dim(dim);
+    if (code_width != 32 && code_width != 64) throw spb::InvalidArgument("code width must be 32 or 64");
+    if (n < 0 || n > (1LL << 30)) throw spb::InvalidArgument("point count out of range");
+    In<float> p(c, points, (size_t)n * dim, mem);
+    Out<int32_t> ol(c, labels, (size_t)n, mem);
+    Out<uint8_t> oc(c, core, (size_t)n, mem);
+    DevBuf<int32_t> ls;
+    DevBuf<uint8_t> cs;
+    int32_t *lp = ol.p;
+    uint8_t *cp = oc.p;
+    if (!lp && n) { ls = DevBuf<int32_t>((size_t)n, c.stream); lp = ls.get(); }
+    if (!cp && n) { cs = DevBuf<uint8_t>((size_t)n, c.stream); cp = cs.get(); }
+    spb::DbscanResult res;
+    spb::adjacency_dbscan(c, p.p, n, dim, eps, code_width, max_adjacency, lp, cp, &res);
+    ol.flush(c);
+    oc.flush(c);
+    finish(c);
+    if (timings) {
+      timings->build_ms = res.ms[0];
+      timings->core_ms = res.ms[1];
+      timings->merge_ms = res.ms[2];
+      timings->finalize_ms = res.ms[3];
     }
   });
 }

@@ -228,3 +228,91 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
 }
 
 }  // namespace spb
+
+namespace spb {
+
+// ---------------------------------------------------------------------------
+// adjacency_graph_dbscan (dbscan.hpp:456-504): the historical min_pts = 2
+// baseline.  Materialises every point's eps-neighbourhood as CRS (query_crs,
+// traversal.hpp:235-266; SP_ECAPACITY beyond max_adjacency, like its
+// CapacityError), unions each point with every other member of its row, and
+// marks a point core iff its row holds more than itself.  Union-find runs in
+// original index space with min-index hooking, so a root is the label.
+// ---------------------------------------------------------------------------
+__global__ void k_point_spheres(const float *__restrict__ pts, int64_t n, int dim, float eps,
+                                float *__restrict__ sph) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    for (int k = 0; k < dim; ++k) sph[i * (dim + 1) + k] = pts[i * dim + k];
+    sph[i * (dim + 1) + dim] = eps;
+  }
+}
+
+__global__ void k_adjacency_unions(int64_t n, const int64_t *__restrict__ off, const int32_t *__restrict__ val,
+                                   int32_t *parent, uint8_t *__restrict__ core) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t root = (int32_t)i;
+  for (int64_t e = off[i]; e < off[i + 1]; ++e) {
+    const int32_t j = val[e];
+    if (j != i) root = uf_union(parent, root, j);
+  }
+  core[i] = (off[i + 1] - off[i]) > 1;
+}
+
+__global__ void k_adjacency_labels(int64_t n, const int32_t *__restrict__ parent, const uint8_t *__restrict__ core,
+                                   int32_t *__restrict__ labels) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    labels[i] = core[i] ? uf_root(parent, (int32_t)i) : -1;
+}
+
+void adjacency_dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int width, int64_t max_adjacency,
+                      int32_t *labels, uint8_t *core, DbscanResult *res) {
+  if (!(eps > 0.f) || !std::isfinite(eps)) throw InvalidArgument("dbscan: eps must be positive and finite");
+  if (n == 0) return;
+  cudaEvent_t ev[5];
+  for (auto &e : ev) SPB_CUDA(cudaEventCreate(&e));
+  struct EvGuard {
+    cudaEvent_t *e;
+    ~EvGuard() {
+      for (int i = 0; i < 5; ++i) cudaEventDestroy(e[i]);
+    }
+  } guard{ev};
+  SPB_CUDA(cudaEventRecord(ev[0], c.stream));
+  Tree t;
+  try {
+    build_tree(c, points, n, dim, true, width, t);
+  } catch (const InvalidArgument &) {
+    throw InvalidArgument("dbscan: non-finite coordinate");
+  }
+  SPB_CUDA(cudaEventRecord(ev[1], c.stream));
+  DevBuf<float> sph((size_t)n * (dim + 1), c.stream);
+  k_point_spheres<<<grid_for(n, 256, 148 * 16), 256, 0, c.stream>>>(points, n, dim, eps, sph.get());
+  SPB_LAUNCHED();
+  DevBuf<int64_t> off((size_t)n + 1, c.stream);
+  const int64_t total = range_crs(c, t, RQ_SPHERES, sph.get(), n, off.get(), nullptr, 0);
+  if (total > max_adjacency) throw CapacityError();
+  DevBuf<int32_t> val((size_t)std::max<int64_t>(total, 1), c.stream);
+  range_crs(c, t, RQ_SPHERES, sph.get(), n, off.get(), val.get(), total);
+  SPB_CUDA(cudaEventRecord(ev[2], c.stream));
+  DevBuf<int32_t> parent((size_t)n, c.stream);
+  k_iota<<<grid_for(n, 256, 148 * 16), 256, 0, c.stream>>>(parent.get(), n);
+  SPB_LAUNCHED();
+  k_adjacency_unions<<<(unsigned)((n + 127) / 128), 128, 0, c.stream>>>(n, off.get(), val.get(), parent.get(), core);
+  SPB_LAUNCHED();
+  SPB_CUDA(cudaEventRecord(ev[3], c.stream));
+  k_adjacency_labels<<<grid_for(n, 256, 148 * 16), 256, 0, c.stream>>>(n, parent.get(), core, labels);
+  SPB_LAUNCHED();
+  SPB_CUDA(cudaEventRecord(ev[4], c.stream));
+  SPB_CUDA(cudaEventSynchronize(ev[4]));
+  if (res) {
+    for (int i = 0; i < 4; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      res->ms[i] = ms;
+    }
+  }
+}
+
+}  // namespace spb

@@ -504,3 +504,118 @@ void walk_lengths(Ctx &c, const Tree &t, float eps, int32_t *steps, int32_t *hit
 }
 
 }  // namespace spb
+
+namespace spb {
+
+// ---------------------------------------------------------------------------
+// check_equivalence (verify.hpp:21-61) on the device.  violation codes:
+// 1 core flag, 2 noise, 3 core partition (one reference cluster split),
+// 4 core clusters merged, 5 border point without an in-cluster core point
+// within eps.  The border test walks the point tree (early exit on the first
+// qualifying core point) instead of the reference's O(n^2) scan.
+// ---------------------------------------------------------------------------
+__global__ void k_eq_flags(int64_t n, const int32_t *__restrict__ gl, const uint8_t *__restrict__ gc,
+                           const int32_t *__restrict__ wl, const uint8_t *__restrict__ wc,
+                           unsigned long long *__restrict__ first) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    if ((gc[i] != 0) != (wc[i] != 0)) atomicMin(&first[0], (unsigned long long)i);
+    if ((gl[i] == -1) != (wl[i] == -1)) atomicMin(&first[1], (unsigned long long)i);
+  }
+}
+
+// (want, got) label pairs of core points, packed for sorting
+__global__ void k_eq_pairs(int64_t n, const int32_t *__restrict__ gl, const int32_t *__restrict__ wl,
+                           const uint8_t *__restrict__ wc, uint64_t *__restrict__ fwd, uint64_t *__restrict__ rev,
+                           uint32_t *__restrict__ idx) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const bool c = wc[i] != 0;
+    fwd[i] = c ? ((uint64_t)(uint32_t)wl[i] << 32) | (uint32_t)gl[i] : ~0ull;
+    rev[i] = c ? ((uint64_t)(uint32_t)gl[i] << 32) | (uint32_t)wl[i] : ~0ull;
+    idx[i] = (uint32_t)i;
+  }
+}
+
+// sorted pairs: equal high words with different low words violate the map
+__global__ void k_eq_bijective(int64_t n, const uint64_t *__restrict__ s, const uint32_t *__restrict__ idx,
+                               unsigned long long *__restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n; i += stride) {
+    const uint64_t a = s[i], b = s[i + 1];
+    if (b == ~0ull) continue;
+    if ((a >> 32) == (b >> 32) && (uint32_t)a != (uint32_t)b) {
+      const uint32_t x = idx[i], y = idx[i + 1];
+      atomicMin(out, (unsigned long long)(x > y ? x : y));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) k_eq_border(const float4 *__restrict__ nodes, const float4 *__restrict__ leafpt,
+                                                   const int32_t *__restrict__ perm, int64_t n, Radius R,
+                                                   const int32_t *__restrict__ gl, const uint8_t *__restrict__ gc,
+                                                   unsigned long long *__restrict__ out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int32_t b = perm[p];
+  if (gc[b] || gl[b] == -1) return;
+  const float4 me = ld_node(leafpt, p);
+  const int32_t lab = gl[b];
+  int32_t cur = 0;
+  bool ok = false;
+  while (cur != kSentinel && !ok) {
+    if (cur >= n - 1) {
+      const float4 L = ld_node(leafpt, cur - (n - 1));
+      if (hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z)) {
+        const int32_t c = perm[cur - (n - 1)];
+        ok = gc[c] && gl[c] == lab;
+      }
+      cur = __float_as_int(L.w);
+    } else {
+      const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+      cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
+    }
+  }
+  if (!ok) atomicMin(out, (unsigned long long)b);
+}
+
+int64_t check_equivalence(Ctx &c, const float *pts, int64_t n, int dim, float eps, const int32_t *gl,
+                          const uint8_t *gc, const int32_t *wl, const uint8_t *wc, int *kind) {
+  *kind = 0;
+  if (n <= 0) return -1;
+  DevBuf<unsigned long long> first(5, c.stream);
+  SPB_CUDA(cudaMemsetAsync(first.get(), 0xff, 5 * sizeof(unsigned long long), c.stream));
+  const unsigned G = grid_for(n, 256, 148 * 16);
+  k_eq_flags<<<G, 256, 0, c.stream>>>(n, gl, gc, wl, wc, first.get());
+  SPB_LAUNCHED();
+  {
+    DevBuf<uint64_t> f0((size_t)n, c.stream), r0((size_t)n, c.stream), t((size_t)n, c.stream);
+    DevBuf<uint32_t> i0((size_t)n, c.stream), i1((size_t)n, c.stream), j0((size_t)n, c.stream);
+    k_eq_pairs<<<G, 256, 0, c.stream>>>(n, gl, wl, wc, f0.get(), r0.get(), i0.get());
+    SPB_LAUNCHED();
+    SPB_CUDA(cudaMemcpyAsync(j0.get(), i0.get(), (size_t)n * 4, cudaMemcpyDeviceToDevice, c.stream));
+    for (int which = 0; which < 2; ++which) {
+      uint64_t *ka = which ? r0.get() : f0.get(), *kb = t.get();
+      uint32_t *va = which ? j0.get() : i0.get(), *vb = i1.get();
+      radix_sort_pairs(c, &ka, &va, &kb, &vb, n, 64, false);
+      k_eq_bijective<<<G, 256, 0, c.stream>>>(n, ka, va, first.get() + 2 + which);
+      SPB_LAUNCHED();
+    }
+  }
+  Tree t;
+  build_tree(c, pts, n, dim, true, 64, t);
+  k_eq_border<<<(unsigned)((n + 127) / 128), 128, 0, c.stream>>>(t.nodes, t.leafpt, t.perm, n, make_radius(eps), gl,
+                                                                   gc, first.get() + 4);
+  SPB_LAUNCHED();
+  unsigned long long h[5];
+  SPB_CUDA(cudaMemcpyAsync(h, first.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  for (int k = 0; k < 5; ++k)
+    if (h[k] != ~0ull) {
+      *kind = k + 1;
+      return (int64_t)h[k];
+    }
+  return -1;
+}
+
+}  // namespace spb

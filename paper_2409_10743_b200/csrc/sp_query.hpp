@@ -22,6 +22,9 @@ int64_t pair_list(Ctx &c, const Tree &t, float eps, int32_t *pairs, int64_t capa
 void knn(Ctx &c, const Tree &t, const float *origins, int64_t nq, int32_t k, int32_t *idx, float *dist);
 void exclusive_scan(Ctx &c, const int32_t *in, int64_t n, int64_t *out);
 void walk_lengths(Ctx &c, const Tree &t, float eps, int32_t *steps, int32_t *hits);
+// -1 if equivalent, else the first violating point (kind 1..5, see sp_b200.h)
+int64_t check_equivalence(Ctx &c, const float *pts, int64_t n, int dim, float eps, const int32_t *gl,
+                          const uint8_t *gc, const int32_t *wl, const uint8_t *wc, int *kind);
 
 struct DbscanResult {
   double ms[4] = {0, 0, 0, 0};  // build, core, merge, finalize
@@ -30,6 +33,9 @@ struct DbscanResult {
 // labels/core: device arrays of n entries (original point order).
 void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t min_pts, int algo, int width,
             int32_t *labels, uint8_t *core, DbscanResult *res);
+
+void adjacency_dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int width, int64_t max_adjacency,
+                      int32_t *labels, uint8_t *core, DbscanResult *res);
 
 void generate_field(Ctx &c, int64_t n_total, int64_t first, int64_t count, uint64_t seed, float *out);
 void generate_uniform(Ctx &c, int64_t n, int dim, uint64_t seed, float *out);

@@ -132,3 +132,18 @@ def test_c1_labels_hash(sp, oracle):
     assert fnv1a64(out.labels) == g["labels_hash"]
     assert fnv1a64(out.core_flags) == g["core_hash"]
     assert summarize(out.labels, out.core_flags) == (g["clusters"], g["noise"], g["core"])
+
+
+def test_adjacency_graph_dbscan_equals_fof_and_overflows(sp, oracle):
+    # test_dbscan.cpp:306-338: legacy == FoF; the CRS cap raises CapacityError
+    rng = np.random.default_rng(8)
+    for dim in (2, 3):
+        p = rng.random((20000, dim), dtype=np.float32)
+        a = sp.adjacency_graph_dbscan(p, 0.01)
+        b = sp.friends_of_friends(p, 0.01)
+        assert np.array_equal(a.labels, b.labels) and np.array_equal(a.core_flags, b.core_flags)
+    with pytest.raises(sp.CapacityError):
+        sp.adjacency_graph_dbscan(p, 0.01, max_adjacency=100)
+    c = dbscan_cases()["uniform3_fof"]
+    out = sp.adjacency_graph_dbscan(c["points"], float(c["eps"]))
+    assert np.array_equal(out.labels, c["labels"])

@@ -90,3 +90,45 @@ def test_c3_full_size(sp, oracle):
     assert out.stats.distance_checks == g["distance_checks"]
     assert summarize(out.labels, out.core_flags) == (g["clusters"], g["noise"], g["core"])
     assert fnv1a64(out.core_flags) == g["core_hash"]
+
+
+def test_device_check_equivalence_matches_oracle_checker(sp, oracle):
+    # verify.hpp:21-61 on the device, incl. the fault-injection cases of
+    # test_dbscan.cpp:340-404
+    c = dbscan_cases()["clustered3_m4"]
+    pts, eps = c["points"], float(c["eps"])
+    want = sp.DbscanOutput(c["labels"], c["core"])
+    got = sp.fdbscan(pts, sp.DbscanParams(eps, 4))
+    assert sp.check_equivalence(pts, eps, got, want) is None
+    core = c["core"].copy()
+    core[int(np.argmax(core))] ^= 1
+    assert "core flag" in sp.check_equivalence(pts, eps, sp.DbscanOutput(c["labels"], core), want)
+    lab = c["labels"].copy()
+    i = int(np.argmax(lab == -1))
+    lab[i] = lab[int(np.argmax(c["core"]))]
+    assert sp.check_equivalence(pts, eps, sp.DbscanOutput(lab, c["core"]), want) is not None
+    # merge two reference clusters into one
+    lab = c["labels"].copy()
+    cl = np.unique(lab[c["core"] == 1])
+    lab[lab == cl[1]] = cl[0]
+    msg = sp.check_equivalence(pts, eps, sp.DbscanOutput(lab, c["core"]), want)
+    assert msg is not None and "merged" in msg
+    # a border point relabelled to a far cluster
+    lab = c["labels"].copy()
+    border = np.where((c["core"] == 0) & (lab >= 0))[0]
+    if len(border):
+        far = [x for x in cl if x != lab[border[0]]][-1]
+        lab[border[0]] = far
+        msg = sp.check_equivalence(pts, eps, sp.DbscanOutput(lab, c["core"]), want)
+        assert msg is not None and "border" in msg
+
+
+def test_c3_densebox_equivalent_to_fdbscan_at_full_size(sp):
+    import torch
+    n = 1 << 26
+    p = sp.generate_field(n, seed=7)
+    eps = eps_for(n)
+    a = sp.fdbscan_densebox(p, sp.DbscanParams(eps, 5))
+    b = sp.fdbscan(p, sp.DbscanParams(eps, 5))
+    assert bool(torch.equal(a.core_flags, b.core_flags))
+    assert sp.check_equivalence(p, eps, a, b) is None
