@@ -177,6 +177,12 @@ int sp_dbscan(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, i
 int sp_dbscan_adjacency(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, int code_width,
                         int64_t max_adjacency, int32_t *labels, uint8_t *core, sp_timings *timings, int mem);
 
+/* dbscan_reference (dbscan.hpp:188-222): brute-force O(n^2) DBSCAN on the
+ * device, independent of the tree — the reference CLI's --verify / --algo
+ * oracle counterpart, for small inputs. */
+int sp_dbscan_bruteforce(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, int32_t min_pts,
+                         int32_t *labels, uint8_t *core, int mem);
+
 /* check_equivalence (verify.hpp:21-61): *violation = -1 when `got` is an
  * equivalent clustering of `want`, else the index of the first violating
  * point with *kind = 1 core flag, 2 noise, 3 core partition split, 4 core
@@ -194,6 +200,12 @@ int sp_check_equivalence(sp_ctx *ctx, const float *points, int64_t n, int dim, f
  * can be produced independently (out: float[count*3], device or host). */
 int sp_generate_field(sp_ctx *ctx, int64_t n_total, int64_t first, int64_t count, uint64_t seed, float *out,
                       int mem);
+/* The reference's generators (generate.cpp:17-66) with the same engine and
+ * distributions (std::mt19937_64, uniform_real / normal <double>), so specs
+ * reproduce its bits: kind 0 uniform(n, dim, extent), kind 1
+ * gaussian_clusters(n, dim, k, sigma, extent, seed).  Host memory. */
+int sp_generate_reference(int kind, int64_t n, int dim, int32_t k, double sigma, double extent, uint64_t seed,
+                          float *out);
 /* Uniform points in [0,1)^dim from the same Philox stream. */
 int sp_generate_uniform(sp_ctx *ctx, int64_t n, int dim, uint64_t seed, float *out, int mem);
 

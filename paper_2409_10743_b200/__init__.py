@@ -37,7 +37,8 @@ from . import build as _build
 __all__ = [
     "Bvh", "DbscanOutput", "DbscanParams", "DbscanTimings", "DbscanStats", "InvalidArgument", "CapacityError",
     "CudaError", "range_count", "query_crs", "nearest_query", "pair_traversal", "sort_queries", "morton_codes",
-    "fdbscan", "friends_of_friends", "fdbscan_densebox", "adjacency_graph_dbscan", "check_equivalence", "generate_field", "generate_uniform",
+    "fdbscan", "friends_of_friends", "fdbscan_densebox", "adjacency_graph_dbscan", "dbscan_reference",
+    "check_equivalence", "generate_reference_uniform", "generate_reference_gaussian", "generate_field", "generate_uniform",
     "Context",
     "default_context", "library_path",
 ]
@@ -96,6 +97,8 @@ def _load() -> C.CDLL:
         "sp_sort_queries": (C.c_int, [vp, vp, i64, C.c_int, vp, C.c_int]),
         "sp_morton_codes": (C.c_int, [vp, vp, i64, C.c_int, C.c_int, C.c_int, vp, C.c_int]),
         "sp_dbscan": (C.c_int, [vp, vp, i64, C.c_int, f32, i32, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int]),
+        "sp_dbscan_bruteforce": (C.c_int, [vp, vp, i64, C.c_int, f32, i32, vp, vp, C.c_int]),
+        "sp_generate_reference": (C.c_int, [C.c_int, i64, C.c_int, i32, C.c_double, C.c_double, C.c_uint64, vp]),
         "sp_dbscan_adjacency": (C.c_int, [vp, vp, i64, C.c_int, f32, C.c_int, i64, vp, vp, vp, C.c_int]),
         "sp_check_equivalence": (C.c_int, [vp, vp, i64, C.c_int, f32, vp, vp, vp, vp, C.POINTER(i64),
                                            C.POINTER(C.c_int), C.c_int]),
@@ -545,6 +548,36 @@ def adjacency_graph_dbscan(points, eps: float, width: int = 64, max_adjacency: O
     cap = (1 << 62) if max_adjacency is None else int(max_adjacency)
     ctx._check(_lib.sp_dbscan_adjacency(ctx.h, p, n, dim, C.c_float(eps), int(width), cap, lp, cp, C.byref(t), mem))
     return DbscanOutput(labels, core, DbscanTimings(t.build_ms, t.core_ms, t.merge_ms, t.finalize_ms))
+
+
+def dbscan_reference(points, params: DbscanParams, ctx: Optional[Context] = None) -> DbscanOutput:
+    """dbscan_reference (dbscan.hpp:188-222): brute-force O(n^2) DBSCAN on the
+    device, independent of the tree (for verification of small inputs)."""
+    ctx = ctx or default_context()
+    dim = _dim_of(points)
+    n = int(points.shape[0])
+    p, mem, keep = _in(points, np.float32)
+    dev = mem == SP_MEM_DEVICE
+    labels, lp = _out(dev, (n,), np.int32, _torch_dtype("int32") if dev else None, points.device if dev else None)
+    core, cp = _out(dev, (n,), np.uint8, _torch_dtype("uint8") if dev else None, points.device if dev else None)
+    ctx._check(_lib.sp_dbscan_bruteforce(ctx.h, p, n, dim, C.c_float(params.eps), int(params.min_pts), lp, cp, mem))
+    return DbscanOutput(labels, core)
+
+
+def generate_reference_uniform(n: int, dim: int = 3, extent: float = 1.0, seed: int = 0) -> np.ndarray:
+    """generate(UniformSpec) (generate.cpp:17-31), bit-identical."""
+    out = np.empty(max(n * dim, 1), np.float32)
+    if _lib.sp_generate_reference(0, n, dim, 1, 0.0, extent, seed, out.ctypes.data_as(C.c_void_p)) != SP_OK:
+        raise InvalidArgument("generate: bad uniform spec")
+    return out[: n * dim].reshape(n, dim)
+
+
+def generate_reference_gaussian(n: int, dim: int, k: int, sigma: float, extent: float, seed: int) -> np.ndarray:
+    """generate(GaussianClustersSpec) (generate.cpp:33-66), bit-identical."""
+    out = np.empty(max(n * dim, 1), np.float32)
+    if _lib.sp_generate_reference(1, n, dim, k, sigma, extent, seed, out.ctypes.data_as(C.c_void_p)) != SP_OK:
+        raise InvalidArgument("generate: bad gaussian_clusters spec")
+    return out[: n * dim].reshape(n, dim)
 
 
 def check_equivalence(points, eps: float, got: DbscanOutput, want: DbscanOutput, ctx: Optional[Context] = None):

@@ -544,6 +544,20 @@ int sp_dbscan_adjacency(sp_ctx *ctx, const float *points, int64_t n, int dim, fl
   });
 }
 
+int sp_dbscan_bruteforce(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, int32_t min_pts,
+                         int32_t *labels, uint8_t *core, int mem) {
+  return guarded(ctx, [&](spb::Ctx &c) {
+    check_dim(dim);
+    In<float> p(c, points, (size_t)n * dim, mem);
+    Out<int32_t> ol(c, labels, (size_t)n, mem);
+    Out<uint8_t> oc(c, core, (size_t)n, mem);
+    spb::bruteforce_dbscan(c, p.p, n, dim, eps, min_pts, ol.p, oc.p);
+    ol.flush(c);
+    oc.flush(c);
+    finish(c);
+  });
+}
+
 int sp_generate_field(sp_ctx *ctx, int64_t n_total, int64_t first, int64_t count, uint64_t seed, float *out,
                       int mem) {
   return guarded(ctx, [&](spb::Ctx &c) {

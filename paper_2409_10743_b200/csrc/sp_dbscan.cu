@@ -316,3 +316,83 @@ void adjacency_dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps
 }
 
 }  // namespace spb
+
+namespace spb {
+
+// ---------------------------------------------------------------------------
+// dbscan_reference (dbscan.hpp:188-222) on the device: brute-force O(n^2)
+// neighbourhoods, exact core flags, core-core unions, and each border point
+// claimed by one core neighbour.  Independent of the tree; the CLI's
+// --verify / --algo oracle counterpart (intended for small n).
+// ---------------------------------------------------------------------------
+__global__ void k_bf_core(const float4 *__restrict__ p4, int64_t n, Radius R, int32_t min_pts,
+                          uint8_t *__restrict__ core) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 a = p4[i];
+  int32_t c = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    const float4 b = p4[j];
+    c += hit_point(R, a.x, a.y, a.z, b.x, b.y, b.z);
+  }
+  core[i] = c >= min_pts;
+}
+
+__global__ void k_bf_merge(const float4 *__restrict__ p4, int64_t n, Radius R, const uint8_t *__restrict__ core,
+                           int32_t *parent, uint32_t *claims) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !core[i]) return;
+  const float4 a = p4[i];
+  int32_t root = (int32_t)i;
+  for (int64_t j = 0; j < n; ++j) {
+    if (j == i) continue;
+    const float4 b = p4[j];
+    if (!hit_point(R, a.x, a.y, a.z, b.x, b.y, b.z)) continue;
+    if (core[j]) {
+      if (j > i) root = uf_union(parent, root, (int32_t)j);
+    } else {
+      const uint32_t bit = 1u << (j & 31);
+      if (!(atomicOr(&claims[j >> 5], bit) & bit)) root = uf_union(parent, root, (int32_t)j);
+    }
+  }
+}
+
+__global__ void k_bf_points(const float *__restrict__ pts, int64_t n, int dim, float4 *__restrict__ p4) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    p4[i] = make_float4(pts[i * dim], pts[i * dim + 1], dim == 3 ? pts[i * dim + 2] : 0.f, 0.f);
+}
+
+__global__ void k_bf_labels(int64_t n, const int32_t *__restrict__ parent, const uint8_t *__restrict__ core,
+                            const uint32_t *__restrict__ claims, int32_t *__restrict__ labels) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const bool member = core[i] || ((claims[i >> 5] >> (i & 31)) & 1u);
+    labels[i] = member ? uf_root(parent, (int32_t)i) : -1;
+  }
+}
+
+void bruteforce_dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t min_pts, int32_t *labels,
+                       uint8_t *core) {
+  if (!(eps > 0.f) || !std::isfinite(eps)) throw InvalidArgument("dbscan: eps must be positive and finite");
+  if (min_pts < 2) throw InvalidArgument("dbscan: min_pts must be at least 2");
+  if (n == 0) return;
+  const Radius R = make_radius(eps);
+  DevBuf<float4> p4((size_t)n, c.stream);
+  DevBuf<int32_t> parent((size_t)n, c.stream);
+  DevBuf<uint32_t> claims((size_t)((n + 31) / 32), c.stream);
+  const unsigned G = grid_for(n, 256, 148 * 16), Gq = (unsigned)((n + 127) / 128);
+  k_bf_points<<<G, 256, 0, c.stream>>>(points, n, dim, p4.get());
+  SPB_LAUNCHED();
+  SPB_CUDA(cudaMemsetAsync(claims.get(), 0, claims.n * sizeof(uint32_t), c.stream));
+  k_iota<<<G, 256, 0, c.stream>>>(parent.get(), n);
+  SPB_LAUNCHED();
+  k_bf_core<<<Gq, 128, 0, c.stream>>>(p4.get(), n, R, min_pts, core);
+  SPB_LAUNCHED();
+  k_bf_merge<<<Gq, 128, 0, c.stream>>>(p4.get(), n, R, core, parent.get(), claims.get());
+  SPB_LAUNCHED();
+  k_bf_labels<<<G, 256, 0, c.stream>>>(n, parent.get(), core, claims.get(), labels);
+  SPB_LAUNCHED();
+}
+
+}  // namespace spb

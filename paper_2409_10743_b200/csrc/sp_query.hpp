@@ -37,6 +37,9 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
 void adjacency_dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int width, int64_t max_adjacency,
                       int32_t *labels, uint8_t *core, DbscanResult *res);
 
+void bruteforce_dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t min_pts, int32_t *labels,
+                       uint8_t *core);
+
 void generate_field(Ctx &c, int64_t n_total, int64_t first, int64_t count, uint64_t seed, float *out);
 void generate_uniform(Ctx &c, int64_t n, int dim, uint64_t seed, float *out);
 
