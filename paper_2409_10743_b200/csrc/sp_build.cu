@@ -388,16 +388,19 @@ void onesweep_passes(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_a
   DevBuf<unsigned long long> lookback((size_t)ntiles * RS_BINS, c.stream);
   SPB_CUDA(cudaMemsetAsync(hist.get(), 0, hist.n * sizeof(uint32_t), c.stream));
   SPB_CUDA(cudaMemsetAsync(lookback.get(), 0, lookback.n * sizeof(unsigned long long), c.stream));
+  if (getenv("SPB_SORT_MARKS")) mark(c, "sort_setup");
   k_rs_hist<<<grid_for(n, 256, 148 * 4), 256, 0, c.stream>>>(*keys, n, npass, hist.get());
   SPB_LAUNCHED();
   k_rs_scan<<<npass, RS_BINS, 0, c.stream>>>(hist.get());
   SPB_LAUNCHED();
+  if (getenv("SPB_SORT_MARKS")) mark(c, "sort_hist");
   uint32_t *ctr = hist.get() + (size_t)npass * RS_BINS;
   for (int p = 0; p < npass; ++p) {
     k_rs_onesweep<ITEMS><<<(unsigned)ntiles, RS_THREADS, SMEM, c.stream>>>(
         *keys, (p == 0 && vals_iota) ? nullptr : *vals, *keys_alt, *vals_alt, n, 8 * p,
         hist.get() + (size_t)p * RS_BINS, lookback.get(), ctr + p, (uint32_t)(2 * p + 1));
     SPB_LAUNCHED();
+    if (getenv("SPB_SORT_MARKS")) mark(c, "sort_pass");
     std::swap(*keys, *keys_alt);
     std::swap(*vals, *vals_alt);
   }
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(256) k_delta(const uint64_t *__restrict__ sk, 
     uint64_t a = sk[i], b = sk[i + 1];
     int d;
     if (a != b) d = __clzll((long long)(a ^ b)) - (64 - width);
-    else d = width + __clz((int)(sv[i] ^ sv[i + 1]));
+    else d = width + __clz((int)(sv ? sv[i] ^ sv[i + 1] : (uint32_t)(i ^ (i + 1))));
     delta[i] = d;
   }
 }
@@ -504,8 +507,8 @@ __global__ void __launch_bounds__(256) k_hierarchy(int64_t n, const int32_t *__r
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   HierView H{n, delta};
-  const uint32_t oi = perm[p];
-  perm_out[p] = (int32_t)oi;
+  const uint32_t oi = perm ? perm[p] : (uint32_t)p;
+  if (perm_out) perm_out[p] = (int32_t)oi;
   const int sz = POINTS ? dim : 2 * dim;
   const float *o = obj + (int64_t)oi * sz;
   float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f};
@@ -573,6 +576,26 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
                                                 nullptr);
   SPB_LAUNCHED();
   mark(c, "hierarchy");
+}
+
+void build_sorted_hierarchy(Ctx &c, const uint64_t *keys, int64_t m, int dim, const float *boxes, Tree &t) {
+  t.n = m;
+  t.dim = dim;
+  t.width = 64;
+  t.points = false;
+  t.stream = c.stream;
+  if (m == 0) return;
+  SPB_CUDA(cudaMallocAsync(&t.nodes, (size_t)(2 * m - 1) * 2 * sizeof(float4), c.stream));
+  SPB_CUDA(cudaMallocAsync(&t.perm, (size_t)m * sizeof(int32_t), c.stream));
+  DevBuf<int32_t> delta(m > 1 ? m - 1 : 1, c.stream), flags(m > 1 ? m - 1 : 1, c.stream);
+  if (m > 1) {
+    k_delta<<<grid_for(m, 256, 148 * 16), 256, 0, c.stream>>>(keys, nullptr, m, 64, delta.get());
+    SPB_LAUNCHED();
+    SPB_CUDA(cudaMemsetAsync(flags.get(), 0xff, (size_t)(m - 1) * sizeof(int32_t), c.stream));
+  }
+  k_hierarchy<false><<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(m, delta.get(), nullptr, boxes, dim, t.nodes,
+                                                                        flags.get(), t.perm, nullptr);
+  SPB_LAUNCHED();
 }
 
 void sort_points(Ctx &c, const float *pts, int64_t n, int dim, int32_t *order) {

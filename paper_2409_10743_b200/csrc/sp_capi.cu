@@ -38,49 +38,75 @@ void stream_after(cudaStream_t waiter, cudaStream_t producer) {
   SPB_CUDA(cudaEventDestroy(e));
 }
 
-// Input array: device pointer as-is, or a device copy of a host array
-// (uploaded on the H2D stream, released in compute-stream order).
+spb::Ctx::Staging &stage(spb::Ctx &c, bool input, size_t bytes) {
+  const int parity = (int)(c.calls & 1);
+  int &used = input ? c.in_used : c.out_used;
+  if (used >= 8) throw spb::CudaError("too many host arrays in one call");
+  spb::Ctx::Staging &s = (input ? c.in_stage : c.out_stage)[parity][used++];
+  if (!s.done) SPB_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+  if (s.cap < bytes) {
+    // grow (rare): make sure nobody still uses the old block, then replace it
+    SPB_CUDA(cudaEventSynchronize(s.done));
+    if (s.p) SPB_CUDA(cudaFree(s.p));
+    s.p = nullptr;
+    s.cap = 0;
+    SPB_CUDA(cudaMalloc(&s.p, bytes));
+    s.cap = bytes;
+  }
+  return s;
+}
+
+// Input array: device pointer as-is, or a device copy of a host array in a
+// double-buffered staging slot, uploaded on the H2D stream once the slot's
+// previous consumer (two calls ago) has finished.
 template <class T>
 struct In {
-  DevBuf<T> buf;
   const T *p = nullptr;
+  spb::Ctx::Staging *st = nullptr;
+  spb::Ctx *ctx = nullptr;
   In(spb::Ctx &c, const T *src, size_t count, int mem) {
     if (!src || count == 0) return;
     if (mem == SP_MEM_DEVICE) {
       p = src;
       return;
     }
-    buf = DevBuf<T>(count, c.h2d);
-    SPB_CUDA(cudaMemcpyAsync(buf.get(), src, count * sizeof(T), cudaMemcpyHostToDevice, c.h2d));
+    st = &stage(c, true, count * sizeof(T));
+    ctx = &c;
+    SPB_CUDA(cudaStreamWaitEvent(c.h2d, st->done, 0));
+    SPB_CUDA(cudaMemcpyAsync(st->p, src, count * sizeof(T), cudaMemcpyHostToDevice, c.h2d));
     stream_after(c.stream, c.h2d);
-    buf.s = c.stream;
-    p = buf.get();
+    p = static_cast<const T *>(st->p);
+  }
+  ~In() {
+    if (st) cudaEventRecord(st->done, ctx->stream);  // consumed by this call's kernels
   }
 };
 
-// Output array: device pointer as-is, or a device scratch downloaded by
-// flush() on the D2H stream once the compute stream has produced it.
+// Output array: device pointer as-is, or a staging slot the kernels write
+// (after its previous download finished) and flush() downloads on the D2H
+// stream once the compute stream has produced it.
 template <class T>
 struct Out {
-  DevBuf<T> buf;
   T *p = nullptr;
   T *host = nullptr;
   size_t count = 0;
+  spb::Ctx::Staging *st = nullptr;
   Out(spb::Ctx &c, T *dst, size_t n, int mem) : count(n) {
     if (!dst || n == 0) return;
     if (mem == SP_MEM_DEVICE) {
       p = dst;
       return;
     }
-    buf = DevBuf<T>(n, c.stream);
-    p = buf.get();
+    st = &stage(c, false, n * sizeof(T));
+    SPB_CUDA(cudaStreamWaitEvent(c.stream, st->done, 0));
+    p = static_cast<T *>(st->p);
     host = dst;
   }
   void flush(spb::Ctx &c) {
     if (!host) return;
     stream_after(c.d2h, c.stream);
-    SPB_CUDA(cudaMemcpyAsync(host, buf.get(), count * sizeof(T), cudaMemcpyDeviceToHost, c.d2h));
-    buf.s = c.d2h;
+    SPB_CUDA(cudaMemcpyAsync(host, st->p, count * sizeof(T), cudaMemcpyDeviceToHost, c.d2h));
+    SPB_CUDA(cudaEventRecord(st->done, c.d2h));
   }
 };
 
@@ -103,6 +129,8 @@ int guarded(sp_ctx *ctx, F &&f) {
   DeviceGuard dg(ctx->c.device);
   spb::g_launch_counter = &ctx->c.launches;
   spb::reset_marks(ctx->c);
+  ctx->c.in_used = ctx->c.out_used = 0;
+  ++ctx->c.calls;
   int rc = SP_OK;
   try {
     f(ctx->c);
@@ -195,6 +223,12 @@ int sp_ctx_destroy(sp_ctx *ctx) {
     if (ctx->c.h2d) cudaStreamDestroy(ctx->c.h2d);
     if (ctx->c.d2h) cudaStreamDestroy(ctx->c.d2h);
     if (ctx->c.d_err) cudaFree(ctx->c.d_err);
+    for (auto *arr : {&ctx->c.in_stage, &ctx->c.out_stage})
+      for (auto &row : *arr)
+        for (auto &st : row) {
+          if (st.p) cudaFree(st.p);
+          if (st.done) cudaEventDestroy(st.done);
+        }
     if (ctx->c.owns_stream) cudaStreamDestroy(ctx->c.stream);
   }
   delete ctx;

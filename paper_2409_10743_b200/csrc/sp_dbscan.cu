@@ -156,6 +156,11 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
   if (algo == 1) min_pts = 2;
   if (min_pts < 2) throw InvalidArgument("dbscan: min_pts must be at least 2");
   if (n == 0) return;
+  if (min_pts == 2 && !getenv("SPB_FOF_POINTS")) {
+    // friends-of-friends over grid cells (the DenseBox shortcut)
+    extern bool fof_cells(Ctx &, const float *, int64_t, int, float, int32_t *, uint8_t *, DbscanResult *);
+    if (algo != 2 && fof_cells(c, points, n, dim, eps, labels, core, res)) return;
+  }
   if (algo == 2) {
     extern void densebox(Ctx &, const float *, int64_t, int, float, int32_t, int, int32_t *, uint8_t *,
                          DbscanResult *);

@@ -380,6 +380,138 @@ __global__ void k_dense_core(const int32_t *__restrict__ point_cell, int64_t n, 
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) core[i] = point_cell[i] >= 0;
 }
 
+// ---------------------------------------------------------------------------
+// FoF over grid cells (the FDBSCAN-DenseBox dense-cell shortcut
+// applied to friends-of-friends).  With cell length eps/sqrt(d)*(1-1e-6)
+// (dense_grid.hpp:71-103) any two points of a cell are within eps, so a cell
+// is one set from the start.  Points are sorted once by the Morton key of
+// their cell; the LBVH is built over the non-empty cells in that order (tight
+// cell boxes); each cell walks the ropes from its own leaf (later cells only,
+// traversal.hpp:162-184) with a conservative box-box test, skips cells that
+// are already in its set, and otherwise tests member pairs until the first
+// close pair, which unions the two cells.  Labels are canonical, so the result
+// equals the point-based FoF bit for bit.
+// ---------------------------------------------------------------------------
+__global__ void k_cell_ranges(const int64_t *__restrict__ cell_start, int64_t m, int64_t n,
+                              const uint64_t *__restrict__ skeys, const float4 *__restrict__ cpts, int dim,
+                              uint64_t *__restrict__ ckeys, float *__restrict__ boxes, int32_t *__restrict__ cell_of,
+                              uint8_t *__restrict__ multi) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride) {
+    const int64_t s = cell_start[j], e = j + 1 < m ? cell_start[j + 1] : n;
+    float lo[3] = {3.4028235e38f, 3.4028235e38f, 3.4028235e38f};
+    float hi[3] = {-3.4028235e38f, -3.4028235e38f, -3.4028235e38f};
+    for (int64_t k = s; k < e; ++k) {
+      const float4 q = cpts[k];
+      lo[0] = fminf(lo[0], q.x); lo[1] = fminf(lo[1], q.y); lo[2] = fminf(lo[2], q.z);
+      hi[0] = fmaxf(hi[0], q.x); hi[1] = fmaxf(hi[1], q.y); hi[2] = fmaxf(hi[2], q.z);
+      cell_of[k] = (int32_t)j;
+    }
+    for (int k = 0; k < dim; ++k) {
+      boxes[j * 2 * dim + k] = lo[k];
+      boxes[j * 2 * dim + dim + k] = hi[k];
+    }
+    ckeys[j] = skeys[s];
+    multi[j] = (e - s) > 1;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_fof_cells_merge(const float4 *__restrict__ nodes, int64_t m,
+                                                         const int64_t *__restrict__ cell_start, int64_t n,
+                                                         const float4 *__restrict__ cpts, Radius R, int32_t *parent) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= m) return;
+  const int64_t first_leaf = m - 1;
+  const float4 qlo = ld_node(nodes, 2 * (first_leaf + a)), qhi = ld_node(nodes, 2 * (first_leaf + a) + 1);
+  const int64_t sa = cell_start[a], ea = a + 1 < m ? cell_start[a + 1] : n;
+  int32_t root = (int32_t)a;
+  int32_t cur = node_rope(qhi);
+  while (cur != kSentinel) {
+    const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+    bool far;
+    if (R.fast) {
+      far = sq3(fmaxf(fmaxf(__fsub_rn(lo.x, qhi.x), __fsub_rn(qlo.x, hi.x)), 0.f),
+                fmaxf(fmaxf(__fsub_rn(lo.y, qhi.y), __fsub_rn(qlo.y, hi.y)), 0.f),
+                fmaxf(fmaxf(__fsub_rn(lo.z, qhi.z), __fsub_rn(qlo.z, hi.z)), 0.f)) > R.hi32;
+    } else {
+      const double gx = fmax(fmax((double)lo.x - (double)qhi.x, (double)qlo.x - (double)hi.x), 0.0);
+      const double gy = fmax(fmax((double)lo.y - (double)qhi.y, (double)qlo.y - (double)hi.y), 0.0);
+      const double gz = fmax(fmax((double)lo.z - (double)qhi.z, (double)qlo.z - (double)hi.z), 0.0);
+      far = gx * gx + gy * gy + gz * gz > R.thr * (1.0 + 0x1p-30);
+    }
+    if (far) {
+      cur = node_rope(hi);
+      continue;
+    }
+    if (cur < first_leaf) {
+      cur = node_link(lo);
+      continue;
+    }
+    const int32_t b = (int32_t)(cur - first_leaf);
+    if (parent[b] != root) {
+      const int32_t ra = uf_find(parent, root), rb = uf_find(parent, b);
+      root = ra;
+      if (ra != rb) {
+        const int64_t sb = cell_start[b], eb = b + 1 < m ? cell_start[b + 1] : n;
+        bool found = false;
+        for (int64_t i = sa; i < ea && !found; ++i) {
+          const float4 x = cpts[i];
+          for (int64_t j = sb; j < eb; ++j) {
+            const float4 y = cpts[j];
+            if (hit_point(R, x.x, x.y, x.z, y.x, y.y, y.z)) {
+              found = true;
+              break;
+            }
+          }
+        }
+        if (found) root = uf_union(parent, ra, rb);
+      }
+    }
+    cur = node_rope(hi);
+  }
+}
+
+// cells: core iff the cell has two points or its set spans several cells
+__global__ void k_fof_cells_core(int64_t m, int32_t *parent, uint8_t *multi) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= m) return;
+  const int32_t r = uf_root(parent, (int32_t)a);
+  if (r != a) {
+    parent[a] = r;
+    multi[a] = 1;
+    multi[r] = 1;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_fof_cells_minobj(int64_t n, const int32_t *__restrict__ cell_of,
+                                                          const int32_t *__restrict__ parent,
+                                                          const float4 *__restrict__ cpts, int32_t *minobj) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int32_t key = -1, v = 0x7fffffff;
+  if (k < n) {
+    key = uf_root(parent, cell_of[k]);
+    v = __float_as_int(cpts[k].w);
+  }
+  const uint32_t peers = __match_any_sync(0xffffffffu, key);
+  const int32_t mn = (int32_t)__reduce_min_sync(peers, (uint32_t)v);
+  if (key >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicMin(&minobj[key], mn);
+}
+
+__global__ void __launch_bounds__(256) k_fof_cells_labels(int64_t n, const int32_t *__restrict__ cell_of,
+                                                          const int32_t *__restrict__ parent,
+                                                          const uint8_t *__restrict__ multi,
+                                                          const float4 *__restrict__ cpts,
+                                                          const int32_t *__restrict__ minobj,
+                                                          int32_t *__restrict__ labels, uint8_t *__restrict__ core) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int32_t cl = cell_of[k];
+  const int32_t o = __float_as_int(cpts[k].w);
+  const bool c = multi[cl] != 0;
+  labels[o] = c ? minobj[uf_root(parent, cl)] : -1;
+  core[o] = c;
+}
+
 }  // namespace
 
 void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t min_pts, int width, int32_t *labels,
@@ -564,6 +696,111 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
     res->num_dense_points = num_dense_points;
   }
   for (auto &e : ev) cudaEventDestroy(e);
+}
+
+// Returns false (nothing written) when the grid does not apply: coordinates
+// that could saturate (no dense cells in the reference either) or cell
+// coordinates too wide for a 63-bit Morton key.
+bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t *labels, uint8_t *core_out,
+               DbscanResult *res) {
+  const float cell = (float)((double)eps / std::sqrt((double)dim) * (1.0 - 1e-6));
+  if (!(cell > 0.f)) return false;
+  cudaEvent_t ev[5];
+  for (auto &e : ev) SPB_CUDA(cudaEventCreate(&e));
+  struct EvGuard {
+    cudaEvent_t *e;
+    ~EvGuard() {
+      for (int i = 0; i < 5; ++i) cudaEventDestroy(e[i]);
+    }
+  } guard{ev};
+  SPB_CUDA(cudaEventRecord(ev[0], c.stream));
+  mark(c, "start");
+  DevBuf<float> scene(6, c.stream);
+  DevBuf<int> bad(1, c.stream);
+  scene_bounds(c, pts, n, dim, true, scene.get(), bad.get());
+  float hs[6];
+  int hbad = 0;
+  SPB_CUDA(cudaMemcpyAsync(hs, scene.get(), sizeof(hs), cudaMemcpyDeviceToHost, c.stream));
+  SPB_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  if (hbad) throw InvalidArgument("dbscan: non-finite coordinate");
+  int bits = 1;
+  for (int k = 0; k < dim; ++k) {
+    const double extent = (double)hs[3 + k] - (double)hs[k];
+    if (extent / (double)cell >= 4.0e18) return false;
+    const int64_t mc = cell_coord(hs[3 + k], hs[k], cell);
+    while (bits < 63 && (1LL << bits) <= mc) ++bits;
+  }
+  if ((int64_t)bits * dim > 63) return false;
+  mark(c, "bounds");
+  const unsigned G = grid_for(n, 256, 148 * 16);
+  DevBuf<uint64_t> k0((size_t)n, c.stream), k1((size_t)n, c.stream);
+  DevBuf<uint32_t> v0((size_t)n, c.stream), v1((size_t)n, c.stream);
+  k_cell_keys<<<G, 256, 0, c.stream>>>(pts, n, dim, scene.get(), cell, -1, k0.get());
+  SPB_LAUNCHED();
+  mark(c, "morton");
+  uint64_t *ka = k0.get(), *kb = k1.get();
+  uint32_t *va = v0.get(), *vb = v1.get();
+  radix_sort_pairs(c, &ka, &va, &kb, &vb, n, bits * dim, true);
+  mark(c, "sort");
+  DevBuf<float4> cpts((size_t)n, c.stream);
+  k_cell_points<<<G, 256, 0, c.stream>>>(va, pts, n, dim, cpts.get());
+  SPB_LAUNCHED();
+  DevBuf<int32_t> head((size_t)n, c.stream);
+  DevBuf<int64_t> hscan((size_t)n + 1, c.stream);
+  k_heads<<<G, 256, 0, c.stream>>>(ka, va, pts, dim, scene.get(), cell, n, true, head.get());
+  SPB_LAUNCHED();
+  exclusive_scan(c, head.get(), n, hscan.get());
+  int64_t m = 0;
+  SPB_CUDA(cudaMemcpyAsync(&m, hscan.get() + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  DevBuf<int64_t> cell_start((size_t)m, c.stream);
+  k_cell_starts<<<G, 256, 0, c.stream>>>(head.get(), hscan.get(), n, cell_start.get());
+  SPB_LAUNCHED();
+  head.reset();
+  hscan.reset();
+  DevBuf<uint64_t> ckeys((size_t)m, c.stream);
+  DevBuf<float> boxes((size_t)m * 2 * dim, c.stream);
+  DevBuf<int32_t> cell_of((size_t)n, c.stream);
+  DevBuf<uint8_t> multi((size_t)m, c.stream);
+  k_cell_ranges<<<grid_for(m, 256, 148 * 16), 256, 0, c.stream>>>(cell_start.get(), m, n, ka, cpts.get(), dim,
+                                                                   ckeys.get(), boxes.get(), cell_of.get(),
+                                                                   multi.get());
+  SPB_LAUNCHED();
+  Tree t;
+  build_sorted_hierarchy(c, ckeys.get(), m, dim, boxes.get(), t);
+  mark(c, "hierarchy");
+  SPB_CUDA(cudaEventRecord(ev[1], c.stream));
+  SPB_CUDA(cudaEventRecord(ev[2], c.stream));
+  DevBuf<int32_t> parent((size_t)m, c.stream), minobj((size_t)m, c.stream);
+  k_iota32<<<grid_for(m, 256, 148 * 16), 256, 0, c.stream>>>(parent.get(), m);
+  SPB_LAUNCHED();
+  k_fof_cells_merge<<<(unsigned)((m + 127) / 128), 128, 0, c.stream>>>(t.nodes, m, cell_start.get(), n, cpts.get(),
+                                                                       make_radius(eps), parent.get());
+  SPB_LAUNCHED();
+  SPB_CUDA(cudaEventRecord(ev[3], c.stream));
+  mark(c, "merge");
+  k_fof_cells_core<<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(m, parent.get(), multi.get());
+  SPB_LAUNCHED();
+  SPB_CUDA(cudaMemsetAsync(minobj.get(), 0x7f, (size_t)m * sizeof(int32_t), c.stream));
+  k_fof_cells_minobj<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(n, cell_of.get(), parent.get(), cpts.get(),
+                                                                        minobj.get());
+  SPB_LAUNCHED();
+  k_fof_cells_labels<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(n, cell_of.get(), parent.get(), multi.get(),
+                                                                        cpts.get(), minobj.get(), labels, core_out);
+  SPB_LAUNCHED();
+  SPB_CUDA(cudaEventRecord(ev[4], c.stream));
+  mark(c, "finalize");
+  if (c.async()) return true;
+  SPB_CUDA(cudaEventSynchronize(ev[4]));
+  if (res) {
+    for (int i = 0; i < 4; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      res->ms[i] = ms;
+    }
+  }
+  return true;
 }
 
 }  // namespace spb

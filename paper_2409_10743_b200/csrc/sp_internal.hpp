@@ -34,6 +34,19 @@ struct Ctx {
   int *d_err = nullptr;
   cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams for host buffers
   bool async() const { return (flags & 1) != 0; }
+  // Double-buffered device staging for host arrays (per call parity, per
+  // argument position).  A slot is reused two calls later, after the event
+  // recorded when its last consumer (kernels for inputs, the download for
+  // outputs) finished — explicit, so copy streams never wait on unrelated
+  // compute the way cross-stream pool reuse would make them.
+  struct Staging {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t done = nullptr;  // last consumer of this slot
+  };
+  Staging in_stage[2][8], out_stage[2][8];
+  int64_t calls = 0;
+  int in_used = 0, out_used = 0;
 };
 
 // Record a phase boundary on the context stream (cheap; no host sync).
@@ -120,6 +133,9 @@ void radix_sort_pairs(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_
 // Full Bvh::build into `t` (allocates t.nodes/perm/scene). Throws
 // InvalidArgument on non-finite input.
 void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, int width, Tree &t);
+// LBVH over m objects already in key order (strictly increasing keys): leaf p
+// is object p with box boxes[p] (2*dim floats); no sort, identity permutation.
+void build_sorted_hierarchy(Ctx &c, const uint64_t *keys, int64_t m, int dim, const float *boxes, Tree &t);
 // sort_queries: the stable 64-bit Morton order of points against their scene.
 void sort_points(Ctx &c, const float *pts, int64_t n, int dim, int32_t *order);
 
