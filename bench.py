@@ -102,21 +102,27 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # per-kernel algorithmic bytes for the FoF pipeline phases
 # ---------------------------------------------------------------------------
-def phase_bytes(phase: str, n: int, pairs_per_pt: float, key_bits: int = 63) -> float:
+def phase_bytes(phase: str, n: int, cells: int, key_bits: int) -> float:
+    """Algorithmic bytes of one FoF step's phases: n points,
+    `cells` non-empty grid cells, `key_bits` cell-key bits (8-bit digits)."""
     npass = (key_bits + 7) // 8
+    f = cells / float(n)
     per = {
-        "bounds": 12.0,                                 # read xyz
-        "morton": 12.0 + 8.0,                           # read xyz, write code
-        "sort": 8.0 + 20.0 + 24.0 * (npass - 1),        # histogram read; pass 0 (iota values); 12 B in+out/pass
-        "hierarchy": 16.0 + 124.0,                      # delta (2 keys+ids, write) + leaf/internal writes, gathers
-        "merge": 32.0 + 64.0 + 4.0 + 1.0 + 8.0 * pairs_per_pt,  # own leaf, tree once, parent init, flag, unions
-        "finalize": 22.0,
-        "core": 32.0 + 64.0 + 1.0,
+        "bounds": 12.0,                                   # read xyz
+        "morton": 12.0 + 8.0,                             # read xyz, write cell key
+        "sort": 8.0 + 20.0 + 24.0 * (npass - 1),          # histogram read; pass 0 (iota values); 12 B in+out/pass
+        # gather sorted points (perm 4 + xyz 12 + write 16), cell heads (keys 8 + write 4), scan (4 + 8),
+        # cell ranges (points 16 + cell_of 4) + per cell: key 8 + box 24 + starts 8 + hierarchy 140
+        "hierarchy": 4 + 12 + 16 + 12 + 12 + 20 + (8 + 24 + 8 + 140) * f,
+        # cell tree read once (2 nodes x 32 B per cell), member points 16 B, parent 4 B per cell
+        "merge": 16.0 + (64.0 + 4.0) * f,
+        # cell core flags, per point: cell_of 4 + point 16 + min-index atomics 4 + labels 4 + core 1 + root 4
+        "finalize": 33.0 + 12.0 * f,
     }
     return per.get(phase, 0.0) * n
 
 
-PROFILED = {"merge": "merge_2p27", "sort": "sort_2p27", "hierarchy": "hier_2p27"}
+PROFILED = {"merge": "merge_cells_2p27", "sort": "sort_cells_2p27", "hierarchy": "hier_cells_2p27"}
 
 
 def profiled_traffic(phase: str, n: int):
@@ -201,6 +207,7 @@ def workload_config(args, world):
 # our arm
 # ---------------------------------------------------------------------------
 def run_ours(args, rank, world, local_rank):
+    import numpy as np
     import torch
     import torch.distributed as dist
     import paper_2409_10743_b200 as sp
@@ -230,7 +237,10 @@ def run_ours(args, rank, world, local_rank):
 
     for _ in range(args.warmup):
         step()
-    # close pairs per point (for the merge kernel's byte model), outside timing
+    # workload statistics for the byte models, outside timing: non-empty grid
+    # cells of the FoF pipeline, their key width, and close pairs per point
+    cells = ctx.counter("fof_cells")
+    key_bits = 3 * max(1, int(np.ceil(np.log2(1.0 / (eps / np.sqrt(3.0) * (1 - 1e-6)) + 1))))
     pairs_per_pt = None
     if world == 1:
         b = sp.Bvh.build(pts, ctx=ctx)
@@ -302,7 +312,7 @@ def run_ours(args, rank, world, local_rank):
     roofline = None
     if phases:
         dom = max(phases, key=phases.get)
-        ach_bytes = phase_bytes(dom, n, pairs_per_pt or 0.0)
+        ach_bytes = phase_bytes(dom, n, max(cells, 1), key_bits)
         ach = ach_bytes / (phases[dom] / 1e3) / 1e9
         roofline = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(ach / peak, 4), "traffic": profiled_traffic(dom, n), "peak_source": peak_src,
@@ -337,6 +347,7 @@ def run_ours(args, rank, world, local_rank):
         "bvh_build_mpts_s": (n / (build_ms / 1e3) / 1e6) if build_ms else None,
         "phases_ms": {k: round(v, 3) for k, v in phases.items()},
         "close_pairs_per_point": pairs_per_pt,
+        "fof_cells": cells,
     }
     print(json.dumps(line), flush=True)
 

@@ -94,6 +94,9 @@ int64_t sp_ctx_kernel_launches(const sp_ctx *ctx);
  * milliseconds, e.g. "bounds", "morton", "sort", "hierarchy", "core",
  * "merge", "finalize". */
 int sp_ctx_phase_count(const sp_ctx *ctx);
+/* Diagnostic counter of the last call, -1 if absent (e.g. "fof_cells": the
+ * number of non-empty grid cells the FoF pipeline clustered). */
+int64_t sp_ctx_counter(const sp_ctx *ctx, const char *name);
 const char *sp_ctx_phase_name(const sp_ctx *ctx, int i);
 double sp_ctx_phase_ms(const sp_ctx *ctx, int i);
 

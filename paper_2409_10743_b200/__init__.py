@@ -83,6 +83,7 @@ def _load() -> C.CDLL:
         "sp_last_error": (C.c_char_p, [vp]),
         "sp_ctx_kernel_launches": (i64, [vp]),
         "sp_ctx_phase_count": (C.c_int, [vp]),
+        "sp_ctx_counter": (i64, [vp, C.c_char_p]),
         "sp_ctx_phase_name": (C.c_char_p, [vp, C.c_int]),
         "sp_ctx_phase_ms": (C.c_double, [vp, C.c_int]),
         "sp_bvh_build": (C.c_int, [vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, pp]),
@@ -160,6 +161,10 @@ class Context:
     @property
     def kernel_launches(self) -> int:
         return int(_lib.sp_ctx_kernel_launches(self.h))
+
+    def counter(self, name: str) -> int:
+        """Diagnostic counter of the last call (-1 if absent)."""
+        return int(_lib.sp_ctx_counter(self.h, name.encode()))
 
     def phases(self) -> list:
         """[(name, ms)] device-event phase times of the last call."""

@@ -130,6 +130,7 @@ int guarded(sp_ctx *ctx, F &&f) {
   spb::g_launch_counter = &ctx->c.launches;
   spb::reset_marks(ctx->c);
   ctx->c.in_used = ctx->c.out_used = 0;
+  ctx->c.counters.clear();
   ++ctx->c.calls;
   int rc = SP_OK;
   try {
@@ -276,6 +277,13 @@ int sp_ctx_set_flags(sp_ctx *ctx, int flags) {
 const char *sp_last_error(const sp_ctx *ctx) { return ctx ? ctx->c.last_error.c_str() : "null context"; }
 
 int64_t sp_ctx_kernel_launches(const sp_ctx *ctx) { return ctx ? ctx->c.launches : 0; }
+
+int64_t sp_ctx_counter(const sp_ctx *ctx, const char *name) {
+  if (!ctx || !name) return -1;
+  for (const auto &kv : ctx->c.counters)
+    if (kv.first == name) return kv.second;
+  return -1;
+}
 
 int sp_ctx_phase_count(const sp_ctx *ctx) { return ctx ? (int)ctx->c.phases.size() : 0; }
 

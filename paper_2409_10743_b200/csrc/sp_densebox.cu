@@ -416,6 +416,45 @@ __global__ void k_cell_ranges(const int64_t *__restrict__ cell_start, int64_t m,
   }
 }
 
+__device__ __forceinline__ bool cells_far(const Radius &R, const float4 &qlo, const float4 &qhi, const float4 &lo,
+                                          const float4 &hi) {
+  if (R.fast)
+    return sq3(fmaxf(fmaxf(__fsub_rn(lo.x, qhi.x), __fsub_rn(qlo.x, hi.x)), 0.f),
+               fmaxf(fmaxf(__fsub_rn(lo.y, qhi.y), __fsub_rn(qlo.y, hi.y)), 0.f),
+               fmaxf(fmaxf(__fsub_rn(lo.z, qhi.z), __fsub_rn(qlo.z, hi.z)), 0.f)) > R.hi32;
+  const double gx = fmax(fmax((double)lo.x - (double)qhi.x, (double)qlo.x - (double)hi.x), 0.0);
+  const double gy = fmax(fmax((double)lo.y - (double)qhi.y, (double)qlo.y - (double)hi.y), 0.0);
+  const double gz = fmax(fmax((double)lo.z - (double)qhi.z, (double)qlo.z - (double)hi.z), 0.0);
+  return gx * gx + gy * gy + gz * gz > R.thr * (1.0 + 0x1p-30);
+}
+
+// Union cell a's set (root hint `root`) with leaf cell b's when a member pair
+// is within eps; returns the updated hint.
+__device__ __forceinline__ int32_t cells_leaf(const int64_t *__restrict__ cell_start, int64_t m, int64_t n,
+                                              const float4 *__restrict__ cpts, const Radius &R, int32_t *parent,
+                                              int64_t sa, int64_t ea, int32_t root, int32_t b) {
+  if (parent[b] == root) return root;
+  const int32_t ra = uf_find(parent, root), rb = uf_find(parent, b);
+  if (ra == rb) return ra;
+  const int64_t sb = cell_start[b], eb = b + 1 < m ? cell_start[b + 1] : n;
+  bool found = false;
+  for (int64_t i = sa; i < ea && !found; ++i) {
+    const float4 x = cpts[i];
+    for (int64_t j = sb; j < eb; ++j) {
+      const float4 y = cpts[j];
+      if (hit_point(R, x.x, x.y, x.z, y.x, y.y, y.z)) {
+        found = true;
+        break;
+      }
+    }
+  }
+  return found ? uf_union(parent, ra, rb) : ra;
+}
+
+// One thread per non-empty cell a: a stackless walk of the cell hierarchy
+// from a's rope visits only cells b > a (each cell pair once); cells whose
+// point boxes are within eps are united when a member pair is within eps,
+// skipped early when b already hangs off a's root (root hint).
 __global__ void __launch_bounds__(128) k_fof_cells_merge(const float4 *__restrict__ nodes, int64_t m,
                                                          const int64_t *__restrict__ cell_start, int64_t n,
                                                          const float4 *__restrict__ cpts, Radius R, int32_t *parent) {
@@ -428,18 +467,7 @@ __global__ void __launch_bounds__(128) k_fof_cells_merge(const float4 *__restric
   int32_t cur = node_rope(qhi);
   while (cur != kSentinel) {
     const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
-    bool far;
-    if (R.fast) {
-      far = sq3(fmaxf(fmaxf(__fsub_rn(lo.x, qhi.x), __fsub_rn(qlo.x, hi.x)), 0.f),
-                fmaxf(fmaxf(__fsub_rn(lo.y, qhi.y), __fsub_rn(qlo.y, hi.y)), 0.f),
-                fmaxf(fmaxf(__fsub_rn(lo.z, qhi.z), __fsub_rn(qlo.z, hi.z)), 0.f)) > R.hi32;
-    } else {
-      const double gx = fmax(fmax((double)lo.x - (double)qhi.x, (double)qlo.x - (double)hi.x), 0.0);
-      const double gy = fmax(fmax((double)lo.y - (double)qhi.y, (double)qlo.y - (double)hi.y), 0.0);
-      const double gz = fmax(fmax((double)lo.z - (double)qhi.z, (double)qlo.z - (double)hi.z), 0.0);
-      far = gx * gx + gy * gy + gz * gz > R.thr * (1.0 + 0x1p-30);
-    }
-    if (far) {
+    if (cells_far(R, qlo, qhi, lo, hi)) {
       cur = node_rope(hi);
       continue;
     }
@@ -447,26 +475,7 @@ __global__ void __launch_bounds__(128) k_fof_cells_merge(const float4 *__restric
       cur = node_link(lo);
       continue;
     }
-    const int32_t b = (int32_t)(cur - first_leaf);
-    if (parent[b] != root) {
-      const int32_t ra = uf_find(parent, root), rb = uf_find(parent, b);
-      root = ra;
-      if (ra != rb) {
-        const int64_t sb = cell_start[b], eb = b + 1 < m ? cell_start[b + 1] : n;
-        bool found = false;
-        for (int64_t i = sa; i < ea && !found; ++i) {
-          const float4 x = cpts[i];
-          for (int64_t j = sb; j < eb; ++j) {
-            const float4 y = cpts[j];
-            if (hit_point(R, x.x, x.y, x.z, y.x, y.y, y.z)) {
-              found = true;
-              break;
-            }
-          }
-        }
-        if (found) root = uf_union(parent, ra, rb);
-      }
-    }
+    root = cells_leaf(cell_start, m, n, cpts, R, parent, sa, ea, root, (int32_t)(cur - first_leaf));
     cur = node_rope(hi);
   }
 }
@@ -754,6 +763,7 @@ bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t 
   int64_t m = 0;
   SPB_CUDA(cudaMemcpyAsync(&m, hscan.get() + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
   SPB_CUDA(cudaStreamSynchronize(c.stream));
+  c.count("fof_cells", m);
   DevBuf<int64_t> cell_start((size_t)m, c.stream);
   k_cell_starts<<<G, 256, 0, c.stream>>>(head.get(), hscan.get(), n, cell_start.get());
   SPB_LAUNCHED();

@@ -47,6 +47,9 @@ struct Ctx {
   Staging in_stage[2][8], out_stage[2][8];
   int64_t calls = 0;
   int in_used = 0, out_used = 0;
+  // diagnostic counters of the last call (e.g. "fof_cells": non-empty cells)
+  std::vector<std::pair<std::string, int64_t>> counters;
+  void count(const char *name, int64_t v) { counters.emplace_back(name, v); }
 };
 
 // Record a phase boundary on the context stream (cheap; no host sync).
