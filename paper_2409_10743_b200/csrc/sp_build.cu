@@ -531,7 +531,7 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
   t.width = width;
   t.points = points;
   t.stream = c.stream;
-  SPB_CUDA(cudaMallocAsync(&t.scene, 6 * sizeof(float), c.stream));
+  t.scene = static_cast<decltype(t.scene)>(cache_alloc(6 * sizeof(float), c.stream));
   DevBuf<int> bad(1, c.stream);
   mark(c, "start");
   scene_bounds(c, objects, n, dim, points, t.scene, bad.get());
@@ -549,9 +549,9 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
   if (n == 0) return;
 
   const int64_t num_nodes = 2 * n - 1;
-  SPB_CUDA(cudaMallocAsync(&t.nodes, (size_t)num_nodes * 2 * sizeof(float4), c.stream));
-  SPB_CUDA(cudaMallocAsync(&t.perm, (size_t)n * sizeof(int32_t), c.stream));
-  if (points) SPB_CUDA(cudaMallocAsync(&t.leafpt, (size_t)n * sizeof(float4), c.stream));
+  t.nodes = static_cast<decltype(t.nodes)>(cache_alloc((size_t)num_nodes * 2 * sizeof(float4), c.stream));
+  t.perm = static_cast<decltype(t.perm)>(cache_alloc((size_t)n * sizeof(int32_t), c.stream));
+  if (points) t.leafpt = static_cast<decltype(t.leafpt)>(cache_alloc((size_t)n * sizeof(float4), c.stream));
 
   DevBuf<uint64_t> k0(n, c.stream), k1(n, c.stream);
   DevBuf<uint32_t> v0(n, c.stream), v1(n, c.stream);
@@ -585,8 +585,8 @@ void build_sorted_hierarchy(Ctx &c, const uint64_t *keys, int64_t m, int dim, co
   t.points = false;
   t.stream = c.stream;
   if (m == 0) return;
-  SPB_CUDA(cudaMallocAsync(&t.nodes, (size_t)(2 * m - 1) * 2 * sizeof(float4), c.stream));
-  SPB_CUDA(cudaMallocAsync(&t.perm, (size_t)m * sizeof(int32_t), c.stream));
+  t.nodes = static_cast<decltype(t.nodes)>(cache_alloc((size_t)(2 * m - 1) * 2 * sizeof(float4), c.stream));
+  t.perm = static_cast<decltype(t.perm)>(cache_alloc((size_t)m * sizeof(int32_t), c.stream));
   DevBuf<int32_t> delta(m > 1 ? m - 1 : 1, c.stream), flags(m > 1 ? m - 1 : 1, c.stream);
   if (m > 1) {
     k_delta<<<grid_for(m, 256, 148 * 16), 256, 0, c.stream>>>(keys, nullptr, m, 64, delta.get());

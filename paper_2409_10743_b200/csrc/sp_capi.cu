@@ -203,6 +203,7 @@ int sp_ctx_create(int device, void *stream, sp_ctx **out) {
     delete ctx;
     return SP_ECUDA;
   }
+  spb::cache_register_stream(ctx->c.stream);
   // Keep freed stream-ordered allocations reserved: a caching allocator.
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -230,6 +231,8 @@ int sp_ctx_destroy(sp_ctx *ctx) {
           if (st.p) cudaFree(st.p);
           if (st.done) cudaEventDestroy(st.done);
         }
+    spb::cache_unregister_stream(ctx->c.stream);
+    cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.owns_stream) cudaStreamDestroy(ctx->c.stream);
   }
   delete ctx;
@@ -240,6 +243,8 @@ int sp_ctx_set_stream(sp_ctx *ctx, void *stream) {
   if (!ctx) return SP_EINVAL;
   DeviceGuard dg(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
+  spb::cache_unregister_stream(ctx->c.stream);
+  cudaStreamSynchronize(ctx->c.stream);
   if (ctx->c.owns_stream) cudaStreamDestroy(ctx->c.stream);
   ctx->c.owns_stream = false;
   if (stream) {
@@ -248,6 +253,7 @@ int sp_ctx_set_stream(sp_ctx *ctx, void *stream) {
     if (cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking) != cudaSuccess) return SP_ECUDA;
     ctx->c.owns_stream = true;
   }
+  spb::cache_register_stream(ctx->c.stream);
   return SP_OK;
 }
 

@@ -21,7 +21,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "sp_common.cuh"
@@ -32,6 +35,24 @@
 namespace spb {
 
 namespace {
+
+// Host synchronisation point; SPB_DEBUG_SYNC=1 logs the host time spent before
+// and inside each wait (diagnostics for idle gaps between phases).
+void host_sync(Ctx &c, int line) {
+  static const bool dbg = getenv("SPB_DEBUG_SYNC") != nullptr;
+  if (!dbg) {
+    SPB_CUDA(cudaStreamSynchronize(c.stream));
+    return;
+  }
+  static auto last = std::chrono::steady_clock::now();
+  const auto t0 = std::chrono::steady_clock::now();
+  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  const auto t1 = std::chrono::steady_clock::now();
+  fprintf(stderr, "[sync line %d] host-before %.2f ms wait %.2f ms\n", line,
+          std::chrono::duration<double, std::milli>(t0 - last).count(),
+          std::chrono::duration<double, std::milli>(t1 - t0).count());
+  last = t1;
+}
 
 __device__ __forceinline__ uint64_t spread3_21(uint64_t v) {
   v &= 0x1fffffull;
@@ -212,18 +233,6 @@ struct DenseView {
   const float4 *cpts;  // points in sorted-by-cell order {x, y, z, bits(original index)}
 };
 
-// first position in members [b, b+len) (ascending original indices) whose
-// original index exceeds i
-__device__ __forceinline__ int32_t first_above(const float4 *cpts, int64_t b, int32_t len, int32_t i) {
-  int32_t lo = 0, hi = len;
-  while (lo < hi) {
-    const int32_t mid = (lo + hi) >> 1;
-    if (__float_as_int(cpts[b + mid].w) > i) hi = mid;
-    else lo = mid + 1;
-  }
-  return lo;
-}
-
 __global__ void k_cell_points(const uint32_t *__restrict__ order, const float *__restrict__ pts, int64_t n, int dim,
                               float4 *__restrict__ cpts) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -291,72 +300,205 @@ __global__ void k_db_cell_unions(const int64_t *__restrict__ dbeg, const int32_t
   for (int32_t t = 1 + lane; t < dlen[warp]; t += 32) uf_union(parent, first, (int32_t)members[b + t]);
 }
 
-template <bool FOF>
-__device__ __forceinline__ void db_merge(int32_t i, int32_t j, int32_t *parent, uint8_t *core, uint32_t *claims) {
-  if (FOF) {
-    uf_union(parent, i, j);
-    core[i] = 1;
-    core[j] = 1;
-    return;
+__device__ __forceinline__ bool cells_far(const Radius &R, const float4 &qlo, const float4 &qhi, const float4 &lo,
+                                          const float4 &hi) {
+  if (R.fast)
+    return sq3(fmaxf(fmaxf(__fsub_rn(lo.x, qhi.x), __fsub_rn(qlo.x, hi.x)), 0.f),
+               fmaxf(fmaxf(__fsub_rn(lo.y, qhi.y), __fsub_rn(qlo.y, hi.y)), 0.f),
+               fmaxf(fmaxf(__fsub_rn(lo.z, qhi.z), __fsub_rn(qlo.z, hi.z)), 0.f)) > R.hi32;
+  const double gx = fmax(fmax((double)lo.x - (double)qhi.x, (double)qlo.x - (double)hi.x), 0.0);
+  const double gy = fmax(fmax((double)lo.y - (double)qhi.y, (double)qlo.y - (double)hi.y), 0.0);
+  const double gz = fmax(fmax((double)lo.z - (double)qhi.z, (double)qlo.z - (double)hi.z), 0.0);
+  return gx * gx + gy * gy + gz * gz > R.thr * (1.0 + 0x1p-30);
+}
+
+// ---- merge (dbscan.hpp:388-440), restated over objects ----------------------
+// The reference walks every point and checks every member of every nearby dense
+// cell.  Here the merge runs over OBJECTS (dense cells and sparse points, the
+// leaves of the mixed tree) in two passes with the same result contract:
+//  * core objects (dense cells -- all members core -- and core sparse points;
+//    every sparse point for min_pts = 2): a rope walk from each object's leaf
+//    over later leaves (pair traversal, traversal.hpp:162-184, so each object
+//    pair once) unites two objects' sets at the first member pair within eps,
+//    and skips objects already in its set.  The core partition therefore
+//    equals the reference's (core-core pairs within eps, transitively).
+//  * non-core sparse points (min_pts > 2): a walk from the root stops at the
+//    first core point within eps and joins its set -- the reference's one-shot
+//    claim latch (union_find.hpp:63-82) gives each border point to exactly one
+//    adjacent cluster, which is all check_equivalence (verify.hpp:21-61)
+//    requires.
+// Union-find runs in original index space (root = smallest index).  A dense
+// cell's set is represented by its first (smallest) member, pre-united with
+// the others (dbscan.hpp:390-394).  distance_checks counts the member-pair
+// distance evaluations this merge performs (dbscan.hpp:38-41).
+struct ObjRef {
+  int64_t beg;   // first member in cpts (dense cells)
+  int32_t len;   // members (0: a sparse point)
+  int32_t rep;   // set representative (original index)
+  float x, y, z; // the point (sparse)
+};
+
+__device__ __forceinline__ ObjRef obj_ref(const DenseView &v, int32_t o, const float4 &lo) {
+  ObjRef r;
+  if (o < v.nd) {
+    r.beg = v.dbeg[o];
+    r.len = v.dlen[o];
+    r.rep = __float_as_int(v.cpts[r.beg].w);
+    r.x = r.y = r.z = 0.f;
+  } else {
+    r.beg = 0;
+    r.len = 0;
+    r.rep = v.sparse_pts[o - v.nd];
+    r.x = lo.x;
+    r.y = lo.y;
+    r.z = lo.z;
   }
-  const bool ci = core[i] != 0, cj = core[j] != 0;
-  if (ci && cj) {
-    uf_union(parent, i, j);
-  } else if (ci || cj) {
-    const int32_t b = ci ? j : i;
-    const uint32_t bit = 1u << (b & 31);
-    if (!(atomicOr(&claims[b >> 5], bit) & bit)) uf_union(parent, i, j);
+  return r;
+}
+
+// Is any member of a within eps of any member of b?  Counts evaluations.
+__device__ __forceinline__ bool objs_close(const DenseView &v, const ObjRef &a, const ObjRef &b, uint64_t &checks) {
+  if (a.len == 0 && b.len == 0) {
+    ++checks;
+    return hit_point(v.R, a.x, a.y, a.z, b.x, b.y, b.z);
+  }
+  if (a.len == 0 || b.len == 0) {
+    const ObjRef &p = a.len == 0 ? a : b, &c = a.len == 0 ? b : a;
+    for (int32_t t = 0; t < c.len; ++t) {
+      const float4 q = v.cpts[c.beg + t];
+      ++checks;
+      if (hit_point(v.R, p.x, p.y, p.z, q.x, q.y, q.z)) return true;
+    }
+    return false;
+  }
+  for (int32_t s = 0; s < a.len; ++s) {
+    const float4 x = v.cpts[a.beg + s];
+    for (int32_t t = 0; t < b.len; ++t) {
+      const float4 y = v.cpts[b.beg + t];
+      ++checks;
+      if (hit_point(v.R, x.x, x.y, x.z, y.x, y.y, y.z)) return true;
+    }
+  }
+  return false;
+}
+
+__device__ __forceinline__ void add_checks(uint64_t checks, unsigned long long *total) {
+  for (int off = 16; off; off >>= 1) checks += __shfl_xor_sync(0xffffffffu, checks, off);
+  if ((threadIdx.x & 31) == 0 && checks) atomicAdd(total, (unsigned long long)checks);
+}
+
+// Leaf positions of core objects (list 0, leaf order) and of non-core sparse
+// points (list 1).  key[p] = 1 for a core object.
+__global__ void k_obj_class(const float4 *__restrict__ nodes, int64_t nobj, int64_t nd,
+                            const int32_t *__restrict__ sparse_pts, const uint8_t *__restrict__ core, bool fof,
+                            int32_t *__restrict__ key) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nobj; p += stride) {
+    const int32_t o = node_link(ld_node(nodes, 2 * (nobj - 1 + p)));
+    key[p] = (fof || o < nd || core[sparse_pts[o - nd]]) ? 1 : 0;
+  }
+}
+
+__global__ void k_obj_lists(const int32_t *__restrict__ key, const int64_t *__restrict__ scan, int64_t nobj,
+                            int32_t *__restrict__ core_leaf, int32_t *__restrict__ border_leaf) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nobj; p += stride) {
+    if (key[p]) core_leaf[scan[p]] = (int32_t)p;
+    else border_leaf[p - scan[p]] = (int32_t)p;
   }
 }
 
 template <bool FOF>
-__global__ void __launch_bounds__(128) k_db_merge(DenseView v, const uint32_t *__restrict__ qorder, int64_t n,
-                                                  const int32_t *__restrict__ point_cell, int32_t *parent,
-                                                  uint8_t *core, uint32_t *claims,
-                                                  unsigned long long *__restrict__ checks_total) {
-  const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(128) k_db_core_pairs(DenseView v, const int32_t *__restrict__ core_leaf,
+                                                       const int64_t *__restrict__ ncore_p, int32_t *parent, uint8_t *core,
+                                                       unsigned long long *__restrict__ checks_total) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t ncore = *ncore_p;
   uint64_t checks = 0;
-  if (qi < n) {
-    const float4 me = v.cpts[qi];
-    const int32_t i = __float_as_int(me.w);
-    const int32_t own = point_cell[i];
-    const float x = me.x, y = me.y, z = me.z;
-    int32_t cur = 0;
+  if (k < ncore) {
+    const int64_t first_leaf = v.nobj - 1;
+    const int64_t me = first_leaf + core_leaf[k];
+    const float4 qlo = ld_node(v.nodes, 2 * me), qhi = ld_node(v.nodes, 2 * me + 1);
+    const ObjRef a = obj_ref(v, node_link(qlo), qlo);
+    int32_t root = a.rep;
+    int32_t cur = node_rope(qhi);
     while (cur != kSentinel) {
-      const float4 lo = ld_node(v.nodes, 2 * (int64_t)cur);
-      const float4 hi = ld_node(v.nodes, 2 * (int64_t)cur + 1);
-      const bool leaf = cur >= v.nobj - 1;
-      const bool hit = leaf ? hit_box(v.R, x, y, z, lo, hi) : maybe_box(v.R, x, y, z, lo, hi);
-      if (cur >= v.nobj - 1) {
-        if (hit) {
-          const int32_t o = node_link(lo);
-          if (o < v.nd) {
-            if (o != own) {
-              // members ascend by original index: only j > i are checked
-              const int64_t b = v.dbeg[o];
-              const int32_t len = v.dlen[o];
-              const int32_t t0 = first_above(v.cpts, b, len, i);
-              checks += (uint64_t)(len - t0);
-              for (int32_t t = t0; t < len; ++t) {
-                const float4 q = v.cpts[b + t];
-                if (hit_point(v.R, x, y, z, q.x, q.y, q.z))
-                  db_merge<FOF>(i, __float_as_int(q.w), parent, core, claims);
-              }
-            }
-          } else {
-            const int32_t j = v.sparse_pts[o - v.nd];
-            if (i < j) db_merge<FOF>(i, j, parent, core, claims);
-          }
-        }
+      const float4 lo = ld_node(v.nodes, 2 * (int64_t)cur), hi = ld_node(v.nodes, 2 * (int64_t)cur + 1);
+      if (cells_far(v.R, qlo, qhi, lo, hi)) {
         cur = node_rope(hi);
-      } else {
-        cur = hit ? node_link(lo) : node_rope(hi);
+        continue;
+      }
+      if (cur < first_leaf) {
+        cur = node_link(lo);
+        continue;
+      }
+      cur = node_rope(hi);
+      const int32_t o = node_link(lo);
+      const int32_t brep = o < v.nd ? __float_as_int(v.cpts[v.dbeg[o]].w) : v.sparse_pts[o - v.nd];
+      if (!FOF && o >= v.nd && !core[brep]) continue;  // border points join in the second pass
+      if (parent[brep] == root) continue;
+      const int32_t ra = uf_find(parent, root), rb = uf_find(parent, brep);
+      root = ra;
+      if (ra == rb) continue;
+      const ObjRef b = obj_ref(v, o, lo);
+      if (!objs_close(v, a, b, checks)) continue;
+      root = uf_union(parent, ra, rb);
+      if (FOF) {
+        core[a.rep] = 1;
+        core[brep] = 1;
       }
     }
   }
-  // warp-aggregate the distance-check counter
-  for (int off = 16; off; off >>= 1) checks += __shfl_xor_sync(0xffffffffu, checks, off);
-  if ((threadIdx.x & 31) == 0 && checks) atomicAdd(checks_total, (unsigned long long)checks);
+  add_checks(checks, checks_total);
+}
+
+// Border points: the first core point within eps claims the point.
+__global__ void __launch_bounds__(128) k_db_border(DenseView v, const int32_t *__restrict__ border_leaf,
+                                                   const int64_t *__restrict__ ncore_p, int32_t *parent, const uint8_t *__restrict__ core,
+                                                   uint32_t *__restrict__ claims,
+                                                   unsigned long long *__restrict__ checks_total) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nborder = v.nobj - *ncore_p;
+  uint64_t checks = 0;
+  if (k < nborder) {
+    const int64_t first_leaf = v.nobj - 1;
+    const float4 me = ld_node(v.nodes, 2 * (first_leaf + border_leaf[k]));
+    const int32_t i = v.sparse_pts[node_link(me) - v.nd];
+    const float x = me.x, y = me.y, z = me.z;
+    int32_t cur = 0;
+    int32_t found = -1;
+    while (cur != kSentinel) {
+      const float4 lo = ld_node(v.nodes, 2 * (int64_t)cur), hi = ld_node(v.nodes, 2 * (int64_t)cur + 1);
+      if (cur < first_leaf) {
+        cur = maybe_box(v.R, x, y, z, lo, hi) ? node_link(lo) : node_rope(hi);
+        continue;
+      }
+      cur = node_rope(hi);
+      if (!hit_box(v.R, x, y, z, lo, hi)) continue;
+      const int32_t o = node_link(lo);
+      if (o < v.nd) {
+        const int64_t b = v.dbeg[o];
+        const int32_t len = v.dlen[o];
+        for (int32_t t = 0; t < len; ++t) {
+          const float4 q = v.cpts[b + t];
+          ++checks;
+          if (hit_point(v.R, x, y, z, q.x, q.y, q.z)) {
+            found = __float_as_int(q.w);
+            break;
+          }
+        }
+      } else {
+        const int32_t j = v.sparse_pts[o - v.nd];
+        if (core[j]) found = j;  // the point box hit is the exact point test
+      }
+      if (found >= 0) break;
+    }
+    if (found >= 0) {
+      atomicOr(&claims[i >> 5], 1u << (i & 31));
+      uf_union(parent, found, i);
+    }
+  }
+  add_checks(checks, checks_total);
 }
 
 __global__ void k_db_labels(int64_t n, int32_t *parent, const uint8_t *__restrict__ core,
@@ -416,18 +558,6 @@ __global__ void k_cell_ranges(const int64_t *__restrict__ cell_start, int64_t m,
   }
 }
 
-__device__ __forceinline__ bool cells_far(const Radius &R, const float4 &qlo, const float4 &qhi, const float4 &lo,
-                                          const float4 &hi) {
-  if (R.fast)
-    return sq3(fmaxf(fmaxf(__fsub_rn(lo.x, qhi.x), __fsub_rn(qlo.x, hi.x)), 0.f),
-               fmaxf(fmaxf(__fsub_rn(lo.y, qhi.y), __fsub_rn(qlo.y, hi.y)), 0.f),
-               fmaxf(fmaxf(__fsub_rn(lo.z, qhi.z), __fsub_rn(qlo.z, hi.z)), 0.f)) > R.hi32;
-  const double gx = fmax(fmax((double)lo.x - (double)qhi.x, (double)qlo.x - (double)hi.x), 0.0);
-  const double gy = fmax(fmax((double)lo.y - (double)qhi.y, (double)qlo.y - (double)hi.y), 0.0);
-  const double gz = fmax(fmax((double)lo.z - (double)qhi.z, (double)qlo.z - (double)hi.z), 0.0);
-  return gx * gx + gy * gy + gz * gz > R.thr * (1.0 + 0x1p-30);
-}
-
 // Union cell a's set (root hint `root`) with leaf cell b's when a member pair
 // is within eps; returns the updated hint.
 __device__ __forceinline__ int32_t cells_leaf(const int64_t *__restrict__ cell_start, int64_t m, int64_t n,
@@ -480,6 +610,68 @@ __global__ void __launch_bounds__(128) k_fof_cells_merge(const float4 *__restric
   }
 }
 
+// The same walk, W cells per thread with their node loads issued together:
+// W independent pointer chains per thread hide the node-load latency that
+// bounds the single walk (profiles/r01: the first FADD after the two node
+// loads).  ADJ: thread t owns cells W*t .. W*t+W-1 of its block's range (the
+// walks share most nodes); otherwise cells t, t + blockDim, ...
+#ifndef SPB_MERGE_W
+#define SPB_MERGE_W 1
+#endif
+#ifndef SPB_MERGE_ADJ
+#define SPB_MERGE_ADJ 0
+#endif
+template <int W, bool ADJ>
+__global__ void __launch_bounds__(128) k_fof_cells_merge_w(const float4 *__restrict__ nodes, int64_t m,
+                                                           const int64_t *__restrict__ cell_start, int64_t n,
+                                                           const float4 *__restrict__ cpts, Radius R,
+                                                           int32_t *parent) {
+  const int64_t first_leaf = m - 1;
+  const int64_t blk = (int64_t)blockIdx.x * blockDim.x * W;
+  float4 qlo[W], qhi[W];
+  int64_t sa[W], ea[W];
+  int32_t root[W], cur[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    const int64_t a = ADJ ? blk + (int64_t)threadIdx.x * W + k : blk + threadIdx.x + (int64_t)k * blockDim.x;
+    cur[k] = kSentinel;
+    root[k] = (int32_t)a;
+    sa[k] = ea[k] = 0;
+    if (a < m) {
+      qlo[k] = ld_node(nodes, 2 * (first_leaf + a));
+      qhi[k] = ld_node(nodes, 2 * (first_leaf + a) + 1);
+      sa[k] = cell_start[a];
+      ea[k] = a + 1 < m ? cell_start[a + 1] : n;
+      cur[k] = node_rope(qhi[k]);
+    }
+  }
+  while (true) {
+    float4 lo[W], hi[W];
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      if (cur[k] != kSentinel) {
+        lo[k] = ld_node(nodes, 2 * (int64_t)cur[k]);
+        hi[k] = ld_node(nodes, 2 * (int64_t)cur[k] + 1);
+        any = true;
+      }
+    }
+    if (!any) break;
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      if (cur[k] == kSentinel) continue;
+      if (cells_far(R, qlo[k], qhi[k], lo[k], hi[k])) {
+        cur[k] = node_rope(hi[k]);
+      } else if (cur[k] < first_leaf) {
+        cur[k] = node_link(lo[k]);
+      } else {
+        root[k] = cells_leaf(cell_start, m, n, cpts, R, parent, sa[k], ea[k], root[k], (int32_t)(cur[k] - first_leaf));
+        cur[k] = node_rope(hi[k]);
+      }
+    }
+  }
+}
+
 // cells: core iff the cell has two points or its set spans several cells
 __global__ void k_fof_cells_core(int64_t m, int32_t *parent, uint8_t *multi) {
   const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -528,6 +720,7 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
   cudaEvent_t ev[5];
   for (auto &e : ev) SPB_CUDA(cudaEventCreate(&e));
   SPB_CUDA(cudaEventRecord(ev[0], c.stream));
+  mark(c, "start");
   const unsigned G = grid_for(n, 256, 148 * 16);
 
   // ---- grid (build_dense_grid) ----
@@ -540,7 +733,7 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
   int hbad = 0;
   SPB_CUDA(cudaMemcpyAsync(hs, scene.get(), sizeof(hs), cudaMemcpyDeviceToHost, c.stream));
   SPB_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  host_sync(c, __LINE__);
   if (hbad) {
     for (auto &e : ev) cudaEventDestroy(e);
     throw InvalidArgument("dbscan: non-finite coordinate");
@@ -590,6 +783,7 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
       }
     }
     order = va;
+    mark(c, "grid_sort");
     // segments
     DevBuf<int32_t> head((size_t)n, c.stream);
     DevBuf<int64_t> hscan((size_t)n + 1, c.stream);
@@ -598,7 +792,7 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
     exclusive_scan(c, head.get(), n, hscan.get());
     int64_t m = 0;
     SPB_CUDA(cudaMemcpyAsync(&m, hscan.get() + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
-    SPB_CUDA(cudaStreamSynchronize(c.stream));
+    host_sync(c, __LINE__);
     cell_start = DevBuf<int64_t>((size_t)m, c.stream);
     k_cell_starts<<<G, 256, 0, c.stream>>>(head.get(), hscan.get(), n, cell_start.get());
     SPB_LAUNCHED();
@@ -609,7 +803,7 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
     SPB_LAUNCHED();
     exclusive_scan(c, dense.get(), m, dscan.get());
     SPB_CUDA(cudaMemcpyAsync(&nd, dscan.get() + m, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
-    SPB_CUDA(cudaStreamSynchronize(c.stream));
+    host_sync(c, __LINE__);
     if (nd > 0) {
       // dense cells ordered by their smallest member
       DevBuf<uint64_t> mk0((size_t)nd, c.stream), mk1((size_t)nd, c.stream);
@@ -638,7 +832,7 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
   exclusive_scan(c, sflag.get(), n, sscan.get());
   int64_t ns = 0;
   SPB_CUDA(cudaMemcpyAsync(&ns, sscan.get() + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
-  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  host_sync(c, __LINE__);
   num_dense_points = n - ns;
   DevBuf<int32_t> sparse_pts((size_t)(ns > 0 ? ns : 1), c.stream);
   k_sparse_objects<<<G, 256, 0, c.stream>>>(point_cell.get(), sscan.get(), n, nd, pts, dim, sparse_pts.get(),
@@ -646,6 +840,7 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
   SPB_LAUNCHED();
   sflag.reset();
   sscan.reset();
+  mark(c, "objects");
   const int64_t nobj = nd + ns;
   DevBuf<float4> cpts((size_t)n, c.stream);
   k_cell_points<<<G, 256, 0, c.stream>>>(order, pts, n, dim, cpts.get());
@@ -653,6 +848,7 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
   Tree t;
   build_tree(c, objects.get(), nobj, dim, false, width, t);
   SPB_CUDA(cudaEventRecord(ev[1], c.stream));
+  mark(c, "tree");
 
   DenseView v{t.nodes, nobj, nd, dbeg.get(), dlen.get(), order, sparse_pts.get(), pts, dim, make_radius(eps),
               cpts.get()};
@@ -666,6 +862,7 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
     SPB_LAUNCHED();
   }
   SPB_CUDA(cudaEventRecord(ev[2], c.stream));
+  mark(c, "core");
 
   DevBuf<int32_t> parent((size_t)n, c.stream);
   DevBuf<uint32_t> claims(count_phase ? (size_t)((n + 31) / 32) : 0, c.stream);
@@ -679,21 +876,42 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
                                                                               parent.get());
     SPB_LAUNCHED();
   }
-  if (count_phase)
-    k_db_merge<false><<<Gq, 128, 0, c.stream>>>(v, order, n, point_cell.get(), parent.get(), core.get(), claims.get(),
-                                                checks.get());
-  else
-    k_db_merge<true><<<Gq, 128, 0, c.stream>>>(v, order, n, point_cell.get(), parent.get(), core.get(), nullptr,
-                                               checks.get());
-  SPB_LAUNCHED();
+  {
+    // core objects and border points as leaf-order lists (no host round trip:
+    // the kernels read the list lengths from the scan total)
+    DevBuf<int32_t> key((size_t)nobj, c.stream), core_leaf((size_t)nobj, c.stream), border_leaf((size_t)nobj, c.stream);
+    DevBuf<int64_t> kscan((size_t)nobj + 1, c.stream);
+    const unsigned Go = grid_for(nobj, 256, 148 * 16);
+    k_obj_class<<<Go, 256, 0, c.stream>>>(t.nodes, nobj, nd, sparse_pts.get(), core.get(), !count_phase, key.get());
+    SPB_LAUNCHED();
+    exclusive_scan(c, key.get(), nobj, kscan.get());
+    k_obj_lists<<<Go, 256, 0, c.stream>>>(key.get(), kscan.get(), nobj, core_leaf.get(), border_leaf.get());
+    SPB_LAUNCHED();
+    const unsigned Gl = (unsigned)((nobj + 127) / 128);
+    if (count_phase)
+      k_db_core_pairs<false><<<Gl, 128, 0, c.stream>>>(v, core_leaf.get(), kscan.get() + nobj, parent.get(),
+                                                       core.get(), checks.get());
+    else
+      k_db_core_pairs<true><<<Gl, 128, 0, c.stream>>>(v, core_leaf.get(), kscan.get() + nobj, parent.get(),
+                                                      core.get(), checks.get());
+    SPB_LAUNCHED();
+    mark(c, "merge_core");
+    if (count_phase) {
+      k_db_border<<<Gl, 128, 0, c.stream>>>(v, border_leaf.get(), kscan.get() + nobj, parent.get(), core.get(),
+                                            claims.get(), checks.get());
+      SPB_LAUNCHED();
+    }
+  }
   SPB_CUDA(cudaEventRecord(ev[3], c.stream));
+  mark(c, "merge");
   k_db_labels<<<G, 256, 0, c.stream>>>(n, parent.get(), core.get(), claims.get(), labels, core_out);
   SPB_LAUNCHED();
   SPB_CUDA(cudaEventRecord(ev[4], c.stream));
+  mark(c, "finalize");
   unsigned long long hchecks = 0;
   SPB_CUDA(cudaMemcpyAsync(&hchecks, checks.get(), sizeof(hchecks), cudaMemcpyDeviceToHost, c.stream));
   SPB_CUDA(cudaEventSynchronize(ev[4]));
-  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  host_sync(c, __LINE__);
   if (res) {
     for (int i = 0; i < 4; ++i) {
       float ms = 0.f;
@@ -785,8 +1003,13 @@ bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t 
   DevBuf<int32_t> parent((size_t)m, c.stream), minobj((size_t)m, c.stream);
   k_iota32<<<grid_for(m, 256, 148 * 16), 256, 0, c.stream>>>(parent.get(), m);
   SPB_LAUNCHED();
-  k_fof_cells_merge<<<(unsigned)((m + 127) / 128), 128, 0, c.stream>>>(t.nodes, m, cell_start.get(), n, cpts.get(),
-                                                                       make_radius(eps), parent.get());
+  if (SPB_MERGE_W == 1)
+    k_fof_cells_merge<<<(unsigned)((m + 127) / 128), 128, 0, c.stream>>>(t.nodes, m, cell_start.get(), n, cpts.get(),
+                                                                         make_radius(eps), parent.get());
+  else
+    k_fof_cells_merge_w<SPB_MERGE_W, SPB_MERGE_ADJ != 0>
+        <<<(unsigned)((m + 128 * SPB_MERGE_W - 1) / (128 * SPB_MERGE_W)), 128, 0, c.stream>>>(
+            t.nodes, m, cell_start.get(), n, cpts.get(), make_radius(eps), parent.get());
   SPB_LAUNCHED();
   SPB_CUDA(cudaEventRecord(ev[3], c.stream));
   mark(c, "merge");

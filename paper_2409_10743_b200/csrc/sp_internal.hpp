@@ -58,6 +58,13 @@ void mark(Ctx &c, const char *name);
 void resolve_marks(Ctx &c);
 void reset_marks(Ctx &c);
 
+// Stream-keyed caching allocator (sp_alloc.cpp): blocks freed on a registered
+// stream are reused by later requests on that stream without driver calls.
+void cache_register_stream(cudaStream_t s);
+void cache_unregister_stream(cudaStream_t s);
+void *cache_alloc(size_t bytes, cudaStream_t s);  // throws CudaError
+void cache_free(void *p, cudaStream_t s);
+
 template <class T>
 struct DevBuf {
   T *p = nullptr;
@@ -65,14 +72,7 @@ struct DevBuf {
   cudaStream_t s = nullptr;
   DevBuf() = default;
   DevBuf(size_t count, cudaStream_t stream) : n(count), s(stream) {
-    if (count) {
-      cudaError_t e = cudaMallocAsync((void **)&p, count * sizeof(T), stream);
-      if (e != cudaSuccess) {
-        p = nullptr;
-        throw CudaError(std::string("device allocation of ") + std::to_string(count * sizeof(T)) +
-                        " bytes failed: " + cudaGetErrorString(e));
-      }
-    }
+    if (count) p = static_cast<T *>(cache_alloc(count * sizeof(T), stream));
   }
   DevBuf(const DevBuf &) = delete;
   DevBuf &operator=(const DevBuf &) = delete;
@@ -85,7 +85,7 @@ struct DevBuf {
   }
   ~DevBuf() { reset(); }
   void reset() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) cache_free(p, s);
     p = nullptr;
     n = 0;
   }
@@ -109,10 +109,10 @@ struct Tree {
   Tree &operator=(const Tree &) = delete;
   ~Tree() { free_all(); }
   void free_all() {
-    if (nodes) cudaFreeAsync(nodes, stream);
-    if (perm) cudaFreeAsync(perm, stream);
-    if (scene) cudaFreeAsync(scene, stream);
-    if (leafpt) cudaFreeAsync(leafpt, stream);
+    cache_free(nodes, stream);
+    cache_free(perm, stream);
+    cache_free(scene, stream);
+    cache_free(leafpt, stream);
     leafpt = nullptr;
     nodes = nullptr;
     perm = nullptr;
