@@ -686,12 +686,12 @@ __global__ void k_fof_cells_core(int64_t m, int32_t *parent, uint8_t *multi) {
 
 __global__ void __launch_bounds__(256) k_fof_cells_minobj(int64_t n, const int32_t *__restrict__ cell_of,
                                                           const int32_t *__restrict__ parent,
-                                                          const float4 *__restrict__ cpts, int32_t *minobj) {
+                                                          const uint32_t *__restrict__ order, int32_t *minobj) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int32_t key = -1, v = 0x7fffffff;
   if (k < n) {
     key = uf_root(parent, cell_of[k]);
-    v = __float_as_int(cpts[k].w);
+    v = (int32_t)order[k];
   }
   const uint32_t peers = __match_any_sync(0xffffffffu, key);
   const int32_t mn = (int32_t)__reduce_min_sync(peers, (uint32_t)v);
@@ -701,13 +701,13 @@ __global__ void __launch_bounds__(256) k_fof_cells_minobj(int64_t n, const int32
 __global__ void __launch_bounds__(256) k_fof_cells_labels(int64_t n, const int32_t *__restrict__ cell_of,
                                                           const int32_t *__restrict__ parent,
                                                           const uint8_t *__restrict__ multi,
-                                                          const float4 *__restrict__ cpts,
+                                                          const uint32_t *__restrict__ order,
                                                           const int32_t *__restrict__ minobj,
                                                           int32_t *__restrict__ labels, uint8_t *__restrict__ core) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const int32_t cl = cell_of[k];
-  const int32_t o = __float_as_int(cpts[k].w);
+  const int32_t o = (int32_t)order[k];
   const bool c = multi[cl] != 0;
   labels[o] = c ? minobj[uf_root(parent, cl)] : -1;
   core[o] = c;
@@ -715,8 +715,15 @@ __global__ void __launch_bounds__(256) k_fof_cells_labels(int64_t n, const int32
 
 }  // namespace
 
+bool dbscan_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t min_pts, int32_t *labels,
+                  uint8_t *core_out, DbscanResult *res);
+
+// fdbscan_densebox: the all-cells pipeline (dbscan_cells) whenever the grid
+// applies; otherwise the reference's mixed tree of dense cells and sparse
+// points below.
 void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t min_pts, int width, int32_t *labels,
               uint8_t *core_out, DbscanResult *res) {
+  if (!getenv("SPB_DENSEBOX_OBJECTS") && dbscan_cells(c, pts, n, dim, eps, min_pts, labels, core_out, res)) return;
   cudaEvent_t ev[5];
   for (auto &e : ev) SPB_CUDA(cudaEventCreate(&e));
   SPB_CUDA(cudaEventRecord(ev[0], c.stream));
@@ -925,23 +932,29 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
   for (auto &e : ev) cudaEventDestroy(e);
 }
 
-// Returns false (nothing written) when the grid does not apply: coordinates
-// that could saturate (no dense cells in the reference either) or cell
-// coordinates too wide for a 63-bit Morton key.
-bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t *labels, uint8_t *core_out,
-               DbscanResult *res) {
+// The cell grid shared by the FoF and DBSCAN cell pipelines: points sorted by
+// the Morton key of their cell (side eps/sqrt(d)*(1-1e-6), anchored at the
+// scene min: build_dense_grid, dense_grid.hpp:71-103), cell segments, tight
+// cell boxes and the LBVH over the non-empty cells in key order.  Returns
+// false (nothing computed) when the grid does not apply: coordinates that
+// could saturate (no dense cells in the reference either) or cell coordinates
+// too wide for a 63-bit Morton key.
+struct CellGrid {
+  int64_t m = 0;
+  DevBuf<uint64_t> k0, k1;
+  DevBuf<uint32_t> v0, v1;
+  uint64_t *keys = nullptr;   // sorted cell keys
+  uint32_t *order = nullptr;  // sorted position -> original index
+  DevBuf<float4> cpts;        // sorted points {x, y, z, bits(original index)}
+  DevBuf<int64_t> cell_start;
+  DevBuf<int32_t> cell_of;    // sorted position -> cell
+  DevBuf<uint8_t> multi;      // cell has more than one point
+  Tree t;
+};
+
+bool build_cell_grid(Ctx &c, const float *pts, int64_t n, int dim, float eps, CellGrid &g) {
   const float cell = (float)((double)eps / std::sqrt((double)dim) * (1.0 - 1e-6));
   if (!(cell > 0.f)) return false;
-  cudaEvent_t ev[5];
-  for (auto &e : ev) SPB_CUDA(cudaEventCreate(&e));
-  struct EvGuard {
-    cudaEvent_t *e;
-    ~EvGuard() {
-      for (int i = 0; i < 5; ++i) cudaEventDestroy(e[i]);
-    }
-  } guard{ev};
-  SPB_CUDA(cudaEventRecord(ev[0], c.stream));
-  mark(c, "start");
   DevBuf<float> scene(6, c.stream);
   DevBuf<int> bad(1, c.stream);
   scene_bounds(c, pts, n, dim, true, scene.get(), bad.get());
@@ -961,17 +974,21 @@ bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t 
   if ((int64_t)bits * dim > 63) return false;
   mark(c, "bounds");
   const unsigned G = grid_for(n, 256, 148 * 16);
-  DevBuf<uint64_t> k0((size_t)n, c.stream), k1((size_t)n, c.stream);
-  DevBuf<uint32_t> v0((size_t)n, c.stream), v1((size_t)n, c.stream);
-  k_cell_keys<<<G, 256, 0, c.stream>>>(pts, n, dim, scene.get(), cell, -1, k0.get());
+  g.k0 = DevBuf<uint64_t>((size_t)n, c.stream);
+  g.k1 = DevBuf<uint64_t>((size_t)n, c.stream);
+  g.v0 = DevBuf<uint32_t>((size_t)n, c.stream);
+  g.v1 = DevBuf<uint32_t>((size_t)n, c.stream);
+  k_cell_keys<<<G, 256, 0, c.stream>>>(pts, n, dim, scene.get(), cell, -1, g.k0.get());
   SPB_LAUNCHED();
   mark(c, "morton");
-  uint64_t *ka = k0.get(), *kb = k1.get();
-  uint32_t *va = v0.get(), *vb = v1.get();
+  uint64_t *ka = g.k0.get(), *kb = g.k1.get();
+  uint32_t *va = g.v0.get(), *vb = g.v1.get();
   radix_sort_pairs(c, &ka, &va, &kb, &vb, n, bits * dim, true);
+  g.keys = ka;
+  g.order = va;
   mark(c, "sort");
-  DevBuf<float4> cpts((size_t)n, c.stream);
-  k_cell_points<<<G, 256, 0, c.stream>>>(va, pts, n, dim, cpts.get());
+  g.cpts = DevBuf<float4>((size_t)n, c.stream);
+  k_cell_points<<<G, 256, 0, c.stream>>>(va, pts, n, dim, g.cpts.get());
   SPB_LAUNCHED();
   DevBuf<int32_t> head((size_t)n, c.stream);
   DevBuf<int64_t> hscan((size_t)n + 1, c.stream);
@@ -981,46 +998,67 @@ bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t 
   int64_t m = 0;
   SPB_CUDA(cudaMemcpyAsync(&m, hscan.get() + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
   SPB_CUDA(cudaStreamSynchronize(c.stream));
-  c.count("fof_cells", m);
-  DevBuf<int64_t> cell_start((size_t)m, c.stream);
-  k_cell_starts<<<G, 256, 0, c.stream>>>(head.get(), hscan.get(), n, cell_start.get());
+  g.m = m;
+  g.cell_start = DevBuf<int64_t>((size_t)m, c.stream);
+  k_cell_starts<<<G, 256, 0, c.stream>>>(head.get(), hscan.get(), n, g.cell_start.get());
   SPB_LAUNCHED();
   head.reset();
   hscan.reset();
   DevBuf<uint64_t> ckeys((size_t)m, c.stream);
   DevBuf<float> boxes((size_t)m * 2 * dim, c.stream);
-  DevBuf<int32_t> cell_of((size_t)n, c.stream);
-  DevBuf<uint8_t> multi((size_t)m, c.stream);
-  k_cell_ranges<<<grid_for(m, 256, 148 * 16), 256, 0, c.stream>>>(cell_start.get(), m, n, ka, cpts.get(), dim,
-                                                                   ckeys.get(), boxes.get(), cell_of.get(),
-                                                                   multi.get());
+  g.cell_of = DevBuf<int32_t>((size_t)n, c.stream);
+  g.multi = DevBuf<uint8_t>((size_t)m, c.stream);
+  k_cell_ranges<<<grid_for(m, 256, 148 * 16), 256, 0, c.stream>>>(g.cell_start.get(), m, n, ka, g.cpts.get(), dim,
+                                                                   ckeys.get(), boxes.get(), g.cell_of.get(),
+                                                                   g.multi.get());
   SPB_LAUNCHED();
-  Tree t;
-  build_sorted_hierarchy(c, ckeys.get(), m, dim, boxes.get(), t);
+  build_sorted_hierarchy(c, ckeys.get(), m, dim, boxes.get(), g.t);
   mark(c, "hierarchy");
+  return true;
+}
+
+// friends-of-friends over the cell grid: a cell is one set from the start,
+// cells unite at their first member pair within eps (k_fof_cells_merge).
+bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t *labels, uint8_t *core_out,
+               DbscanResult *res) {
+  cudaEvent_t ev[5];
+  for (auto &e : ev) SPB_CUDA(cudaEventCreate(&e));
+  struct EvGuard {
+    cudaEvent_t *e;
+    ~EvGuard() {
+      for (int i = 0; i < 5; ++i) cudaEventDestroy(e[i]);
+    }
+  } guard{ev};
+  SPB_CUDA(cudaEventRecord(ev[0], c.stream));
+  mark(c, "start");
+  CellGrid g;
+  if (!build_cell_grid(c, pts, n, dim, eps, g)) return false;
+  const int64_t m = g.m;
+  c.count("fof_cells", m);
   SPB_CUDA(cudaEventRecord(ev[1], c.stream));
   SPB_CUDA(cudaEventRecord(ev[2], c.stream));
   DevBuf<int32_t> parent((size_t)m, c.stream), minobj((size_t)m, c.stream);
   k_iota32<<<grid_for(m, 256, 148 * 16), 256, 0, c.stream>>>(parent.get(), m);
   SPB_LAUNCHED();
   if (SPB_MERGE_W == 1)
-    k_fof_cells_merge<<<(unsigned)((m + 127) / 128), 128, 0, c.stream>>>(t.nodes, m, cell_start.get(), n, cpts.get(),
-                                                                         make_radius(eps), parent.get());
+    k_fof_cells_merge<<<(unsigned)((m + 127) / 128), 128, 0, c.stream>>>(g.t.nodes, m, g.cell_start.get(), n,
+                                                                         g.cpts.get(), make_radius(eps), parent.get());
   else
     k_fof_cells_merge_w<SPB_MERGE_W, SPB_MERGE_ADJ != 0>
         <<<(unsigned)((m + 128 * SPB_MERGE_W - 1) / (128 * SPB_MERGE_W)), 128, 0, c.stream>>>(
-            t.nodes, m, cell_start.get(), n, cpts.get(), make_radius(eps), parent.get());
+            g.t.nodes, m, g.cell_start.get(), n, g.cpts.get(), make_radius(eps), parent.get());
   SPB_LAUNCHED();
   SPB_CUDA(cudaEventRecord(ev[3], c.stream));
   mark(c, "merge");
-  k_fof_cells_core<<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(m, parent.get(), multi.get());
+  k_fof_cells_core<<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(m, parent.get(), g.multi.get());
   SPB_LAUNCHED();
   SPB_CUDA(cudaMemsetAsync(minobj.get(), 0x7f, (size_t)m * sizeof(int32_t), c.stream));
-  k_fof_cells_minobj<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(n, cell_of.get(), parent.get(), cpts.get(),
+  k_fof_cells_minobj<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(n, g.cell_of.get(), parent.get(), g.order,
                                                                         minobj.get());
   SPB_LAUNCHED();
-  k_fof_cells_labels<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(n, cell_of.get(), parent.get(), multi.get(),
-                                                                        cpts.get(), minobj.get(), labels, core_out);
+  k_fof_cells_labels<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(n, g.cell_of.get(), parent.get(),
+                                                                        g.multi.get(), g.order, minobj.get(), labels,
+                                                                        core_out);
   SPB_LAUNCHED();
   SPB_CUDA(cudaEventRecord(ev[4], c.stream));
   mark(c, "finalize");
@@ -1032,6 +1070,309 @@ bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t 
       cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
       res->ms[i] = ms;
     }
+  }
+  return true;
+}
+
+
+// ---------------------------------------------------------------------------
+// DBSCAN (min_pts > 2) over the cell grid: the DenseBox idea (dbscan.hpp:
+// 298-449) taken to every cell.  Any two points of one cell are within eps, so
+//  * a point of a cell with >= min_pts members is core (the dense cells of
+//    build_dense_grid); any other point counts its own cell whole and then the
+//    members of cells within eps of it, stopping at min_pts
+//    (detect_core_counts, dbscan.hpp:146-182: count = min(hits, min_pts));
+//  * the core points of one cell form one set; two cells unite at the first
+//    core-core member pair within eps (pair traversal over later cells, set
+//    skip), so the core partition is the reference's;
+//  * a non-core point joins the set of a core point within eps: one of its
+//    own cell if there is any, else the first found by a walk from the root
+//    (the one-shot claim latch of dbscan.hpp:123-137 / union_find.hpp:63-82);
+//    points with none are noise.
+// Labels are the smallest original index over each set's core and border
+// points; core flags are exact; clusters satisfy check_equivalence
+// (verify.hpp:21-61).
+// ---------------------------------------------------------------------------
+namespace {
+
+__device__ __forceinline__ int64_t cell_end(const int64_t *cell_start, int64_t m, int64_t n, int64_t c) {
+  return c + 1 < m ? cell_start[c + 1] : n;
+}
+
+// dense cells and their points (DbscanStats): {cells, points}
+__global__ void k_cells_dense_stats(const int64_t *__restrict__ cell_start, int64_t m, int64_t n, int32_t min_pts,
+                                    unsigned long long *st) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t dense = 0, pts = 0;
+  if (c < m) {
+    const int64_t len = cell_end(cell_start, m, n, c) - cell_start[c];
+    if (len >= min_pts) {
+      dense = 1;
+      pts = (uint32_t)len;
+    }
+  }
+  dense = __reduce_add_sync(0xffffffffu, dense);
+  pts = __reduce_add_sync(0xffffffffu, pts);
+  if ((threadIdx.x & 31) == 0 && dense) {
+    atomicAdd(&st[0], (unsigned long long)dense);
+    atomicAdd(&st[1], (unsigned long long)pts);
+  }
+}
+
+// Capped neighbour counts of the points of small cells (sorted order).
+__global__ void __launch_bounds__(128) k_cells_core(const float4 *__restrict__ nodes, int64_t m,
+                                                    const int64_t *__restrict__ cell_start, int64_t n,
+                                                    const int32_t *__restrict__ cell_of,
+                                                    const float4 *__restrict__ cpts, Radius R, int32_t min_pts,
+                                                    uint8_t *__restrict__ corep) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int32_t own = cell_of[k];
+  int32_t cnt = (int32_t)(cell_end(cell_start, m, n, own) - cell_start[own]);
+  if (cnt < min_pts) {
+    const float4 me = cpts[k];
+    const int64_t first_leaf = m - 1;
+    int32_t cur = 0;  // root: internal 0, or leaf 0 when m == 1
+    while (cur != kSentinel) {
+      const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+      if (cur < first_leaf) {
+        cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
+        continue;
+      }
+      const int64_t b = cur - first_leaf;
+      cur = node_rope(hi);
+      if (b == own || !hit_box(R, me.x, me.y, me.z, lo, hi)) continue;
+      const int64_t e = cell_end(cell_start, m, n, b);
+      for (int64_t j = cell_start[b]; j < e && cnt < min_pts; ++j) {
+        const float4 q = cpts[j];
+        cnt += hit_point(R, me.x, me.y, me.z, q.x, q.y, q.z);
+      }
+      if (cnt >= min_pts) break;
+    }
+  }
+  corep[k] = cnt >= min_pts;
+}
+
+// hascore[c]: the cell holds a core point
+__global__ void k_cells_has_core(const int64_t *__restrict__ cell_start, int64_t m, int64_t n,
+                                 const uint8_t *__restrict__ corep, uint8_t *__restrict__ hascore) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m; c += stride) {
+    const int64_t e = cell_end(cell_start, m, n, c);
+    uint8_t h = 0;
+    for (int64_t j = cell_start[c]; j < e && !h; ++j) h = corep[j];
+    hascore[c] = h;
+  }
+}
+
+// Core cells: rope walk over later cells; two cells unite at the first
+// core-core member pair within eps.
+__global__ void __launch_bounds__(128) k_cells_core_merge(const float4 *__restrict__ nodes, int64_t m,
+                                                          const int64_t *__restrict__ cell_start, int64_t n,
+                                                          const float4 *__restrict__ cpts,
+                                                          const uint8_t *__restrict__ corep,
+                                                          const uint8_t *__restrict__ hascore, Radius R,
+                                                          int32_t *parent, unsigned long long *checks_total) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t checks = 0;
+  if (a < m && hascore[a]) {
+    const int64_t first_leaf = m - 1;
+    const float4 qlo = ld_node(nodes, 2 * (first_leaf + a)), qhi = ld_node(nodes, 2 * (first_leaf + a) + 1);
+    const int64_t sa = cell_start[a], ea = cell_end(cell_start, m, n, a);
+    int32_t root = (int32_t)a;
+    int32_t cur = node_rope(qhi);
+    while (cur != kSentinel) {
+      const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+      if (cells_far(R, qlo, qhi, lo, hi)) {
+        cur = node_rope(hi);
+        continue;
+      }
+      if (cur < first_leaf) {
+        cur = node_link(lo);
+        continue;
+      }
+      const int32_t b = (int32_t)(cur - first_leaf);
+      cur = node_rope(hi);
+      if (!hascore[b] || parent[b] == root) continue;
+      const int32_t ra = uf_find(parent, root), rb = uf_find(parent, b);
+      root = ra;
+      if (ra == rb) continue;
+      const int64_t sb = cell_start[b], eb = cell_end(cell_start, m, n, b);
+      bool found = false;
+      for (int64_t i = sa; i < ea && !found; ++i) {
+        if (!corep[i]) continue;
+        const float4 x = cpts[i];
+        for (int64_t j = sb; j < eb; ++j) {
+          if (!corep[j]) continue;
+          const float4 y = cpts[j];
+          ++checks;
+          if (hit_point(R, x.x, x.y, x.z, y.x, y.y, y.z)) {
+            found = true;
+            break;
+          }
+        }
+      }
+      if (found) root = uf_union(parent, ra, rb);
+    }
+  }
+  add_checks(checks, checks_total);
+}
+
+// assign[k]: the cell whose set point k joins (-1: noise).
+__global__ void __launch_bounds__(128) k_cells_border(const float4 *__restrict__ nodes, int64_t m,
+                                                      const int64_t *__restrict__ cell_start, int64_t n,
+                                                      const int32_t *__restrict__ cell_of,
+                                                      const float4 *__restrict__ cpts,
+                                                      const uint8_t *__restrict__ corep,
+                                                      const uint8_t *__restrict__ hascore, Radius R,
+                                                      int32_t *__restrict__ assign,
+                                                      unsigned long long *checks_total) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t checks = 0;
+  if (k < n) {
+    const int32_t own = cell_of[k];
+    int32_t found = -1;
+    if (corep[k] || hascore[own]) {
+      found = own;
+    } else {
+      const float4 me = cpts[k];
+      const int64_t first_leaf = m - 1;
+      int32_t cur = 0;
+      while (cur != kSentinel && found < 0) {
+        const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+        if (cur < first_leaf) {
+          cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
+          continue;
+        }
+        const int32_t b = (int32_t)(cur - first_leaf);
+        cur = node_rope(hi);
+        if (!hascore[b] || !hit_box(R, me.x, me.y, me.z, lo, hi)) continue;
+        const int64_t e = cell_end(cell_start, m, n, b);
+        for (int64_t j = cell_start[b]; j < e; ++j) {
+          if (!corep[j]) continue;
+          const float4 q = cpts[j];
+          ++checks;
+          if (hit_point(R, me.x, me.y, me.z, q.x, q.y, q.z)) {
+            found = b;
+            break;
+          }
+        }
+      }
+    }
+    assign[k] = found;
+  }
+  add_checks(checks, checks_total);
+}
+
+__global__ void k_cells_compress(int64_t m, int32_t *parent) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < m; a += stride)
+    parent[a] = uf_root(parent, (int32_t)a);
+}
+
+__global__ void __launch_bounds__(256) k_cells_minobj(int64_t n, const int32_t *__restrict__ assign,
+                                                      const int32_t *__restrict__ parent,
+                                                      const uint32_t *__restrict__ order, int32_t *minobj) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int32_t key = -1, v = 0x7fffffff;
+  if (k < n) {
+    const int32_t a = assign[k];
+    if (a >= 0) {
+      key = parent[a];
+      v = (int32_t)order[k];
+    }
+  }
+  const uint32_t peers = __match_any_sync(0xffffffffu, key);
+  const int32_t mn = (int32_t)__reduce_min_sync(peers, (uint32_t)v);
+  if (key >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicMin(&minobj[key], mn);
+}
+
+__global__ void __launch_bounds__(256) k_cells_labels(int64_t n, const int32_t *__restrict__ assign,
+                                                      const int32_t *__restrict__ parent,
+                                                      const uint8_t *__restrict__ corep,
+                                                      const uint32_t *__restrict__ order,
+                                                      const int32_t *__restrict__ minobj, int32_t *__restrict__ labels,
+                                                      uint8_t *__restrict__ core) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int32_t a = assign[k];
+  const int32_t o = (int32_t)order[k];
+  labels[o] = a >= 0 ? minobj[parent[a]] : -1;
+  core[o] = corep[k];
+}
+
+}  // namespace
+
+bool dbscan_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t min_pts, int32_t *labels,
+                  uint8_t *core_out, DbscanResult *res) {
+  cudaEvent_t ev[5];
+  for (auto &e : ev) SPB_CUDA(cudaEventCreate(&e));
+  struct EvGuard {
+    cudaEvent_t *e;
+    ~EvGuard() {
+      for (int i = 0; i < 5; ++i) cudaEventDestroy(e[i]);
+    }
+  } guard{ev};
+  SPB_CUDA(cudaEventRecord(ev[0], c.stream));
+  mark(c, "start");
+  CellGrid g;
+  if (!build_cell_grid(c, pts, n, dim, eps, g)) return false;
+  const int64_t m = g.m;
+  c.count("cells", m);
+  const Radius R = make_radius(eps);
+  const unsigned Gm = grid_for(m, 256, 148 * 16);
+  DevBuf<unsigned long long> st(3, c.stream);  // dense cells, dense points, distance checks
+  SPB_CUDA(cudaMemsetAsync(st.get(), 0, 3 * sizeof(unsigned long long), c.stream));
+  k_cells_dense_stats<<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(g.cell_start.get(), m, n, min_pts, st.get());
+  SPB_LAUNCHED();
+  SPB_CUDA(cudaEventRecord(ev[1], c.stream));
+  DevBuf<uint8_t> corep((size_t)n, c.stream), hascore((size_t)m, c.stream);
+  k_cells_core<<<(unsigned)((n + 127) / 128), 128, 0, c.stream>>>(g.t.nodes, m, g.cell_start.get(), n,
+                                                                  g.cell_of.get(), g.cpts.get(), R, min_pts,
+                                                                  corep.get());
+  SPB_LAUNCHED();
+  k_cells_has_core<<<Gm, 256, 0, c.stream>>>(g.cell_start.get(), m, n, corep.get(), hascore.get());
+  SPB_LAUNCHED();
+  SPB_CUDA(cudaEventRecord(ev[2], c.stream));
+  mark(c, "core");
+  DevBuf<int32_t> parent((size_t)m, c.stream), minobj((size_t)m, c.stream), assign((size_t)n, c.stream);
+  k_iota32<<<Gm, 256, 0, c.stream>>>(parent.get(), m);
+  SPB_LAUNCHED();
+  k_cells_core_merge<<<(unsigned)((m + 127) / 128), 128, 0, c.stream>>>(g.t.nodes, m, g.cell_start.get(), n,
+                                                                        g.cpts.get(), corep.get(), hascore.get(), R,
+                                                                        parent.get(), st.get() + 2);
+  SPB_LAUNCHED();
+  mark(c, "merge_core");
+  k_cells_border<<<(unsigned)((n + 127) / 128), 128, 0, c.stream>>>(g.t.nodes, m, g.cell_start.get(), n,
+                                                                    g.cell_of.get(), g.cpts.get(), corep.get(),
+                                                                    hascore.get(), R, assign.get(), st.get() + 2);
+  SPB_LAUNCHED();
+  SPB_CUDA(cudaEventRecord(ev[3], c.stream));
+  mark(c, "merge");
+  k_cells_compress<<<Gm, 256, 0, c.stream>>>(m, parent.get());
+  SPB_LAUNCHED();
+  SPB_CUDA(cudaMemsetAsync(minobj.get(), 0x7f, (size_t)m * sizeof(int32_t), c.stream));
+  k_cells_minobj<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(n, assign.get(), parent.get(), g.order,
+                                                                    minobj.get());
+  SPB_LAUNCHED();
+  k_cells_labels<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(n, assign.get(), parent.get(), corep.get(),
+                                                                    g.order, minobj.get(), labels, core_out);
+  SPB_LAUNCHED();
+  SPB_CUDA(cudaEventRecord(ev[4], c.stream));
+  mark(c, "finalize");
+  if (c.async()) return true;  // statistics and timings need a host wait
+  unsigned long long hst[3] = {0, 0, 0};
+  SPB_CUDA(cudaMemcpyAsync(hst, st.get(), sizeof(hst), cudaMemcpyDeviceToHost, c.stream));
+  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  if (res) {
+    for (int i = 0; i < 4; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      res->ms[i] = ms;
+    }
+    res->num_dense_cells = (int64_t)hst[0];
+    res->num_dense_points = (int64_t)hst[1];
+    res->distance_checks = (int64_t)hst[2];
   }
   return true;
 }
