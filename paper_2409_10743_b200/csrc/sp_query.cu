@@ -362,6 +362,18 @@ __global__ void __launch_bounds__(128) k_knn(const float4 *__restrict__ nodes, i
   float *hd = KMAX > 0 ? hd_local : gdist + qi * (int64_t)kk;
   int32_t *hx = KMAX > 0 ? hi_local : gidx + qi * (int64_t)kk;
   int32_t size = 0;
+  // KMAX == 16: an ascending list in registers (worst = last real slot),
+  // sentinels (-inf) before the kk real slots; else a max-heap
+  constexpr bool REG = KMAX == 16;
+  if (REG) {
+#pragma unroll
+    for (int j = 0; j < (REG ? KMAX : 1); ++j) {
+      const bool real = j >= KMAX - kk;
+      hd_local[j] = __int_as_float(real ? 0x7f800000 : (int)0xff800000);
+      hi_local[j] = real ? 0x7fffffff : (int32_t)0x80000000;
+    }
+  }
+  auto worst = [&]() -> float { return REG ? hd_local[KMAX > 0 ? KMAX - 1 : 0] : hd[0]; };
 
   float sd[KNN_STACK];
   int32_t sr[KNN_STACK];
@@ -376,10 +388,26 @@ __global__ void __launch_bounds__(128) k_knn(const float4 *__restrict__ nodes, i
     --top;
     const float d = sd[top];
     const int32_t ref = sr[top];
-    if (size == kk && d > hd[0]) continue;
+    if (size == kk && d > worst()) continue;
     if (ref >= n - 1) {
       const int32_t obj = node_link(ld_node(nodes, 2 * (int64_t)ref));
-      if (size < kk) {  // push + sift up
+      if (REG) {
+        constexpr int K = KMAX > 0 ? KMAX : 1;
+        if (cand_less(d, obj, hd_local[K - 1], hi_local[K - 1])) {
+#pragma unroll
+          for (int j = K - 1; j > 0; --j) {
+            const bool shift = cand_less(d, obj, hd_local[j - 1], hi_local[j - 1]);
+            const bool here = !shift && cand_less(d, obj, hd_local[j], hi_local[j]);
+            hd_local[j] = shift ? hd_local[j - 1] : (here ? d : hd_local[j]);
+            hi_local[j] = shift ? hi_local[j - 1] : (here ? obj : hi_local[j]);
+          }
+          if (cand_less(d, obj, hd_local[0], hi_local[0])) {
+            hd_local[0] = d;
+            hi_local[0] = obj;
+          }
+          if (size < kk) ++size;
+        }
+      } else if (size < kk) {  // push + sift up
         int32_t i = size++;
         while (i > 0) {
           int32_t pa = (i - 1) >> 1;
@@ -420,8 +448,27 @@ __global__ void __launch_bounds__(128) k_knn(const float4 *__restrict__ nodes, i
       int32_t tr = rn; rn = rf; rf = tr;
     }
     const bool full = size == kk;
-    if (!(full && df > hd[0]) && top < KNN_STACK) { sd[top] = df; sr[top] = rf; ++top; }
-    if (!(full && dn > hd[0]) && top < KNN_STACK) { sd[top] = dn; sr[top] = rn; ++top; }
+    const float w = worst();
+    if (!(full && df > w) && top < KNN_STACK) { sd[top] = df; sr[top] = rf; ++top; }
+    if (!(full && dn > w) && top < KNN_STACK) { sd[top] = dn; sr[top] = rn; ++top; }
+  }
+  if (REG) {
+    constexpr int K = KMAX > 0 ? KMAX : 1;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int32_t r = j - (K - kk);
+      if (r >= 0 && r < size) {
+        const int64_t o = q * (int64_t)k + r;
+        out_idx[o] = hi_local[j];
+        if (out_dist) out_dist[o] = hd_local[j];
+      }
+    }
+    for (int32_t j = size; j < k; ++j) {
+      const int64_t o = q * (int64_t)k + j;
+      out_idx[o] = -1;
+      if (out_dist) out_dist[o] = __int_as_float(0x7f800000);
+    }
+    return;
   }
   // heap -> ascending order: repeatedly move the max to the end
   for (int32_t end = size - 1; end > 0; --end) {

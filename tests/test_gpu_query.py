@@ -148,3 +148,18 @@ def test_knn_k_at_least_n_and_degenerate(sp, oracle):
     assert sp.nearest_query(b, np.array([[0, 0, 0]], np.float32), 0).shape == (1, 0)
     idx = sp.nearest_query(b, np.array([[0, 0, 0]], np.float32), 1)
     assert idx.tolist() == [[0]]
+
+
+@pytest.mark.parametrize("scale", [1e-30, 1e-18, 1e15, 1e30])
+def test_knn_extreme_scales(sp, oracle, scale):
+    # the fp32 pruning filter switches off where squared gaps leave the normal
+    # range; results must stay exact at every scale
+    rng = np.random.default_rng(23)
+    pts = (rng.random((2000, 3)) * scale).astype(np.float32)
+    pts[100:140] = pts[7]  # duplicates: worst distance 0
+    org = np.concatenate([(rng.random((300, 3)) * scale).astype(np.float32), pts[:50]])
+    for k in (1, 16, 50):
+        idx, dist = sp.nearest_query(sp.Bvh.build(pts), org, k, with_distances=True)
+        widx, wdist = oracle.knn(pts, 3, org, k)
+        assert np.array_equal(idx, widx), k
+        assert same_float(dist, wdist)
