@@ -193,14 +193,12 @@ void morton_codes(Ctx &c, const float *objects, int64_t n, int dim, bool points,
 // memory in digit order and writes it out coalesced.  Stability of every pass
 // makes the final order equal std::stable_sort's (morton.hpp:113-121).
 // ---------------------------------------------------------------------------
-constexpr int RS_THREADS = 256;
-constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_BINS = 256;
 constexpr int RS_WH = RS_BINS + 1;  // + one slot for out-of-range items
 
-template <int ITEMS>
+template <int ITEMS, int THREADS>
 constexpr size_t rs_smem_bytes() {
-  return (size_t)RS_THREADS * ITEMS * 12 + (size_t)RS_WARPS * RS_WH * 4;
+  return (size_t)THREADS * ITEMS * 12 + (size_t)(THREADS / 32) * RS_WH * 4;
 }
 
 __global__ void __launch_bounds__(256) k_rs_hist(const uint64_t *__restrict__ keys, int64_t n, int npass,
@@ -220,7 +218,7 @@ __global__ void __launch_bounds__(256) k_rs_hist(const uint64_t *__restrict__ ke
 
 // Exclusive scan of each pass's 256 counts (one CTA per pass).
 __global__ void k_rs_scan(uint32_t *ghist) {
-  __shared__ uint32_t wsum[RS_WARPS];
+  __shared__ uint32_t wsum[RS_BINS / 32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   uint32_t *h = ghist + blockIdx.x * RS_BINS;
   uint32_t v = h[t], x = v;
@@ -244,23 +242,26 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
   return v;
 }
 
-template <int ITEMS>
-__global__ void __launch_bounds__(RS_THREADS, ITEMS <= 8 ? 4 : 2) k_rs_onesweep(
+// THREADS threads, ITEMS keys each; threads [0, 256) own one digit each for
+// the cross-warp prefix, the look-back and the tile-local digit scan.
+template <int ITEMS, int THREADS>
+__global__ void __launch_bounds__(THREADS, (THREADS * ITEMS <= 2048) ? 4 : (THREADS >= 512 ? 2 : 2)) k_rs_onesweep(
     const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
     uint32_t *__restrict__ vout, int64_t n, int shift, const uint32_t *__restrict__ binbase,
     unsigned long long *lookback, uint32_t *tile_ctr, uint32_t tag) {
-  constexpr int TILE = RS_THREADS * ITEMS;
+  constexpr int TILE = THREADS * ITEMS;
+  constexpr int WARPS = THREADS / 32;
   extern __shared__ __align__(16) unsigned char rs_smem[];
   uint64_t *skeys = reinterpret_cast<uint64_t *>(rs_smem);
   uint32_t *svals = reinterpret_cast<uint32_t *>(skeys + TILE);
   uint32_t *whist = svals + TILE;
   __shared__ uint32_t s_dstart[RS_BINS];
   __shared__ uint32_t s_gbase[RS_BINS];
-  __shared__ uint32_t s_wsum[RS_WARPS];
+  __shared__ uint32_t s_wsum[RS_BINS / 32];
   __shared__ uint32_t s_tile;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < RS_WARPS * RS_WH; i += RS_THREADS) whist[i] = 0;
+  for (int i = tid; i < WARPS * RS_WH; i += THREADS) whist[i] = 0;
   if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
@@ -307,50 +308,54 @@ __global__ void __launch_bounds__(RS_THREADS, ITEMS <= 8 ? 4 : 2) k_rs_onesweep(
   }
   __syncthreads();
 
-  // Thread t owns digit t: exclusive prefix over warps, then look-back.
+  // Thread t < 256 owns digit t: exclusive prefix over warps, then look-back.
   uint32_t tot = 0;
+  if (tid < RS_BINS) {
 #pragma unroll
-  for (int w = 0; w < RS_WARPS; ++w) {
-    const uint32_t cw = whist[w * RS_WH + tid];
-    whist[w * RS_WH + tid] = tot;
-    tot += cw;
-  }
-  const unsigned long long agg_tag = (unsigned long long)tag << 32;
-  const unsigned long long inc_tag = (unsigned long long)(tag + 1) << 32;
-  unsigned long long *mine = lookback + (size_t)tile * RS_BINS + tid;
-  uint32_t excl = 0;
-  if (tile == 0) {
-    st_volatile_u64(mine, inc_tag | tot);
-  } else {
-    st_volatile_u64(mine, agg_tag | tot);
-    int64_t j = (int64_t)tile - 1;
-    while (true) {
-      const unsigned long long v = ld_volatile_u64(lookback + (size_t)j * RS_BINS + tid);
-      const unsigned long long st = v & 0xffffffff00000000ull;
-      if (st == inc_tag) {
-        excl += (uint32_t)v;
-        break;
-      }
-      if (st == agg_tag) {
-        excl += (uint32_t)v;
-        --j;
-      }
+    for (int w = 0; w < WARPS; ++w) {
+      const uint32_t cw = whist[w * RS_WH + tid];
+      whist[w * RS_WH + tid] = tot;
+      tot += cw;
     }
-    st_volatile_u64(mine, inc_tag | (excl + tot));
+    const unsigned long long agg_tag = (unsigned long long)tag << 32;
+    const unsigned long long inc_tag = (unsigned long long)(tag + 1) << 32;
+    unsigned long long *mine = lookback + (size_t)tile * RS_BINS + tid;
+    uint32_t excl = 0;
+    if (tile == 0) {
+      st_volatile_u64(mine, inc_tag | tot);
+    } else {
+      st_volatile_u64(mine, agg_tag | tot);
+      int64_t j = (int64_t)tile - 1;
+      while (true) {
+        const unsigned long long v = ld_volatile_u64(lookback + (size_t)j * RS_BINS + tid);
+        const unsigned long long st = v & 0xffffffff00000000ull;
+        if (st == inc_tag) {
+          excl += (uint32_t)v;
+          break;
+        }
+        if (st == agg_tag) {
+          excl += (uint32_t)v;
+          --j;
+        }
+      }
+      st_volatile_u64(mine, inc_tag | (excl + tot));
+    }
+    s_gbase[tid] = binbase[tid] + excl;
+    // tile-local digit starts: exclusive scan of tot over the 256 digits
+    uint32_t x = tot;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
+    }
+    if (lane == 31) s_wsum[warp] = x;
+    tot = x - tot;  // exclusive within the warp
   }
-  s_gbase[tid] = binbase[tid] + excl;
-
-  // Tile-local digit starts: exclusive scan of tot over the 256 digits.
-  uint32_t x = tot;
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-    if (lane >= d) x += y;
-  }
-  if (lane == 31) s_wsum[warp] = x;
   __syncthreads();
-  uint32_t off = 0;
-  for (int w = 0; w < warp; ++w) off += s_wsum[w];
-  s_dstart[tid] = off + x - tot;
+  if (tid < RS_BINS) {
+    uint32_t off = 0;
+    for (int w = 0; w < warp; ++w) off += s_wsum[w];
+    s_dstart[tid] = off + tot;
+  }
   __syncthreads();
 
 #pragma unroll
@@ -364,7 +369,7 @@ __global__ void __launch_bounds__(RS_THREADS, ITEMS <= 8 ? 4 : 2) k_rs_onesweep(
   }
   __syncthreads();
   const int valid = (int)((n - base) < (int64_t)TILE ? (n - base) : (int64_t)TILE);
-  for (int pos = tid; pos < valid; pos += RS_THREADS) {
+  for (int pos = tid; pos < valid; pos += THREADS) {
     const uint64_t k = skeys[pos];
     const uint32_t d = (uint32_t)(k >> shift) & 0xffu;
     const uint32_t o = s_gbase[d] + (uint32_t)pos - s_dstart[d];
@@ -373,14 +378,22 @@ __global__ void __launch_bounds__(RS_THREADS, ITEMS <= 8 ? 4 : 2) k_rs_onesweep(
   }
 }
 
-template <int ITEMS>
+#ifndef SPB_RS_THREADS
+#define SPB_RS_THREADS 256
+#endif
+#ifndef SPB_RS_ITEMS
+#define SPB_RS_ITEMS 16
+#endif
+
+template <int ITEMS, int THREADS>
 void onesweep_passes(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_alt, uint32_t **vals_alt, int64_t n,
                      int npass, bool vals_iota) {
-  constexpr int TILE = RS_THREADS * ITEMS;
-  constexpr size_t SMEM = rs_smem_bytes<ITEMS>();
+  constexpr int TILE = THREADS * ITEMS;
+  constexpr size_t SMEM = rs_smem_bytes<ITEMS, THREADS>();
   static bool attr_set = false;
   if (!attr_set) {
-    SPB_CUDA(cudaFuncSetAttribute(k_rs_onesweep<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    SPB_CUDA(cudaFuncSetAttribute(k_rs_onesweep<ITEMS, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)SMEM));
     attr_set = true;
   }
   const int64_t ntiles = (n + TILE - 1) / TILE;
@@ -396,7 +409,7 @@ void onesweep_passes(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_a
   if (getenv("SPB_SORT_MARKS")) mark(c, "sort_hist");
   uint32_t *ctr = hist.get() + (size_t)npass * RS_BINS;
   for (int p = 0; p < npass; ++p) {
-    k_rs_onesweep<ITEMS><<<(unsigned)ntiles, RS_THREADS, SMEM, c.stream>>>(
+    k_rs_onesweep<ITEMS, THREADS><<<(unsigned)ntiles, THREADS, SMEM, c.stream>>>(
         *keys, (p == 0 && vals_iota) ? nullptr : *vals, *keys_alt, *vals_alt, n, 8 * p,
         hist.get() + (size_t)p * RS_BINS, lookback.get(), ctr + p, (uint32_t)(2 * p + 1));
     SPB_LAUNCHED();
@@ -413,10 +426,7 @@ void radix_sort_pairs(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_
     return;
   }
   const int npass = std::max(1, (key_bits + 7) / 8);
-  static const int items = getenv("SPB_RS_ITEMS") ? atoi(getenv("SPB_RS_ITEMS")) : 16;
-  if (items >= 16) onesweep_passes<16>(c, keys, vals, keys_alt, vals_alt, n, npass, vals_iota);
-  else if (items >= 12) onesweep_passes<12>(c, keys, vals, keys_alt, vals_alt, n, npass, vals_iota);
-  else onesweep_passes<8>(c, keys, vals, keys_alt, vals_alt, n, npass, vals_iota);
+  onesweep_passes<SPB_RS_ITEMS, SPB_RS_THREADS>(c, keys, vals, keys_alt, vals_alt, n, npass, vals_iota);
 }
 
 // ---------------------------------------------------------------------------

@@ -1,3 +1,1 @@
-python paper_2409_10743_b200/build.py >/dev/null
-for k in 0 1 2 3 4; do echo "== cfg $k"; SPB_RS_CFG=$k timeout 60 python scripts/prof_fof.py 134217728 3 2>&1 | tail -1; done
-for k in 1 2 3 4; do SPB_RS_CFG=$k timeout 120 python -m pytest tests/test_gpu_bvh.py -x -q -k "random or golden or c1" 2>&1 | tail -1; done
+for v in "$@"; do cp var/$v.so paper_2409_10743_b200/libspb200.so; echo "== $v"; timeout 120 python scripts/build_probe.py 2>&1 | tail -2; done
