@@ -510,6 +510,9 @@ def _dbscan(points, eps, min_pts, algo, width, ctx, out=None):
     dev = mem == SP_MEM_DEVICE
     if out is not None:
         labels, core = out
+        if _is_cuda(labels) != dev or _is_cuda(core) != dev:
+            # one memory-space flag covers every pointer of the call (sp_b200.h)
+            raise ValueError("out arrays must live in the same memory space as the points")
         lp, cp = _ptr(labels), _ptr(core)
     else:
         labels, lp = _out(dev, (n,), np.int32, _torch_dtype("int32") if dev else None, points.device if dev else None)

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstring>
+
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
@@ -26,6 +28,41 @@ void mark(Ctx &c, const char *name) {
   c.mark_names[c.marks_used] = name;
   SPB_CUDA(cudaEventRecord(c.event_pool[c.marks_used], c.stream));
   ++c.marks_used;
+}
+
+namespace {
+struct PeekArgs {
+  const uint8_t *src[8];
+  uint32_t off[8];
+  uint32_t bytes[8];
+  int k;
+};
+__global__ void k_peek(PeekArgs a, uint8_t *dst) {
+  for (int i = 0; i < a.k; ++i)
+    for (uint32_t b = threadIdx.x; b < a.bytes[i]; b += blockDim.x) dst[a.off[i] + b] = a.src[i][b];
+}
+}  // namespace
+
+void peek(Ctx &c, std::initializer_list<PeekItem> items) {
+  if (!c.peek_buf) SPB_CUDA(cudaHostAlloc((void **)&c.peek_buf, 1024, cudaHostAllocMapped | cudaHostAllocPortable));
+  PeekArgs a{};
+  uint32_t off = 0;
+  for (const PeekItem &it : items) {
+    if (a.k == 8 || it.bytes > 64) throw CudaError("peek: too many or too large items");
+    a.src[a.k] = static_cast<const uint8_t *>(it.src);
+    a.off[a.k] = off;
+    a.bytes[a.k] = it.bytes;
+    off += (it.bytes + 7) & ~7u;
+    ++a.k;
+  }
+  k_peek<<<1, 64, 0, c.stream>>>(a, c.peek_buf);
+  SPB_LAUNCHED();
+  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  off = 0;
+  for (const PeekItem &it : items) {
+    memcpy(it.dst, c.peek_buf + off, it.bytes);
+    off += (it.bytes + 7) & ~7u;
+  }
 }
 
 void reset_marks(Ctx &c) {
@@ -552,8 +589,7 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
     SPB_LAUNCHED();
   } else {
     int h_bad = 0;
-    SPB_CUDA(cudaMemcpyAsync(&h_bad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-    SPB_CUDA(cudaStreamSynchronize(c.stream));
+    peek(c, {{bad.get(), &h_bad, sizeof(int)}});
     if (h_bad) throw InvalidArgument("bvh: non-finite object bounds");
   }
   if (n == 0) return;

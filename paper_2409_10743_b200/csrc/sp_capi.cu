@@ -38,6 +38,40 @@ void stream_after(cudaStream_t waiter, cudaStream_t producer) {
   SPB_CUDA(cudaEventDestroy(e));
 }
 
+// SPB_DEBUG_E2E=1: timestamp the copies and the compute of every call with
+// events and print the timeline at sp_ctx_synchronize (pipeline diagnostics).
+struct TraceEv {
+  const char *what;
+  int64_t call;
+  cudaEvent_t e;
+};
+std::vector<TraceEv> &trace() {
+  static std::vector<TraceEv> t;
+  return t;
+}
+bool tracing() {
+  static const bool on = getenv("SPB_DEBUG_E2E") != nullptr;
+  return on;
+}
+void trace_ev(spb::Ctx &c, const char *what, cudaStream_t s) {
+  if (!tracing()) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, s);
+  trace().push_back({what, c.calls, e});
+}
+void trace_dump() {
+  if (!tracing() || trace().empty()) return;
+  cudaEvent_t t0 = trace().front().e;
+  for (auto &t : trace()) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t0, t.e);
+    fprintf(stderr, "[e2e] call %lld %-12s %9.2f ms\n", (long long)t.call, t.what, ms);
+  }
+  for (auto &t : trace()) cudaEventDestroy(t.e);
+  trace().clear();
+}
+
 spb::Ctx::Staging &stage(spb::Ctx &c, bool input, size_t bytes) {
   const int parity = (int)(c.calls & 1);
   int &used = input ? c.in_used : c.out_used;
@@ -73,8 +107,11 @@ struct In {
     st = &stage(c, true, count * sizeof(T));
     ctx = &c;
     SPB_CUDA(cudaStreamWaitEvent(c.h2d, st->done, 0));
+    trace_ev(c, "h2d begin", c.h2d);
     SPB_CUDA(cudaMemcpyAsync(st->p, src, count * sizeof(T), cudaMemcpyHostToDevice, c.h2d));
+    trace_ev(c, "h2d end", c.h2d);
     stream_after(c.stream, c.h2d);
+    trace_ev(c, "compute go", c.stream);
     p = static_cast<const T *>(st->p);
   }
   ~In() {
@@ -104,8 +141,11 @@ struct Out {
   }
   void flush(spb::Ctx &c) {
     if (!host) return;
+    trace_ev(c, "compute end", c.stream);
     stream_after(c.d2h, c.stream);
+    trace_ev(c, "d2h begin", c.d2h);
     SPB_CUDA(cudaMemcpyAsync(host, st->p, count * sizeof(T), cudaMemcpyDeviceToHost, c.d2h));
+    trace_ev(c, "d2h end", c.d2h);
     SPB_CUDA(cudaEventRecord(st->done, c.d2h));
   }
 };
@@ -123,19 +163,23 @@ struct DeviceGuard {
   }
 };
 
+// fresh = false (sp_ctx_synchronize): not a pipeline call, so the marks and
+// counters of the last asynchronous call are kept and resolved.
 template <class F>
-int guarded(sp_ctx *ctx, F &&f) {
+int guarded(sp_ctx *ctx, F &&f, bool fresh = true) {
   if (!ctx) return SP_EINVAL;
   DeviceGuard dg(ctx->c.device);
   spb::g_launch_counter = &ctx->c.launches;
-  spb::reset_marks(ctx->c);
-  ctx->c.in_used = ctx->c.out_used = 0;
-  ctx->c.counters.clear();
-  ++ctx->c.calls;
+  if (fresh) {
+    spb::reset_marks(ctx->c);
+    ctx->c.in_used = ctx->c.out_used = 0;
+    ctx->c.counters.clear();
+    ++ctx->c.calls;
+  }
   int rc = SP_OK;
   try {
     f(ctx->c);
-    if (ctx->c.marks_used && !ctx->c.async()) {
+    if (ctx->c.marks_used && (!ctx->c.async() || !fresh)) {
       SPB_CUDA(cudaStreamSynchronize(ctx->c.stream));
       spb::resolve_marks(ctx->c);
     }
@@ -225,6 +269,7 @@ int sp_ctx_destroy(sp_ctx *ctx) {
     if (ctx->c.h2d) cudaStreamDestroy(ctx->c.h2d);
     if (ctx->c.d2h) cudaStreamDestroy(ctx->c.d2h);
     if (ctx->c.d_err) cudaFree(ctx->c.d_err);
+    if (ctx->c.peek_buf) cudaFreeHost(ctx->c.peek_buf);
     for (auto *arr : {&ctx->c.in_stage, &ctx->c.out_stage})
       for (auto &row : *arr)
         for (auto &st : row) {
@@ -260,13 +305,14 @@ int sp_ctx_set_stream(sp_ctx *ctx, void *stream) {
 int sp_ctx_synchronize(sp_ctx *ctx) {
   return guarded(ctx, [&](spb::Ctx &c) {
     sync_all(c);
+    trace_dump();
     int err = 0;
     SPB_CUDA(cudaMemcpy(&err, c.d_err, sizeof(int), cudaMemcpyDeviceToHost));
     if (err) {
       SPB_CUDA(cudaMemset(c.d_err, 0, sizeof(int)));
       throw spb::InvalidArgument("non-finite coordinate in an asynchronous call");
     }
-  });
+  }, /*fresh=*/false);
 }
 
 int sp_ctx_set_flags(sp_ctx *ctx, int flags) {

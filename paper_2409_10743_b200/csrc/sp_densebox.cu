@@ -738,9 +738,7 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
   scene_bounds(c, pts, n, dim, true, scene.get(), bad.get());
   float hs[6];
   int hbad = 0;
-  SPB_CUDA(cudaMemcpyAsync(hs, scene.get(), sizeof(hs), cudaMemcpyDeviceToHost, c.stream));
-  SPB_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  host_sync(c, __LINE__);
+  peek(c, {{scene.get(), hs, sizeof(hs)}, {bad.get(), &hbad, sizeof(int)}});
   if (hbad) {
     for (auto &e : ev) cudaEventDestroy(e);
     throw InvalidArgument("dbscan: non-finite coordinate");
@@ -798,8 +796,7 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
     SPB_LAUNCHED();
     exclusive_scan(c, head.get(), n, hscan.get());
     int64_t m = 0;
-    SPB_CUDA(cudaMemcpyAsync(&m, hscan.get() + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
-    host_sync(c, __LINE__);
+    peek(c, {{hscan.get() + n, &m, sizeof(int64_t)}});
     cell_start = DevBuf<int64_t>((size_t)m, c.stream);
     k_cell_starts<<<G, 256, 0, c.stream>>>(head.get(), hscan.get(), n, cell_start.get());
     SPB_LAUNCHED();
@@ -809,8 +806,7 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
     k_dense_flags<<<Gm, 256, 0, c.stream>>>(cell_start.get(), m, n, min_pts, no_dense, dense.get());
     SPB_LAUNCHED();
     exclusive_scan(c, dense.get(), m, dscan.get());
-    SPB_CUDA(cudaMemcpyAsync(&nd, dscan.get() + m, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
-    host_sync(c, __LINE__);
+    peek(c, {{dscan.get() + m, &nd, sizeof(int64_t)}});
     if (nd > 0) {
       // dense cells ordered by their smallest member
       DevBuf<uint64_t> mk0((size_t)nd, c.stream), mk1((size_t)nd, c.stream);
@@ -838,8 +834,7 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
   SPB_LAUNCHED();
   exclusive_scan(c, sflag.get(), n, sscan.get());
   int64_t ns = 0;
-  SPB_CUDA(cudaMemcpyAsync(&ns, sscan.get() + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
-  host_sync(c, __LINE__);
+  peek(c, {{sscan.get() + n, &ns, sizeof(int64_t)}});
   num_dense_points = n - ns;
   DevBuf<int32_t> sparse_pts((size_t)(ns > 0 ? ns : 1), c.stream);
   k_sparse_objects<<<G, 256, 0, c.stream>>>(point_cell.get(), sscan.get(), n, nd, pts, dim, sparse_pts.get(),
@@ -916,9 +911,7 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
   SPB_CUDA(cudaEventRecord(ev[4], c.stream));
   mark(c, "finalize");
   unsigned long long hchecks = 0;
-  SPB_CUDA(cudaMemcpyAsync(&hchecks, checks.get(), sizeof(hchecks), cudaMemcpyDeviceToHost, c.stream));
-  SPB_CUDA(cudaEventSynchronize(ev[4]));
-  host_sync(c, __LINE__);
+  peek(c, {{checks.get(), &hchecks, sizeof(hchecks)}});
   if (res) {
     for (int i = 0; i < 4; ++i) {
       float ms = 0.f;
@@ -960,9 +953,7 @@ bool build_cell_grid(Ctx &c, const float *pts, int64_t n, int dim, float eps, Ce
   scene_bounds(c, pts, n, dim, true, scene.get(), bad.get());
   float hs[6];
   int hbad = 0;
-  SPB_CUDA(cudaMemcpyAsync(hs, scene.get(), sizeof(hs), cudaMemcpyDeviceToHost, c.stream));
-  SPB_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  peek(c, {{scene.get(), hs, sizeof(hs)}, {bad.get(), &hbad, sizeof(int)}});
   if (hbad) throw InvalidArgument("dbscan: non-finite coordinate");
   int bits = 1;
   for (int k = 0; k < dim; ++k) {
@@ -996,8 +987,7 @@ bool build_cell_grid(Ctx &c, const float *pts, int64_t n, int dim, float eps, Ce
   SPB_LAUNCHED();
   exclusive_scan(c, head.get(), n, hscan.get());
   int64_t m = 0;
-  SPB_CUDA(cudaMemcpyAsync(&m, hscan.get() + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
-  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  peek(c, {{hscan.get() + n, &m, sizeof(int64_t)}});
   g.m = m;
   g.cell_start = DevBuf<int64_t>((size_t)m, c.stream);
   k_cell_starts<<<G, 256, 0, c.stream>>>(head.get(), hscan.get(), n, g.cell_start.get());
@@ -1362,8 +1352,7 @@ bool dbscan_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32
   mark(c, "finalize");
   if (c.async()) return true;  // statistics and timings need a host wait
   unsigned long long hst[3] = {0, 0, 0};
-  SPB_CUDA(cudaMemcpyAsync(hst, st.get(), sizeof(hst), cudaMemcpyDeviceToHost, c.stream));
-  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  peek(c, {{st.get(), hst, sizeof(hst)}});
   if (res) {
     for (int i = 0; i < 4; ++i) {
       float ms = 0.f;

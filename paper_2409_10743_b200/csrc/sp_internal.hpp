@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <initializer_list>
 #include <string>
 #include <utility>
 #include <vector>
@@ -49,8 +50,21 @@ struct Ctx {
   int in_used = 0, out_used = 0;
   // diagnostic counters of the last call (e.g. "fof_cells": non-empty cells)
   std::vector<std::pair<std::string, int64_t>> counters;
+  uint8_t *peek_buf = nullptr;  // host-mapped pinned scratch for peek()
   void count(const char *name, int64_t v) { counters.emplace_back(name, v); }
 };
+
+// Small device-to-host reads (sizes, flags, bounds) through host-mapped pinned
+// memory written by a kernel, then a wait on the context stream.  No copy
+// engine is involved, so the read never queues behind a bulk download on the
+// same engine (with SP_FLAG_ASYNC the previous call's results are still
+// streaming out while the next call needs its scene bounds).
+struct PeekItem {
+  const void *src;  // device
+  void *dst;        // host
+  uint32_t bytes;   // <= 64
+};
+void peek(Ctx &c, std::initializer_list<PeekItem> items);
 
 // Record a phase boundary on the context stream (cheap; no host sync).
 void mark(Ctx &c, const char *name);

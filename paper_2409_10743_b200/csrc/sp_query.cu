@@ -250,8 +250,7 @@ int64_t range_crs(Ctx &c, const Tree &t, int kind, const float *preds, int64_t n
   range_count(c, t, kind, preds, nq, 0.f, 0, counts.get(), order.get());
   exclusive_scan(c, counts.get(), nq, offsets);
   int64_t total = 0;
-  SPB_CUDA(cudaMemcpyAsync(&total, offsets + nq, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
-  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  peek(c, {{offsets + nq, &total, sizeof(int64_t)}});
   if (total > capacity) return total;
   if (total == 0 || t.n == 0) return total;
   DevBuf<uint64_t> k0((size_t)total, c.stream), k1((size_t)total, c.stream);
@@ -320,8 +319,7 @@ int64_t pair_list(Ctx &c, const Tree &t, float eps, int32_t *pairs, int64_t capa
   SPB_LAUNCHED();
   exclusive_scan(c, counts.get(), t.n, offsets.get());
   int64_t total = 0;
-  SPB_CUDA(cudaMemcpyAsync(&total, offsets.get() + t.n, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
-  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  peek(c, {{offsets.get() + t.n, &total, sizeof(int64_t)}});
   if (total > capacity || total == 0) return total;
   k_pairs<true><<<g, 128, 0, c.stream>>>(t.nodes, t.n, thr, nullptr, offsets.get(), pairs);
   SPB_LAUNCHED();
@@ -655,8 +653,7 @@ int64_t check_equivalence(Ctx &c, const float *pts, int64_t n, int dim, float ep
                                                                    gc, first.get() + 4);
   SPB_LAUNCHED();
   unsigned long long h[5];
-  SPB_CUDA(cudaMemcpyAsync(h, first.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
-  SPB_CUDA(cudaStreamSynchronize(c.stream));
+  peek(c, {{first.get(), h, sizeof(h)}});
   for (int k = 0; k < 5; ++k)
     if (h[k] != ~0ull) {
       *kind = k + 1;

@@ -26,3 +26,13 @@ t = time.perf_counter()
 x = hp.cuda(); torch.cuda.synchronize(); print("h2d %.1f ms" % ((time.perf_counter() - t) * 1e3))
 t = time.perf_counter()
 hl.copy_(torch.empty(n, dtype=torch.int32, device=dev)); torch.cuda.synchronize(); print("d2h labels %.1f ms" % ((time.perf_counter() - t) * 1e3))
+# per-phase times of an overlapped (async) step vs a device-resident step
+c3 = sp.Context(0, stream=torch.cuda.Stream(dev).cuda_stream)
+sp.friends_of_friends(pts, eps, ctx=c3)
+print("device-resident phases", [(k, round(v, 2)) for k, v in c3.phases()])
+c2 = sp.Context(0, stream=torch.cuda.Stream(dev).cuda_stream)
+c2.set_async(True)
+for _ in range(4):
+    sp.friends_of_friends(hp, eps, ctx=c2, out=(hl, hc))
+c2.synchronize()
+print("async e2e phases (last call)", [(k, round(v, 2)) for k, v in c2.phases()])
