@@ -199,7 +199,7 @@ def workload_config(args, world):
     return {"workload": "fof_field: friends_of_friends on HACC-like clustered 3D fp32 field, "
                         "%d points per GPU (C5 per-GPU share), eps = 0.168*n_total^(-1/3)" % n,
             "points_per_gpu": n, "points_total": n * world, "eps": eps_for(n * world), "min_pts": 2,
-            "parallelism": "x-slabs over %d GPU(s) with eps ghost layers" % world if world > 1 else "single GPU",
+            "parallelism": "x-slabs over %d GPU(s) with eps ghost layers" % world if (world > 1 or args.slabs) else "single GPU",
             "l2": "inputs (%.1f GB) larger than L2 (126 MB); no flush needed" % (n * 12 / 1e9)}
 
 
@@ -220,7 +220,8 @@ def run_ours(args, rank, world, local_rank):
     n = args.n
     n_total = n * world
     eps = eps_for(n_total)
-    if world > 1:
+    slabs = world > 1 or args.slabs
+    if slabs:
         from paper_2409_10743_b200 import distributed as spd
         pts = sp.generate_field(n_total, first=rank * n, count=n, seed=args.seed, ctx=ctx)
         step = lambda: spd.fof_slabs(pts, eps, first_index=rank * n, ctx=ctx)
@@ -231,7 +232,7 @@ def run_ours(args, rank, world, local_rank):
         step = lambda: sp.friends_of_friends(pts, eps, ctx=ctx, out=(labels, core))
 
     def barrier():
-        if world > 1:
+        if slabs:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
@@ -242,7 +243,7 @@ def run_ours(args, rank, world, local_rank):
     cells = ctx.counter("fof_cells")
     key_bits = 3 * max(1, int(np.ceil(np.log2(1.0 / (eps / np.sqrt(3.0) * (1 - 1e-6)) + 1))))
     pairs_per_pt = None
-    if world == 1:
+    if not slabs:
         b = sp.Bvh.build(pts, ctx=ctx)
         import ctypes
         tot = ctypes.c_int64(0)
@@ -268,7 +269,7 @@ def run_ours(args, rank, world, local_rank):
     launches = ctx.kernel_launches - launches0
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if slabs:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     ms_per_step = ms / args.steps
@@ -278,7 +279,7 @@ def run_ours(args, rank, world, local_rank):
     e2e_value = None
     h2d = n * 12
     d2h = n * 5
-    if world == 1:
+    if not slabs:
         # Public API with pinned HOST buffers: every step uploads its points
         # and downloads its labels + core flags.  The context runs with
         # SP_FLAG_ASYNC: uploads/downloads go on its copy streams, so step
@@ -305,7 +306,31 @@ def run_ours(args, rank, world, local_rank):
         # the host run must agree bit-for-bit with the device-resident run
         assert torch.equal(host_labels, labels.cpu()) and torch.equal(host_core, core.cpu()), "e2e != device run"
     else:
-        e2e_value = value  # replaced by the distributed host-buffer path once it lands
+        # each rank uploads its pinned host slice, runs the slab FoF over NCCL
+        # and downloads its labels + core flags, copies inside the timed region
+        from paper_2409_10743_b200 import distributed as spd
+        host_pts = torch.empty((n, 3), dtype=torch.float32, pin_memory=True)
+        host_pts.copy_(pts)
+        host_labels = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        host_core = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+
+        def e2e_step():
+            d = host_pts.to(dev, non_blocking=True)
+            lab, cor = spd.fof_slabs(d, eps, first_index=rank * n, ctx=ctx)
+            host_labels.copy_(lab, non_blocking=True)
+            host_core.copy_(cor, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_start.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e_end.record(stream)
+        barrier()
+        t = torch.tensor([e_start.elapsed_time(e_end)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_value = n_total * args.steps / (float(t.item()) / 1e3)
 
     peak, peak_src = measured_peak()
     phases = {k: v / args.steps for k, v in phase_acc.items()}
@@ -503,6 +528,8 @@ def main():
     ap.add_argument("--seed", type=int, default=2409)
     ap.add_argument("--cpu-sample-n", type=int, default=1 << 22)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slabs", action="store_true",
+                    help="run the multi-GPU slab path (NCCL) even at one rank (tests the N > 1 code on one GPU)")
     ap.add_argument("--workload", default="fof_field", choices=["fof_field"] + sorted(CONFIGS),
                     help="fof_field is the headline; c1..c4 are the other SURVEY §8(d) configs (1 GPU)")
     args = ap.parse_args()
@@ -511,9 +538,14 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and rank == 0:
         print("warning: --gpus %d but WORLD_SIZE %d" % (args.gpus, world), file=sys.stderr)
-    if world > 1:
+    if world > 1 or args.slabs:
         import torch
         import torch.distributed as dist
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         backend = "nccl" if args.impl == "ours" else "gloo"
         if args.impl == "ours":
             torch.cuda.set_device(local_rank)
@@ -526,7 +558,7 @@ def main():
         else:
             run_ours(args, rank, world, local_rank)
     finally:
-        if world > 1:
+        if world > 1 or args.slabs:
             import torch.distributed as dist
             dist.barrier()
             dist.destroy_process_group()

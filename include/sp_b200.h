@@ -73,7 +73,8 @@ typedef struct {
 } sp_stats;
 
 /* ---- context (replaces ExecMode / parallel_for, exec.hpp:12-26) ---------- */
-/* stream: a cudaStream_t to run on, or NULL for a context-owned stream. */
+/* stream: a cudaStream_t to run on, or NULL for a context-owned stream
+ * (cudaStreamLegacy, (void *)1, selects the legacy default stream). */
 int sp_ctx_create(int device, void *stream, sp_ctx **out);
 int sp_ctx_destroy(sp_ctx *ctx);
 int sp_ctx_set_stream(sp_ctx *ctx, void *stream);

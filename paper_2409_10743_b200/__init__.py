@@ -125,12 +125,21 @@ class _Stats(C.Structure):
     _fields_ = [("distance_checks", C.c_int64), ("num_dense_cells", C.c_int64), ("num_dense_points", C.c_int64)]
 
 
+def _stream_arg(stream: Optional[int]):
+    """None -> a context-owned stream; a cudaStream_t handle otherwise.  Handle
+    0 (torch's default stream) is the legacy default stream, which the C ABI
+    takes as cudaStreamLegacy ((void *)1) because NULL means "own stream"."""
+    if stream is None:
+        return None
+    return C.c_void_p(stream if stream != 0 else 1)
+
+
 class Context:
     """An sp_ctx: one device + one stream (exec.hpp's ExecMode analogue)."""
 
     def __init__(self, device: int = 0, stream: Optional[int] = None):
         h = C.c_void_p()
-        rc = _lib.sp_ctx_create(device, C.c_void_p(stream) if stream else None, C.byref(h))
+        rc = _lib.sp_ctx_create(device, _stream_arg(stream), C.byref(h))
         if rc != SP_OK:
             raise CudaError("sp_ctx_create(device=%d) failed (status %d): no usable CUDA device" % (device, rc))
         self.h = h
@@ -148,7 +157,7 @@ class Context:
             pass
 
     def set_stream(self, stream: Optional[int]):
-        self._check(_lib.sp_ctx_set_stream(self.h, C.c_void_p(stream) if stream else None))
+        self._check(_lib.sp_ctx_set_stream(self.h, _stream_arg(stream)))
 
     def synchronize(self):
         self._check(_lib.sp_ctx_synchronize(self.h))

@@ -988,6 +988,9 @@ bool build_cell_grid(Ctx &c, const float *pts, int64_t n, int dim, float eps, Ce
   exclusive_scan(c, head.get(), n, hscan.get());
   int64_t m = 0;
   peek(c, {{hscan.get() + n, &m, sizeof(int64_t)}});
+  if (getenv("SPB_DEBUG_PEEK"))
+    fprintf(stderr, "[grid] n %lld scene %g %g %g .. %g %g %g bits %d cells %lld\n", (long long)n, hs[0], hs[1], hs[2],
+            hs[3], hs[4], hs[5], bits, (long long)m);
   g.m = m;
   g.cell_start = DevBuf<int64_t>((size_t)m, c.stream);
   k_cell_starts<<<G, 256, 0, c.stream>>>(head.get(), hscan.get(), n, g.cell_start.get());

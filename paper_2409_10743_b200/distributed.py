@@ -32,7 +32,6 @@ from __future__ import annotations
 
 from typing import Callable, Optional, Tuple
 
-import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -68,30 +67,45 @@ def _device_fof(ctx):
     import paper_2409_10743_b200 as sp
 
     def run(points: torch.Tensor, eps: float):
+        # the torch ops that produced `points` ran on torch's current stream;
+        # a context on another stream must not start before they finish
+        if ctx is not None and points.is_cuda:
+            torch.cuda.current_stream(points.device).synchronize()
         out = sp.friends_of_friends(points, eps, ctx=ctx)
         return out.labels, out.core_flags
 
     return run
 
 
-def label_components(keys: np.ndarray, labels: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+def label_components(keys: torch.Tensor, labels: torch.Tensor) -> Tuple[torch.Tensor, torch.Tensor]:
     """Labels that share a key are connected; returns (unique labels, the
-    minimum label of each one's component)."""
-    from scipy.sparse import coo_matrix
-    from scipy.sparse.csgraph import connected_components
-
-    uniq, inv = np.unique(labels, return_inverse=True)
-    if len(uniq) == 0:
+    minimum label of each one's component).  Runs where the tensors live (the
+    GPU under NCCL): hook-to-min union-find over the compacted labels with
+    pointer jumping, the same invariant as the device union-find (a root is
+    the smallest member, union_find.hpp:15-16)."""
+    keys = torch.as_tensor(keys)
+    labels = torch.as_tensor(labels, device=keys.device)
+    uniq, inv = torch.unique(labels, return_inverse=True)
+    if uniq.numel() == 0:
         return uniq, uniq
-    order = np.argsort(keys, kind="stable")
+    order = torch.argsort(keys, stable=True)
     k, v = keys[order], inv[order]
     same = k[1:] == k[:-1]
     a, b = v[:-1][same], v[1:][same]
-    g = coo_matrix((np.ones(len(a), np.int8), (a, b)), shape=(len(uniq), len(uniq)))
-    _, comp = connected_components(g, directed=False)
-    comp_min = np.full(comp.max() + 1, np.iinfo(np.int64).max, np.int64)
-    np.minimum.at(comp_min, comp, uniq)
-    return uniq, comp_min[comp]
+    parent = torch.arange(uniq.numel(), device=uniq.device, dtype=torch.int64)
+    while True:
+        pa, pb = parent[a], parent[b]
+        lo, hi = torch.minimum(pa, pb), torch.maximum(pa, pb)
+        new = parent.clone()
+        new.scatter_reduce_(0, hi, lo, reduce="amin")  # hook each root under the smaller one
+        while True:  # pointer jumping to full compression
+            nxt = new[new]
+            if torch.equal(nxt, new):
+                break
+            new = nxt
+        if torch.equal(new, parent):
+            return uniq, uniq[parent]
+        parent = new
 
 
 def fof_slabs(points: torch.Tensor, eps: float, first_index: int = 0, ctx=None,
@@ -105,16 +119,30 @@ def fof_slabs(points: torch.Tensor, eps: float, first_index: int = 0, ctx=None,
     world = dist.get_world_size()
     rank = dist.get_rank()
     dev = points.device
+    import os
+    import time
+    timing = os.environ.get("SPB_SLAB_TIMING") is not None
+    t_last = [time.perf_counter()]
+
+    def tick(name):
+        if timing:
+            if dev.type == "cuda":
+                torch.cuda.synchronize(dev)
+            now = time.perf_counter()
+            print("[slabs r%d] %-10s %8.2f ms" % (rank, name, (now - t_last[0]) * 1e3), flush=True)
+            t_last[0] = now
     run_local = local_fof or _device_fof(ctx)
     n_local = points.shape[0]
     gidx = torch.arange(first_index, first_index + n_local, dtype=torch.int64, device=dev)
     x = points[:, 0]
 
-    # 1. splitters from gathered per-rank quantiles (identical on every rank)
+    # 1. splitters from gathered per-rank quantiles of a strided sample
+    #    (identical on every rank; they only balance the slabs)
     if n_local > 0:
+        stride = max(1, n_local // (1 << 20))
+        xs = torch.sort(x[::stride].double()).values
         q = torch.linspace(0, 1, samples, device=dev, dtype=torch.float64)
-        xs = torch.sort(x.double()).values
-        local_q = xs[(q * (n_local - 1)).round().long()]
+        local_q = xs[(q * (xs.numel() - 1)).round().long()]
     else:
         local_q = torch.full((samples,), float("nan"), dtype=torch.float64, device=dev)
     allq = [torch.empty_like(local_q) for _ in range(world)]
@@ -127,70 +155,97 @@ def fof_slabs(points: torch.Tensor, eps: float, first_index: int = 0, ctx=None,
         pos = (torch.arange(1, world, device=dev, dtype=torch.float64) / world * (allq.numel() - 1)).round().long()
         splitters = allq[pos].float()
 
-    # 2. partition: rank d owns x in [splitters[d-1], splitters[d])
-    dest = torch.bucketize(x, splitters, right=True)
-    order = torch.argsort(dest, stable=True)
-    send = torch.bincount(dest, minlength=world)
-    recv = _exchange_counts(send, world)
-    send = send.tolist()
-    own_pts = _all_to_all(points[order], send, recv, 3).view(-1, 3)
-    own_gidx = _all_to_all(gidx[order], send, recv)
+    tick("splitters")
 
-    # 3. ghosts: copies to every other slab within w of the point
+    # 2. partition: rank d owns x in [splitters[d-1], splitters[d]); the stable
+    #    argsort runs on 16-bit slab ids (a one/two-pass radix sort)
+    if world > 1:
+        dest = torch.bucketize(x, splitters, right=True)
+        order = torch.argsort(dest.to(torch.int16), stable=True)
+        send = torch.bincount(dest, minlength=world)
+        recv = _exchange_counts(send, world)
+        send = send.tolist()
+        own_pts = _all_to_all(points[order], send, recv, 3).view(-1, 3)
+        own_gidx = _all_to_all(gidx[order], send, recv)
+    else:
+        order, send, recv = None, [n_local], [n_local]
+        own_pts, own_gidx = points, gidx
+
+    tick("partition")
+
+    # 3. ghosts: copies to every other slab within w of the point; only points
+    #    within w of a splitter can have any
     w = float(eps) * (1.0 + 1e-6) + 1e-37
-    ox = own_pts[:, 0]
-    lo_r = torch.bucketize(ox - w, splitters, right=True)
-    hi_r = torch.bucketize(ox + w, splitters, right=True)
-    span = hi_r - lo_r + 1
-    src = torch.repeat_interleave(torch.arange(own_pts.shape[0], device=dev), span)
-    first = torch.repeat_interleave(lo_r, span)
-    offs = torch.arange(src.numel(), device=dev) - torch.repeat_interleave(torch.cumsum(span, 0) - span, span)
-    tgt = first + offs
-    keep = tgt != rank
-    src, tgt = src[keep], tgt[keep]
-    gorder = torch.argsort(tgt, stable=True)
-    src, tgt = src[gorder], tgt[gorder]
-    gsend = torch.bincount(tgt, minlength=world)
-    grecv = _exchange_counts(gsend, world)
-    gsend = gsend.tolist()
-    ghost_pts = _all_to_all(own_pts[src], gsend, grecv, 3).view(-1, 3)
-    ghost_gidx = _all_to_all(own_gidx[src], gsend, grecv)
+    m_own = own_pts.shape[0]
+    if world > 1:
+        ox = own_pts[:, 0]
+        lo_r = torch.bucketize(ox - w, splitters, right=True)
+        hi_r = torch.bucketize(ox + w, splitters, right=True)
+        near = torch.nonzero(lo_r != hi_r).squeeze(1)
+        lo_n, hi_n = lo_r[near], hi_r[near]
+        span = hi_n - lo_n + 1
+        src = torch.repeat_interleave(near, span)
+        first = torch.repeat_interleave(lo_n, span)
+        offs = torch.arange(src.numel(), device=dev) - torch.repeat_interleave(torch.cumsum(span, 0) - span, span)
+        tgt = first + offs
+        keep = tgt != rank
+        src, tgt = src[keep], tgt[keep]
+        gorder = torch.argsort(tgt.to(torch.int16), stable=True)
+        src, tgt = src[gorder], tgt[gorder]
+        gsend = torch.bincount(tgt, minlength=world)
+        grecv = _exchange_counts(gsend, world)
+        gsend = gsend.tolist()
+        ghost_pts = _all_to_all(own_pts[src], gsend, grecv, 3).view(-1, 3)
+        ghost_gidx = _all_to_all(own_gidx[src], gsend, grecv)
+        all_pts = torch.cat([own_pts, ghost_pts])
+        all_gidx = torch.cat([own_gidx, ghost_gidx])
+    else:
+        src = torch.empty(0, dtype=torch.int64, device=dev)
+        ghost_gidx = torch.empty(0, dtype=torch.int64, device=dev)
+        all_pts, all_gidx = own_pts, own_gidx
     sent_gidx = own_gidx[src]  # my points that live as ghosts elsewhere
 
-    # 4. local FoF over owned + ghosts, in global-index order
-    all_pts = torch.cat([own_pts, ghost_pts])
-    all_gidx = torch.cat([own_gidx, ghost_gidx])
-    perm = torch.argsort(all_gidx)
-    lab, core = run_local(all_pts[perm].contiguous(), eps)
-    lab = lab.to(torch.int64)
-    sorted_gidx = all_gidx[perm]
-    glab_sorted = torch.where(lab >= 0, sorted_gidx[lab.clamp(min=0)], torch.full_like(lab, -1))
-    glab = torch.empty_like(glab_sorted)
-    glab[perm] = glab_sorted
-    core_all = torch.empty_like(core)
-    core_all[perm] = core
-    m_own = own_pts.shape[0]
+    tick("ghosts")
+
+    # 4. local FoF over owned + ghosts; the cluster label becomes the minimum
+    #    GLOBAL index of its local members (a segmented min over the labels)
+    if timing and os.environ.get("SPB_SLAB_INPUT"):
+        print("[slabs r%d] local input %s %s min %s max %s eps %r" % (rank, tuple(all_pts.shape), all_pts.dtype,
+              all_pts.min(0).values.tolist(), all_pts.max(0).values.tolist(), eps), flush=True)
+    lab, core_all = run_local(all_pts.contiguous(), eps)
+    lab = lab.to(dev).to(torch.int64)
+    core_all = core_all.to(dev)
+    member = lab >= 0
+    gmin = torch.full((all_pts.shape[0],), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev)
+    gmin.scatter_reduce_(0, lab[member], all_gidx[member], reduce="amin")
+    glab = torch.where(member, gmin[lab.clamp(min=0)], torch.full_like(lab, -1))
     own_lab, own_core = glab[:m_own], core_all[:m_own]
+
+    tick("local")
 
     # 5. merge across slabs: (global index, label) of every ghost copy and of
     # the originals that were sent as ghosts
     pairs = torch.cat([torch.stack([ghost_gidx, glab[m_own:]], 1), torch.stack([sent_gidx, own_lab[src]], 1)])
     pairs = pairs[pairs[:, 1] >= 0]
-    allpairs = _all_gather_var(pairs, world).cpu().numpy()
-    uniq, final = label_components(allpairs[:, 0], allpairs[:, 1])
-    if len(uniq):
-        u = torch.from_numpy(uniq).to(dev)
-        f = torch.from_numpy(final).to(dev)
+    allpairs = _all_gather_var(pairs, world)
+    u, f = label_components(allpairs[:, 0], allpairs[:, 1])
+    if u.numel():
         idx = torch.searchsorted(u, own_lab.clamp(min=0))
-        idx = idx.clamp(max=len(uniq) - 1)
+        idx = idx.clamp(max=u.numel() - 1)
         hit = (own_lab >= 0) & (u[idx] == own_lab)
         own_lab = torch.where(hit, f[idx], own_lab)
 
+    tick("merge")
+
     # 6. labels back to the input layout
-    back_lab = _all_to_all(own_lab, recv, send)
-    back_core = _all_to_all(own_core.to(torch.int32), recv, send)
-    labels = torch.empty(n_local, dtype=torch.int64, device=dev)
-    labels[order] = back_lab
-    core_out = torch.empty(n_local, dtype=torch.int32, device=dev)
-    core_out[order] = back_core
+    if world > 1:
+        back_lab = _all_to_all(own_lab, recv, send)
+        back_core = _all_to_all(own_core.to(torch.int32), recv, send)
+        labels = torch.empty(n_local, dtype=torch.int64, device=dev)
+        labels[order] = back_lab
+        core_out = torch.empty(n_local, dtype=torch.int32, device=dev)
+        core_out[order] = back_core
+    else:
+        labels, core_out = own_lab, own_core
+    tick("return")
     return labels.to(torch.int32), core_out.to(torch.uint8)

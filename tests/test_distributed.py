@@ -74,11 +74,32 @@ def test_slab_fof_equals_single_run(oracle, tmp_path, world, kind):
 
 def test_label_components():
     from paper_2409_10743_b200.distributed import label_components
-    keys = np.array([5, 5, 7, 7, 9])
-    labs = np.array([10, 3, 3, 8, 11])
+    keys = torch.tensor([5, 5, 7, 7, 9])
+    labs = torch.tensor([10, 3, 3, 8, 11])
     u, f = label_components(keys, labs)
     m = dict(zip(u.tolist(), f.tolist()))
     assert m == {3: 3, 8: 3, 10: 3, 11: 11}
+
+
+def test_label_components_long_chains():
+    # chains of labels linked through shared keys in scrambled order: every
+    # label must map to the minimum of its chain
+    from paper_2409_10743_b200.distributed import label_components
+    g = torch.Generator().manual_seed(3)
+    labs = torch.randperm(5000, generator=g) * 7 + 11
+    chains = torch.arange(5000) % 17
+    keys, vals = [], []
+    for c in range(17):
+        members = labs[chains == c]
+        for i in range(len(members) - 1):  # link consecutive members
+            keys += [c * 100000 + i, c * 100000 + i]
+            vals += [int(members[i]), int(members[i + 1])]
+    perm = torch.randperm(len(keys), generator=g)
+    u, f = label_components(torch.tensor(keys)[perm], torch.tensor(vals)[perm])
+    m = dict(zip(u.tolist(), f.tolist()))
+    for c in range(17):
+        members = labs[chains == c]
+        assert all(m[int(x)] == int(members.min()) for x in members)
 
 
 def _gpu_worker(rank, world, port, pts, eps, out_dir):
@@ -118,3 +139,33 @@ def test_slab_fof_with_device_local_fof(oracle, tmp_path, world):
     want_l, want_c = oracle.dbscan(pts, 3, eps, 2)
     assert np.array_equal(core, want_c)
     assert np.array_equal(labels, want_l)
+
+
+def _nccl_worker(rank, world, port, n, out_dir):
+    # the production path: CUDA tensors, NCCL collectives, device FoF + device merge
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world)
+    import paper_2409_10743_b200 as sp
+    from paper_2409_10743_b200.distributed import fof_slabs
+
+    ctx = sp.Context(0)
+    pts = sp.generate_field(n, seed=2409, ctx=ctx)
+    eps = float(np.float32(0.168 * np.cbrt(1.0 / n)))
+    labels, core = fof_slabs(pts, eps, first_index=0, ctx=ctx)
+    ref = sp.friends_of_friends(pts, eps, ctx=ctx)
+    np.save(os.path.join(out_dir, "ok.npy"), np.array([bool(torch.equal(labels, ref.labels)),
+                                                       bool(torch.equal(core, ref.core_flags))]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_slab_fof_over_nccl_single_rank(tmp_path):
+    # one GPU per rank is all a round's box offers: world_size 1 over NCCL runs
+    # every collective of the slab path on CUDA tensors
+    port = _free_port()
+    mp.spawn(_nccl_worker, args=(1, port, 1 << 22, str(tmp_path)), nprocs=1, join=True)
+    assert np.load(tmp_path / "ok.npy").all()

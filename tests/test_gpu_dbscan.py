@@ -147,3 +147,22 @@ def test_adjacency_graph_dbscan_equals_fof_and_overflows(sp, oracle):
     c = dbscan_cases()["uniform3_fof"]
     out = sp.adjacency_graph_dbscan(c["points"], float(c["eps"]))
     assert np.array_equal(out.labels, c["labels"])
+
+
+def test_context_on_torch_default_stream_is_ordered(sp, oracle):
+    # stream handle 0 (torch's default stream) must mean the legacy default
+    # stream, not "a context-owned stream": the FoF has to see points that
+    # torch produces on that stream right before the call
+    import torch
+    pts = oracle.field(1 << 16)
+    eps = eps_for(1 << 16)
+    base = torch.from_numpy(pts).cuda()
+    torch.cuda.synchronize()
+    ctx = sp.Context(0, stream=torch.cuda.current_stream().cuda_stream)
+    for _ in range(3):
+        dst = torch.zeros_like(base)
+        torch.cuda._sleep(50_000_000)  # ~25 ms of spinning on the default stream
+        dst.copy_(base)
+        out = sp.friends_of_friends(dst, eps, ctx=ctx)
+        lab, core = oracle.dbscan(pts, 3, eps, 2)
+        assert np.array_equal(out.labels.cpu().numpy(), lab)
