@@ -610,68 +610,6 @@ __global__ void __launch_bounds__(128) k_fof_cells_merge(const float4 *__restric
   }
 }
 
-// The same walk, W cells per thread with their node loads issued together:
-// W independent pointer chains per thread hide the node-load latency that
-// bounds the single walk (profiles/r01: the first FADD after the two node
-// loads).  ADJ: thread t owns cells W*t .. W*t+W-1 of its block's range (the
-// walks share most nodes); otherwise cells t, t + blockDim, ...
-#ifndef SPB_MERGE_W
-#define SPB_MERGE_W 1
-#endif
-#ifndef SPB_MERGE_ADJ
-#define SPB_MERGE_ADJ 0
-#endif
-template <int W, bool ADJ>
-__global__ void __launch_bounds__(128) k_fof_cells_merge_w(const float4 *__restrict__ nodes, int64_t m,
-                                                           const int64_t *__restrict__ cell_start, int64_t n,
-                                                           const float4 *__restrict__ cpts, Radius R,
-                                                           int32_t *parent) {
-  const int64_t first_leaf = m - 1;
-  const int64_t blk = (int64_t)blockIdx.x * blockDim.x * W;
-  float4 qlo[W], qhi[W];
-  int64_t sa[W], ea[W];
-  int32_t root[W], cur[W];
-#pragma unroll
-  for (int k = 0; k < W; ++k) {
-    const int64_t a = ADJ ? blk + (int64_t)threadIdx.x * W + k : blk + threadIdx.x + (int64_t)k * blockDim.x;
-    cur[k] = kSentinel;
-    root[k] = (int32_t)a;
-    sa[k] = ea[k] = 0;
-    if (a < m) {
-      qlo[k] = ld_node(nodes, 2 * (first_leaf + a));
-      qhi[k] = ld_node(nodes, 2 * (first_leaf + a) + 1);
-      sa[k] = cell_start[a];
-      ea[k] = a + 1 < m ? cell_start[a + 1] : n;
-      cur[k] = node_rope(qhi[k]);
-    }
-  }
-  while (true) {
-    float4 lo[W], hi[W];
-    bool any = false;
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-      if (cur[k] != kSentinel) {
-        lo[k] = ld_node(nodes, 2 * (int64_t)cur[k]);
-        hi[k] = ld_node(nodes, 2 * (int64_t)cur[k] + 1);
-        any = true;
-      }
-    }
-    if (!any) break;
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-      if (cur[k] == kSentinel) continue;
-      if (cells_far(R, qlo[k], qhi[k], lo[k], hi[k])) {
-        cur[k] = node_rope(hi[k]);
-      } else if (cur[k] < first_leaf) {
-        cur[k] = node_link(lo[k]);
-      } else {
-        root[k] = cells_leaf(cell_start, m, n, cpts, R, parent, sa[k], ea[k], root[k], (int32_t)(cur[k] - first_leaf));
-        cur[k] = node_rope(hi[k]);
-      }
-    }
-  }
-}
-
 // cells: core iff the cell has two points or its set spans several cells
 __global__ void k_fof_cells_core(int64_t m, int32_t *parent, uint8_t *multi) {
   const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1033,13 +971,8 @@ bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t 
   DevBuf<int32_t> parent((size_t)m, c.stream), minobj((size_t)m, c.stream);
   k_iota32<<<grid_for(m, 256, 148 * 16), 256, 0, c.stream>>>(parent.get(), m);
   SPB_LAUNCHED();
-  if (SPB_MERGE_W == 1)
-    k_fof_cells_merge<<<(unsigned)((m + 127) / 128), 128, 0, c.stream>>>(g.t.nodes, m, g.cell_start.get(), n,
-                                                                         g.cpts.get(), make_radius(eps), parent.get());
-  else
-    k_fof_cells_merge_w<SPB_MERGE_W, SPB_MERGE_ADJ != 0>
-        <<<(unsigned)((m + 128 * SPB_MERGE_W - 1) / (128 * SPB_MERGE_W)), 128, 0, c.stream>>>(
-            g.t.nodes, m, g.cell_start.get(), n, g.cpts.get(), make_radius(eps), parent.get());
+  k_fof_cells_merge<<<(unsigned)((m + 127) / 128), 128, 0, c.stream>>>(g.t.nodes, m, g.cell_start.get(), n,
+                                                                       g.cpts.get(), make_radius(eps), parent.get());
   SPB_LAUNCHED();
   SPB_CUDA(cudaEventRecord(ev[3], c.stream));
   mark(c, "merge");
