@@ -648,7 +648,24 @@ __global__ void __launch_bounds__(256) k_fof_cells_labels(int64_t n, const int32
   const int32_t o = (int32_t)order[k];
   const bool c = multi[cl] != 0;
   labels[o] = c ? minobj[uf_root(parent, cl)] : -1;
-  core[o] = c;
+}
+
+// FoF core flags in input order: core <=> the point has a label (every member
+// of a set with >= 2 points is core, every singleton is noise), so the flags
+// are one coalesced pass over the labels instead of a 1-byte scatter.
+__global__ void __launch_bounds__(256) k_fof_core_from_labels(int64_t n, const int32_t *__restrict__ labels,
+                                                              uint8_t *__restrict__ core) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
+    if (i + 4 <= n && ((reinterpret_cast<uintptr_t>(labels + i) | reinterpret_cast<uintptr_t>(core + i)) & 3) == 0) {
+      const int4 l = *reinterpret_cast<const int4 *>(labels + i);
+      const uint32_t packed = (uint32_t)(l.x >= 0) | ((uint32_t)(l.y >= 0) << 8) | ((uint32_t)(l.z >= 0) << 16) |
+                              ((uint32_t)(l.w >= 0) << 24);
+      *reinterpret_cast<uint32_t *>(core + i) = packed;
+    } else {
+      for (int64_t j = i; j < i + 4 && j < n; ++j) core[j] = labels[j] >= 0;
+    }
+  }
 }
 
 }  // namespace
@@ -985,6 +1002,8 @@ bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t 
   k_fof_cells_labels<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(n, g.cell_of.get(), parent.get(),
                                                                         g.multi.get(), g.order, minobj.get(), labels,
                                                                         core_out);
+  SPB_LAUNCHED();
+  k_fof_core_from_labels<<<grid_for((n + 3) / 4, 256, 148 * 16), 256, 0, c.stream>>>(n, labels, core_out);
   SPB_LAUNCHED();
   SPB_CUDA(cudaEventRecord(ev[4], c.stream));
   mark(c, "finalize");
