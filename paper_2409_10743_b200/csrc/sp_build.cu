@@ -273,14 +273,6 @@ __global__ void k_rs_scan(uint32_t *ghist) {
   h[t] = off + x - v;
 }
 
-__device__ __forceinline__ void st_volatile_u64(unsigned long long *p, unsigned long long v) {
-  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long *p) {
-  unsigned long long v;
-  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 
 // THREADS threads, ITEMS keys each; threads [0, 256) own one digit each for
 // the cross-warp prefix, the look-back and the tile-local digit scan.

@@ -133,6 +133,93 @@ __global__ void k_heads(const uint64_t *__restrict__ keys, const uint32_t *__res
   }
 }
 
+// Cell segmentation of the sorted keys in one pass (replaces heads + scan +
+// starts): a stream compaction of the segment heads with a decoupled
+// look-back over 4096-key tiles.  Writes cell_start[j] = first position of
+// cell j, cell_of[i] = cell of sorted position i, and the number of cells.
+constexpr int CC_THREADS = 256, CC_ITEMS = 16, CC_TILE = CC_THREADS * CC_ITEMS;
+__global__ void __launch_bounds__(CC_THREADS) k_cell_compact(const uint64_t *__restrict__ keys, int64_t n,
+                                                              int64_t *__restrict__ cell_start,
+                                                              int32_t *__restrict__ cell_of,
+                                                              unsigned long long *lookback, uint32_t *tile_ctr,
+                                                              int64_t *total) {
+  __shared__ uint32_t s_warp[CC_THREADS / 32];
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_excl;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t wbase = tile * CC_TILE + (int64_t)warp * (CC_ITEMS * 32);
+  // striped items: item i of lane l is element wbase + i*32 + l
+  uint32_t heads[CC_ITEMS];
+  uint64_t prev_last = 0;
+  {
+    const int64_t pi = wbase - 1;
+    prev_last = pi >= 0 && pi < n ? keys[pi] : ~0ull;
+  }
+  uint32_t wcount = 0;
+#pragma unroll
+  for (int i = 0; i < CC_ITEMS; ++i) {
+    const int64_t idx = wbase + i * 32 + lane;
+    const uint64_t k = idx < n ? keys[idx] : 0ull;
+    uint64_t kp = __shfl_up_sync(0xffffffffu, k, 1);
+    if (lane == 0) kp = prev_last;
+    prev_last = __shfl_sync(0xffffffffu, k, 31);
+    const bool h = idx < n && (idx == 0 || k != kp);
+    heads[i] = __ballot_sync(0xffffffffu, h);
+    wcount += __popc(heads[i]);
+  }
+  if (lane == 0) s_warp[warp] = wcount;
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t run = 0;
+    for (int w = 0; w < CC_THREADS / 32; ++w) {
+      const uint32_t c = s_warp[w];
+      s_warp[w] = run;
+      run += c;
+    }
+    // look-back over tiles (aggregate tag 1, inclusive tag 2)
+    unsigned long long *mine = lookback + tile;
+    uint32_t excl = 0;
+    if (tile == 0) {
+      st_volatile_u64(mine, (2ull << 32) | run);
+    } else {
+      st_volatile_u64(mine, (1ull << 32) | run);
+      int64_t j = tile - 1;
+      while (true) {
+        const unsigned long long v = ld_volatile_u64(lookback + j);
+        const unsigned long long st = v >> 32;
+        if (st == 2) {
+          excl += (uint32_t)v;
+          break;
+        }
+        if (st == 1) {
+          excl += (uint32_t)v;
+          --j;
+        }
+      }
+      st_volatile_u64(mine, (2ull << 32) | (excl + run));
+    }
+    s_excl = excl;
+    if ((tile + 1) * (int64_t)CC_TILE >= n) *total = (int64_t)excl + run;
+  }
+  __syncthreads();
+  uint32_t rank = s_excl + s_warp[warp];  // heads before this warp's slice
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int i = 0; i < CC_ITEMS; ++i) {
+    const int64_t idx = wbase + i * 32 + lane;
+    const uint32_t r = rank + __popc(heads[i] & lt);  // heads before idx
+    const bool h = (heads[i] >> lane) & 1u;
+    if (idx < n) {
+      cell_of[idx] = (int32_t)(r + (h ? 1u : 0u)) - 1;
+      if (h) cell_start[r] = idx;
+    }
+    rank += __popc(heads[i]);
+  }
+}
+
 // cell_start[c] = sorted position where cell c begins (c from the head scan).
 __global__ void k_cell_starts(const int32_t *__restrict__ head, const int64_t *__restrict__ scan, int64_t n,
                               int64_t *__restrict__ cell_start) {
@@ -547,7 +634,7 @@ __global__ void k_cell_ranges(const int64_t *__restrict__ cell_start, int64_t m,
       const float4 q = cpts[k];
       lo[0] = fminf(lo[0], q.x); lo[1] = fminf(lo[1], q.y); lo[2] = fminf(lo[2], q.z);
       hi[0] = fmaxf(hi[0], q.x); hi[1] = fmaxf(hi[1], q.y); hi[2] = fmaxf(hi[2], q.z);
-      cell_of[k] = (int32_t)j;
+      if (cell_of) cell_of[k] = (int32_t)j;
     }
     for (int k = 0; k < dim; ++k) {
       boxes[j * 2 * dim + k] = lo[k];
@@ -936,29 +1023,30 @@ bool build_cell_grid(Ctx &c, const float *pts, int64_t n, int dim, float eps, Ce
   g.cpts = DevBuf<float4>((size_t)n, c.stream);
   k_cell_points<<<G, 256, 0, c.stream>>>(va, pts, n, dim, g.cpts.get());
   SPB_LAUNCHED();
-  DevBuf<int32_t> head((size_t)n, c.stream);
-  DevBuf<int64_t> hscan((size_t)n + 1, c.stream);
-  k_heads<<<G, 256, 0, c.stream>>>(ka, va, pts, dim, scene.get(), cell, n, true, head.get());
-  SPB_LAUNCHED();
-  exclusive_scan(c, head.get(), n, hscan.get());
   int64_t m = 0;
-  peek(c, {{hscan.get() + n, &m, sizeof(int64_t)}});
+  g.cell_of = DevBuf<int32_t>((size_t)n, c.stream);
+  g.cell_start = DevBuf<int64_t>((size_t)n, c.stream);  // capacity: m <= n
+  {
+    const int64_t ntiles = (n + CC_TILE - 1) / CC_TILE;
+    DevBuf<unsigned long long> lb((size_t)ntiles, c.stream);
+    DevBuf<uint32_t> ctr(1, c.stream);
+    DevBuf<int64_t> total(1, c.stream);
+    SPB_CUDA(cudaMemsetAsync(lb.get(), 0, lb.n * sizeof(unsigned long long), c.stream));
+    SPB_CUDA(cudaMemsetAsync(ctr.get(), 0, sizeof(uint32_t), c.stream));
+    k_cell_compact<<<(unsigned)ntiles, CC_THREADS, 0, c.stream>>>(ka, n, g.cell_start.get(), g.cell_of.get(), lb.get(),
+                                                                ctr.get(), total.get());
+    SPB_LAUNCHED();
+    peek(c, {{total.get(), &m, sizeof(int64_t)}});
+  }
   if (getenv("SPB_DEBUG_PEEK"))
     fprintf(stderr, "[grid] n %lld scene %g %g %g .. %g %g %g bits %d cells %lld\n", (long long)n, hs[0], hs[1], hs[2],
             hs[3], hs[4], hs[5], bits, (long long)m);
   g.m = m;
-  g.cell_start = DevBuf<int64_t>((size_t)m, c.stream);
-  k_cell_starts<<<G, 256, 0, c.stream>>>(head.get(), hscan.get(), n, g.cell_start.get());
-  SPB_LAUNCHED();
-  head.reset();
-  hscan.reset();
   DevBuf<uint64_t> ckeys((size_t)m, c.stream);
   DevBuf<float> boxes((size_t)m * 2 * dim, c.stream);
-  g.cell_of = DevBuf<int32_t>((size_t)n, c.stream);
   g.multi = DevBuf<uint8_t>((size_t)m, c.stream);
   k_cell_ranges<<<grid_for(m, 256, 148 * 16), 256, 0, c.stream>>>(g.cell_start.get(), m, n, ka, g.cpts.get(), dim,
-                                                                   ckeys.get(), boxes.get(), g.cell_of.get(),
-                                                                   g.multi.get());
+                                                                   ckeys.get(), boxes.get(), nullptr, g.multi.get());
   SPB_LAUNCHED();
   build_sorted_hierarchy(c, ckeys.get(), m, dim, boxes.get(), g.t);
   mark(c, "hierarchy");
