@@ -119,6 +119,42 @@ __global__ void __launch_bounds__(256) k_bounds(const float *__restrict__ obj, i
   if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) *bad = 1;
 }
 
+// 3-D points, 16-byte aligned: four points per thread step (vector loads).
+__global__ void __launch_bounds__(256) k_bounds_p3v(const float *__restrict__ pts, int64_t n,
+                                                    int32_t *__restrict__ ord6, int *__restrict__ bad) {
+  int32_t mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {INT_MIN, INT_MIN, INT_MIN};
+  bool ok = true;
+  const int64_t chunks = n / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  auto take = [&](float x, float y, float z) {
+    ok = ok && isfinite(x) && isfinite(y) && isfinite(z);
+    mn[0] = min(mn[0], ord_of(x)); mx[0] = max(mx[0], ord_of(x));
+    mn[1] = min(mn[1], ord_of(y)); mx[1] = max(mx[1], ord_of(y));
+    mn[2] = min(mn[2], ord_of(z)); mx[2] = max(mx[2], ord_of(z));
+  };
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t ch = t0; ch < chunks; ch += stride) {
+    float x[4], y[4], z[4];
+    load4pts(pts, ch, x, y, z);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) take(x[j], y[j], z[j]);
+  }
+  for (int64_t i = chunks * 4 + t0; i < n; i += stride) take(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    mn[k] = __reduce_min_sync(0xffffffffu, mn[k]);
+    mx[k] = __reduce_max_sync(0xffffffffu, mx[k]);
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      atomicMin(&ord6[k], mn[k]);
+      atomicMax(&ord6[3 + k], mx[k]);
+    }
+  }
+  if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) *bad = 1;
+}
+
 // ord6 -> float scene[6]; axes beyond dim are 0 (2-D data lives at z = 0).
 __global__ void k_bounds_final(const int32_t *ord6, int dim, int64_t n, float *scene) {
   int t = threadIdx.x;
@@ -138,7 +174,9 @@ void scene_bounds(Ctx &c, const float *objects, int64_t n, int dim, bool points,
   SPB_LAUNCHED();
   if (n > 0) {
     unsigned g = grid_for(n, 256, 148 * 8);
-    if (points) k_bounds<true><<<g, 256, 0, c.stream>>>(objects, n, dim, ord.get(), bad);
+    if (points && dim == 3 && aligned16(objects))
+      k_bounds_p3v<<<grid_for((n + 3) / 4, 256, 148 * 8), 256, 0, c.stream>>>(objects, n, ord.get(), bad);
+    else if (points) k_bounds<true><<<g, 256, 0, c.stream>>>(objects, n, dim, ord.get(), bad);
     else k_bounds<false><<<g, 256, 0, c.stream>>>(objects, n, dim, ord.get(), bad);
     SPB_LAUNCHED();
   }
@@ -212,11 +250,43 @@ __global__ void __launch_bounds__(256) k_morton(const float *__restrict__ obj, i
   }
 }
 
+// 3-D points, 16-byte aligned: four codes per thread step (vector loads).
+__global__ void __launch_bounds__(256) k_morton_p3v(const float *__restrict__ pts, int64_t n, int width,
+                                                    const float *__restrict__ scene, uint64_t *__restrict__ codes,
+                                                    uint32_t *__restrict__ vals) {
+  const int bits = width / 3;
+  const uint32_t top = bits >= 32 ? 0xffffffffu : ((1u << bits) - 1u);
+  const double scale = (double)(1ull << bits);
+  const float lo0 = scene[0], lo1 = scene[1], lo2 = scene[2], hi0 = scene[3], hi1 = scene[4], hi2 = scene[5];
+  auto code = [&](float x, float y, float z) -> uint64_t {
+    return encode_bins(axis_bin(x, lo0, hi0, scale, top), axis_bin(y, lo1, hi1, scale, top),
+                       axis_bin(z, lo2, hi2, scale, top), 3);
+  };
+  const int64_t chunks = n / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t ch = t0; ch < chunks; ch += stride) {
+    float x[4], y[4], z[4];
+    load4pts(pts, ch, x, y, z);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      codes[4 * ch + j] = code(x[j], y[j], z[j]);
+      if (vals) vals[4 * ch + j] = (uint32_t)(4 * ch + j);
+    }
+  }
+  for (int64_t i = chunks * 4 + t0; i < n; i += stride) {
+    codes[i] = code(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+    if (vals) vals[i] = (uint32_t)i;
+  }
+}
+
 void morton_codes(Ctx &c, const float *objects, int64_t n, int dim, bool points, int width, const float *scene,
                   uint64_t *codes, uint32_t *vals) {
   if (n <= 0) return;
   unsigned g = grid_for(n, 256, 148 * 16);
-  if (points) k_morton<true><<<g, 256, 0, c.stream>>>(objects, n, dim, width, scene, codes, vals);
+  if (points && dim == 3 && aligned16(objects))
+    k_morton_p3v<<<grid_for((n + 3) / 4, 256, 148 * 16), 256, 0, c.stream>>>(objects, n, width, scene, codes, vals);
+  else if (points) k_morton<true><<<g, 256, 0, c.stream>>>(objects, n, dim, width, scene, codes, vals);
   else k_morton<false><<<g, 256, 0, c.stream>>>(objects, n, dim, width, scene, codes, vals);
   SPB_LAUNCHED();
 }

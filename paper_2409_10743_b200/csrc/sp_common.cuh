@@ -172,6 +172,21 @@ __host__ __device__ __forceinline__ float float_of_ord(int32_t i) {
 
 __device__ __forceinline__ float4 ld_node(const float4 *nodes, int64_t i) { return __ldg(nodes + i); }
 
+// Four consecutive 3-D points (12 floats) as three 16-byte loads; the array
+// must be 16-byte aligned.
+__device__ __forceinline__ void load4pts(const float *__restrict__ pts, int64_t chunk, float x[4], float y[4],
+                                         float z[4]) {
+  const float4 *v = reinterpret_cast<const float4 *>(pts) + 3 * chunk;
+  const float4 a = __ldg(v), b = __ldg(v + 1), d = __ldg(v + 2);
+  x[0] = a.x; y[0] = a.y; z[0] = a.z;
+  x[1] = a.w; y[1] = b.x; z[1] = b.y;
+  x[2] = b.z; y[2] = b.w; z[2] = d.x;
+  x[3] = d.y; y[3] = d.z; z[3] = d.w;
+}
+__host__ __device__ __forceinline__ bool aligned16(const void *p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+}
+
 // Decoupled look-back status words (bypass L1: other CTAs publish them).
 __device__ __forceinline__ void st_volatile_u64(unsigned long long *p, unsigned long long v) {
   asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");

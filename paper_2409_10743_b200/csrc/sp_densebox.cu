@@ -104,6 +104,32 @@ __global__ void k_cell_keys(const float *__restrict__ pts, int64_t n, int dim, c
   }
 }
 
+// 3-D points, 16-byte aligned: Morton cell keys, four points per step.
+__global__ void __launch_bounds__(256) k_cell_keys_p3v(const float *__restrict__ pts, int64_t n,
+                                                       const float *__restrict__ scene, float cell,
+                                                       uint64_t *__restrict__ keys) {
+  const float a0 = scene[0], a1 = scene[1], a2 = scene[2];
+  const int64_t chunks = n / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  auto key = [&](float x, float y, float z) -> uint64_t {
+    return spread3_21((uint64_t)cell_coord(x, a0, cell)) | (spread3_21((uint64_t)cell_coord(y, a1, cell)) << 1) |
+           (spread3_21((uint64_t)cell_coord(z, a2, cell)) << 2);
+  };
+  for (int64_t ch = t0; ch < chunks; ch += stride) {
+    float x[4], y[4], z[4];
+    load4pts(pts, ch, x, y, z);
+    ulonglong2 k01, k23;
+    k01.x = key(x[0], y[0], z[0]);
+    k01.y = key(x[1], y[1], z[1]);
+    k23.x = key(x[2], y[2], z[2]);
+    k23.y = key(x[3], y[3], z[3]);
+    reinterpret_cast<ulonglong2 *>(keys)[2 * ch] = k01;
+    reinterpret_cast<ulonglong2 *>(keys)[2 * ch + 1] = k23;
+  }
+  for (int64_t i = chunks * 4 + t0; i < n; i += stride) keys[i] = key(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+}
+
 __global__ void k_gather_keys(const float *__restrict__ pts, int64_t n, int dim, const float *__restrict__ scene,
                               float cell, int axis, const uint32_t *__restrict__ order, uint64_t *__restrict__ keys) {
   const float a = scene[axis];
@@ -1011,7 +1037,11 @@ bool build_cell_grid(Ctx &c, const float *pts, int64_t n, int dim, float eps, Ce
   g.k1 = DevBuf<uint64_t>((size_t)n, c.stream);
   g.v0 = DevBuf<uint32_t>((size_t)n, c.stream);
   g.v1 = DevBuf<uint32_t>((size_t)n, c.stream);
-  k_cell_keys<<<G, 256, 0, c.stream>>>(pts, n, dim, scene.get(), cell, -1, g.k0.get());
+  if (dim == 3 && aligned16(pts) && aligned16(g.k0.get()))
+    k_cell_keys_p3v<<<grid_for((n + 3) / 4, 256, 148 * 16), 256, 0, c.stream>>>(pts, n, scene.get(), cell,
+                                                                                 g.k0.get());
+  else
+    k_cell_keys<<<G, 256, 0, c.stream>>>(pts, n, dim, scene.get(), cell, -1, g.k0.get());
   SPB_LAUNCHED();
   mark(c, "morton");
   uint64_t *ka = g.k0.get(), *kb = g.k1.get();

@@ -136,3 +136,21 @@ def test_c1_leaf_perm_and_node_arrays(sp, oracle):
     leaves[:, 1] = e["leaf_rope"].view(np.float32)
     leaves[:, 2:] = e["leaf_boxes"]
     assert fnv1a64(np.concatenate([ints.reshape(-1), leaves.reshape(-1)])) == g["node_arrays"]
+
+
+def test_unaligned_device_points_take_the_scalar_path(sp):
+    # the 3-D point kernels load four points as three float4 when the array is
+    # 16-byte aligned; a view starting one point in is not, and must agree
+    import torch
+    rng = np.random.default_rng(41)
+    base = torch.from_numpy(rng.random((40001, 3), dtype=np.float32)).cuda()
+    view = base[1:]  # 12-byte offset
+    dense = view.clone()  # aligned copy of the same points
+    a = sp.Bvh.build(view).export()
+    b = sp.Bvh.build(dense).export()
+    for k in a:
+        assert np.array_equal(np.asarray(a[k]).view(np.uint8), np.asarray(b[k]).view(np.uint8)), k
+    eps = 0.01
+    fa = sp.friends_of_friends(view, eps)
+    fb = sp.friends_of_friends(dense, eps)
+    assert torch.equal(fa.labels, fb.labels) and torch.equal(fa.core_flags, fb.core_flags)
