@@ -387,6 +387,8 @@ CONFIGS = {
                     "centred on them, r = cbrt(30/(n*4pi/3)) (~30.7 neighbours)"),
     "c3": (1 << 26, "C3: fdbscan_densebox min_pts = 5 on the 2^26-point clustered field, eps = 0.168*n^(-1/3)"),
     "c4": (1 << 24, "C4: Bvh::build + nearest_query k = 16, 2^24 uniform points, 2^24 uniform queries"),
+    "c5": (1 << 30, "C5 on ONE GPU: friends_of_friends on the 2^30-point (1.07 B) HACC-like clustered field, "
+                    "eps = 0.168*n^(-1/3)"),
 }
 
 
@@ -417,8 +419,13 @@ def run_config(args):
         times.setdefault(name, []).append((a, b))
         return out
 
-    if w == "c1":
-        step = lambda: timed("fof", lambda: sp.friends_of_friends(pts, eps, ctx=ctx))
+    if w in ("c1", "c5"):
+        if w == "c5":  # outputs preallocated: 5.4 GB per call
+            lab_d = torch.empty(n, dtype=torch.int32, device=dev)
+            core_d = torch.empty(n, dtype=torch.uint8, device=dev)
+            step = lambda: timed("fof", lambda: sp.friends_of_friends(pts, eps, ctx=ctx, out=(lab_d, core_d)))
+        else:
+            step = lambda: timed("fof", lambda: sp.friends_of_friends(pts, eps, ctx=ctx))
         unit, per_step = "points/s", n
     elif w == "c3":
         step = lambda: timed("densebox", lambda: sp.fdbscan_densebox(pts, sp.DbscanParams(eps, 5), ctx=ctx))
@@ -461,7 +468,7 @@ def run_config(args):
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        if w == "c1":
+        if w in ("c1", "c5"):
             sp.friends_of_friends(host_pts, eps, ctx=ctx)
         elif w == "c3":
             sp.fdbscan_densebox(host_pts, sp.DbscanParams(eps, 5), ctx=ctx)
@@ -472,7 +479,7 @@ def run_config(args):
     torch.cuda.synchronize(dev)
     e2e = per_step * args.steps / (time.perf_counter() - t0)
     h2d = n * 12 * (2 if w == "c4" else 1)
-    d2h = {"c1": n * 5, "c3": n * 5, "c2": n * 4, "c4": n * 16 * 4}[w]
+    d2h = {"c1": n * 5, "c3": n * 5, "c5": n * 5, "c2": n * 4, "c4": n * 16 * 4}[w]
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -480,7 +487,11 @@ def run_config(args):
         from oracle_lib import Reference  # the reference CPU path (baseline only)
         if Reference.available():
             R = Reference.get()
-            if w == "c1":
+            if w == "c5":
+                sample = 1 << 22
+                p = R.field(sample)
+                t = time.perf_counter(); R.dbscan(p, 3, eps_for(sample), 2, "fof"); dt = time.perf_counter() - t
+            elif w == "c1":
                 sample = 1000000
                 p = R.uniform(sample, 3, 1.0, 2409)
                 t = time.perf_counter(); R.dbscan(p, 3, eps_for(sample), 2, "fof"); dt = time.perf_counter() - t
@@ -501,7 +512,7 @@ def run_config(args):
             cpu = {"value": sample / dt, "unit": unit, "cores": os.cpu_count(), "kind": "reference",
                    "sample": "%s at n = %d (reference generator), one run, %.2f s" % (w, sample, dt)}
     line = {
-        "metric": {"c1": METRIC, "c3": "FDBSCAN-DenseBox points/sec (min_pts=5)",
+        "metric": {"c1": METRIC, "c5": METRIC, "c3": "FDBSCAN-DenseBox points/sec (min_pts=5)",
                    "c2": "BVH build + range-count queries/sec", "c4": "BVH build + kNN (k=16) queries/sec"}[w],
         "value": per_step * args.steps / (ms / 1e3), "unit": unit, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
