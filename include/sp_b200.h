@@ -175,6 +175,13 @@ int sp_morton_codes(sp_ctx *ctx, const float *objects, int64_t n, int dim, int i
 int sp_dbscan(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, int32_t min_pts, int algo,
               int code_width, int32_t *labels, uint8_t *core, sp_timings *timings, sp_stats *stats, int mem);
 
+/* friends_of_friends with caller-supplied point ids (device or host per
+ * `mem`, n entries, distinct, >= 0): labels[i] = the smallest id of i's
+ * cluster (-1 = noise) instead of the smallest index — the building block of
+ * the multi-GPU slab FoF, which passes global indices (distributed.py). */
+int sp_fof_ids(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, const int32_t *ids,
+               int32_t *labels, uint8_t *core, int mem);
+
 /* adjacency_graph_dbscan (dbscan.hpp:456-504): the legacy min_pts = 2
  * baseline that materialises the eps-neighbourhood CRS; SP_ECAPACITY when
  * the total exceeds max_adjacency (its CapacityError). */

@@ -99,6 +99,7 @@ def _load() -> C.CDLL:
         "sp_morton_codes": (C.c_int, [vp, vp, i64, C.c_int, C.c_int, C.c_int, vp, C.c_int]),
         "sp_dbscan": (C.c_int, [vp, vp, i64, C.c_int, f32, i32, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int]),
         "sp_dbscan_bruteforce": (C.c_int, [vp, vp, i64, C.c_int, f32, i32, vp, vp, C.c_int]),
+        "sp_fof_ids": (C.c_int, [vp, vp, i64, C.c_int, f32, vp, vp, vp, C.c_int]),
         "sp_generate_reference": (C.c_int, [C.c_int, i64, C.c_int, i32, C.c_double, C.c_double, C.c_uint64, vp]),
         "sp_dbscan_adjacency": (C.c_int, [vp, vp, i64, C.c_int, f32, C.c_int, i64, vp, vp, vp, C.c_int]),
         "sp_check_equivalence": (C.c_int, [vp, vp, i64, C.c_int, f32, vp, vp, vp, vp, C.POINTER(i64),
@@ -541,6 +542,29 @@ def fdbscan(points, params: DbscanParams, width: int = 64, ctx: Optional[Context
 def friends_of_friends(points, eps: float, width: int = 64, ctx: Optional[Context] = None, out=None) -> DbscanOutput:
     """friends_of_friends (dbscan.hpp:286-292): FDBSCAN with min_pts = 2."""
     return _dbscan(points, eps, 2, SP_ALGO_FOF, width, ctx, out)
+
+
+def friends_of_friends_ids(points, eps: float, ids, ctx: Optional[Context] = None, out=None):
+    """friends_of_friends whose labels are the smallest ids[i] of each
+    cluster (-1 = noise) instead of the smallest index: the per-slab step of the
+    multi-GPU FoF, which passes global indices (sp_fof_ids).  ids: int32, one
+    per point, distinct, >= 0, in the same memory space as the points."""
+    ctx = ctx or default_context()
+    dim = _dim_of(points)
+    n = int(points.shape[0])
+    p, mem, keep = _in(points, np.float32)
+    dev = mem == SP_MEM_DEVICE
+    if _is_cuda(ids) != dev:
+        raise ValueError("ids must live in the same memory space as the points")
+    ip, _, keep_ids = _in(ids, np.int32)
+    if out is not None:
+        labels, core = out
+        lp, cp = _ptr(labels), _ptr(core)
+    else:
+        labels, lp = _out(dev, (n,), np.int32, _torch_dtype("int32") if dev else None, points.device if dev else None)
+        core, cp = _out(dev, (n,), np.uint8, _torch_dtype("uint8") if dev else None, points.device if dev else None)
+    ctx._check(_lib.sp_fof_ids(ctx.h, p, n, dim, C.c_float(eps), ip, lp, cp, mem))
+    return DbscanOutput(labels, core)
 
 
 def fdbscan_densebox(points, params: DbscanParams, width: int = 64, ctx: Optional[Context] = None,

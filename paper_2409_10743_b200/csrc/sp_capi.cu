@@ -609,6 +609,22 @@ int sp_dbscan(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, i
   });
 }
 
+int sp_fof_ids(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, const int32_t *ids,
+               int32_t *labels, uint8_t *core, int mem) {
+  return guarded(ctx, [&](spb::Ctx &c) {
+    check_dim(dim);
+    if (n < 0 || n > (1LL << 30)) throw spb::InvalidArgument("point count out of range");
+    In<float> p(c, points, (size_t)n * dim, mem);
+    In<int32_t> id(c, ids, (size_t)n, mem);
+    Out<int32_t> ol(c, labels, (size_t)n, mem);
+    Out<uint8_t> oc(c, core, (size_t)n, mem);
+    if (n) spb::dbscan(c, p.p, n, dim, eps, 2, 1, 64, ol.p, oc.p, nullptr, id.p);
+    ol.flush(c);
+    oc.flush(c);
+    finish(c);
+  });
+}
+
 int sp_dbscan_adjacency(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, int code_width,
                         int64_t max_adjacency, int32_t *labels, uint8_t *core, sp_timings *timings, int mem) {
   return guarded(ctx, [&](spb::Ctx &c) {

@@ -121,13 +121,14 @@ __device__ __forceinline__ bool is_member(const uint8_t *corep, const uint32_t *
 // usually share a root).
 __global__ void __launch_bounds__(256) k_final_roots(int64_t n, int32_t *parent, const uint8_t *__restrict__ corep,
                                                      const uint32_t *__restrict__ claims,
-                                                     const int32_t *__restrict__ perm, int32_t *minobj) {
+                                                     const int32_t *__restrict__ perm,
+                                                     const int32_t *__restrict__ ids, int32_t *minobj) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int32_t key = -1, v = 0x7fffffff;
   if (p < n && is_member(corep, claims, p)) {
     key = uf_root(parent, (int32_t)p);
     parent[p] = key;
-    v = perm[p];
+    v = ids ? ids[perm[p]] : perm[p];
   }
   const uint32_t peers = __match_any_sync(0xffffffffu, key);
   const int32_t m = (int32_t)__reduce_min_sync(peers, (uint32_t)v);
@@ -151,15 +152,16 @@ __global__ void __launch_bounds__(256) k_final_labels(int64_t n, const int32_t *
 }
 
 void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t min_pts, int algo, int width,
-            int32_t *labels, uint8_t *core, DbscanResult *res) {
+            int32_t *labels, uint8_t *core, DbscanResult *res, const int32_t *ids) {
   if (!(eps > 0.f) || !std::isfinite(eps)) throw InvalidArgument("dbscan: eps must be positive and finite");
   if (algo == 1) min_pts = 2;
   if (min_pts < 2) throw InvalidArgument("dbscan: min_pts must be at least 2");
   if (n == 0) return;
   if (min_pts == 2 && !getenv("SPB_FOF_POINTS")) {
     // friends-of-friends over grid cells (the DenseBox shortcut)
-    extern bool fof_cells(Ctx &, const float *, int64_t, int, float, int32_t *, uint8_t *, DbscanResult *);
-    if (algo != 2 && fof_cells(c, points, n, dim, eps, labels, core, res)) return;
+    extern bool fof_cells(Ctx &, const float *, int64_t, int, float, int32_t *, uint8_t *, DbscanResult *,
+                          const int32_t *);
+    if (algo != 2 && fof_cells(c, points, n, dim, eps, labels, core, res, ids)) return;
   }
   if (algo == 2) {
     extern void densebox(Ctx &, const float *, int64_t, int, float, int32_t, int, int32_t *, uint8_t *,
@@ -214,7 +216,7 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
     SPB_LAUNCHED();
   }
   SPB_CUDA(cudaMemsetAsync(minobj.get(), 0x7f, (size_t)n * sizeof(int32_t), c.stream));
-  k_final_roots<<<g256, 256, 0, c.stream>>>(n, parent.get(), corep.get(), claims.get(), t.perm, minobj.get());
+  k_final_roots<<<g256, 256, 0, c.stream>>>(n, parent.get(), corep.get(), claims.get(), t.perm, ids, minobj.get());
   SPB_LAUNCHED();
   k_final_labels<<<g256, 256, 0, c.stream>>>(n, parent.get(), corep.get(), claims.get(), t.perm, minobj.get(), labels,
                                              core);

@@ -737,12 +737,13 @@ __global__ void k_fof_cells_core(int64_t m, int32_t *parent, uint8_t *multi) {
 
 __global__ void __launch_bounds__(256) k_fof_cells_minobj(int64_t n, const int32_t *__restrict__ cell_of,
                                                           const int32_t *__restrict__ parent,
-                                                          const uint32_t *__restrict__ order, int32_t *minobj) {
+                                                          const uint32_t *__restrict__ order,
+                                                          const int32_t *__restrict__ ids, int32_t *minobj) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int32_t key = -1, v = 0x7fffffff;
   if (k < n) {
     key = uf_root(parent, cell_of[k]);
-    v = (int32_t)order[k];
+    v = ids ? ids[order[k]] : (int32_t)order[k];
   }
   const uint32_t peers = __match_any_sync(0xffffffffu, key);
   const int32_t mn = (int32_t)__reduce_min_sync(peers, (uint32_t)v);
@@ -1086,7 +1087,7 @@ bool build_cell_grid(Ctx &c, const float *pts, int64_t n, int dim, float eps, Ce
 // friends-of-friends over the cell grid: a cell is one set from the start,
 // cells unite at their first member pair within eps (k_fof_cells_merge).
 bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t *labels, uint8_t *core_out,
-               DbscanResult *res) {
+               DbscanResult *res, const int32_t *ids) {
   cudaEvent_t ev[5];
   for (auto &e : ev) SPB_CUDA(cudaEventCreate(&e));
   struct EvGuard {
@@ -1115,7 +1116,7 @@ bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t 
   SPB_LAUNCHED();
   SPB_CUDA(cudaMemsetAsync(minobj.get(), 0x7f, (size_t)m * sizeof(int32_t), c.stream));
   k_fof_cells_minobj<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(n, g.cell_of.get(), parent.get(), g.order,
-                                                                        minobj.get());
+                                                                        ids, minobj.get());
   SPB_LAUNCHED();
   k_fof_cells_labels<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(n, g.cell_of.get(), parent.get(),
                                                                         g.multi.get(), g.order, minobj.get(), labels,

@@ -31,8 +31,11 @@ struct DbscanResult {
   int64_t distance_checks = 0, num_dense_cells = 0, num_dense_points = 0;
 };
 // labels/core: device arrays of n entries (original point order).
+// ids (optional, device, n entries): FoF labels become the smallest ids[i] of
+// each cluster instead of the smallest index (the distributed FoF passes
+// global indices).
 void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t min_pts, int algo, int width,
-            int32_t *labels, uint8_t *core, DbscanResult *res);
+            int32_t *labels, uint8_t *core, DbscanResult *res, const int32_t *ids = nullptr);
 
 void adjacency_dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int width, int64_t max_adjacency,
                       int32_t *labels, uint8_t *core, DbscanResult *res);

@@ -64,16 +64,19 @@ def _all_gather_var(t: torch.Tensor, world: int) -> torch.Tensor:
 
 
 def _device_fof(ctx):
+    """The device FoF with global ids: labels come back as the smallest global
+    index of each local cluster directly (sp_fof_ids)."""
     import paper_2409_10743_b200 as sp
 
-    def run(points: torch.Tensor, eps: float):
+    def run(points: torch.Tensor, eps: float, gids: torch.Tensor):
         # the torch ops that produced `points` ran on torch's current stream;
         # a context on another stream must not start before they finish
         if ctx is not None and points.is_cuda:
             torch.cuda.current_stream(points.device).synchronize()
-        out = sp.friends_of_friends(points, eps, ctx=ctx)
+        out = sp.friends_of_friends_ids(points, eps, gids.to(torch.int32).contiguous(), ctx=ctx)
         return out.labels, out.core_flags
 
+    run.global_ids = True
     return run
 
 
@@ -212,13 +215,17 @@ def fof_slabs(points: torch.Tensor, eps: float, first_index: int = 0, ctx=None,
     if timing and os.environ.get("SPB_SLAB_INPUT"):
         print("[slabs r%d] local input %s %s min %s max %s eps %r" % (rank, tuple(all_pts.shape), all_pts.dtype,
               all_pts.min(0).values.tolist(), all_pts.max(0).values.tolist(), eps), flush=True)
-    lab, core_all = run_local(all_pts.contiguous(), eps)
-    lab = lab.to(dev).to(torch.int64)
+    if getattr(run_local, "global_ids", False):
+        lab, core_all = run_local(all_pts.contiguous(), eps, all_gidx)
+        glab = lab.to(torch.int64)
+    else:
+        lab, core_all = run_local(all_pts.contiguous(), eps)
+        lab = lab.to(dev).to(torch.int64)
+        member = lab >= 0
+        gmin = torch.full((all_pts.shape[0],), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev)
+        gmin.scatter_reduce_(0, lab[member], all_gidx[member], reduce="amin")
+        glab = torch.where(member, gmin[lab.clamp(min=0)], torch.full_like(lab, -1))
     core_all = core_all.to(dev)
-    member = lab >= 0
-    gmin = torch.full((all_pts.shape[0],), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev)
-    gmin.scatter_reduce_(0, lab[member], all_gidx[member], reduce="amin")
-    glab = torch.where(member, gmin[lab.clamp(min=0)], torch.full_like(lab, -1))
     own_lab, own_core = glab[:m_own], core_all[:m_own]
 
     tick("local")

@@ -166,3 +166,27 @@ def test_context_on_torch_default_stream_is_ordered(sp, oracle):
         out = sp.friends_of_friends(dst, eps, ctx=ctx)
         lab, core = oracle.dbscan(pts, 3, eps, 2)
         assert np.array_equal(out.labels.cpu().numpy(), lab)
+
+
+def test_fof_ids_labels_are_min_id_per_cluster(sp, oracle):
+    # sp_fof_ids: the same clusters, labelled by the smallest caller id
+    import torch
+    pts = oracle.field(1 << 16)
+    eps = eps_for(1 << 16)
+    lab, core = oracle.dbscan(pts, 3, eps, 2)
+    rng = np.random.default_rng(5)
+    ids = (rng.permutation(len(pts)) * 3 + 7).astype(np.int32)
+    want = np.full(len(pts), -1, np.int64)
+    members = lab >= 0
+    mins = {}
+    for i in np.nonzero(members)[0]:
+        mins[lab[i]] = min(mins.get(lab[i], 1 << 40), ids[i])
+    want[members] = [mins[l] for l in lab[members]]
+    for mem in ("device", "host"):
+        p = torch.from_numpy(pts).cuda() if mem == "device" else pts
+        i = torch.from_numpy(ids).cuda() if mem == "device" else ids
+        out = sp.friends_of_friends_ids(p, eps, i)
+        got = out.labels.cpu().numpy() if mem == "device" else out.labels
+        gc = out.core_flags.cpu().numpy() if mem == "device" else out.core_flags
+        assert np.array_equal(got, want.astype(np.int32)), mem
+        assert np.array_equal(gc, core), mem
