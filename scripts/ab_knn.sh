@@ -1,1 +1,1 @@
-for m in new legacy new legacy; do echo "== $m"; if [ $m = legacy ]; then export SPB_KNN_LEGACY=1; else unset SPB_KNN_LEGACY; fi; timeout 120 python scripts/c4_probe.py 2>&1 | tail -1; done
+for f in 1.3 1.5 2.0; do echo "== R factor $f"; SPB_KNN_RFACTOR=$f timeout 120 python scripts/c4_probe.py 2>&1 | tail -2; done
