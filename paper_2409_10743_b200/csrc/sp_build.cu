@@ -412,11 +412,14 @@ __global__ void __launch_bounds__(THREADS, (THREADS * ITEMS <= 2048) ? 4 : SPB_R
       peers &= on ? bal : ~bal;
     }
     // the lowest lane of each digit group advances the warp's counter; the
-    // warp's shared-memory accesses are performed in program order and the
-    // full-mask ballots re-converge the warp every round
+    // __syncwarp()s order the lanes' reads before the update and the update
+    // before the next round's reads (memory-model clean: racecheck reports no
+    // hazard; dropping them saved < 1% and relies on in-order warp execution)
     const uint32_t r = __popc(peers & lt);
     const uint32_t b = wh[d];
+    __syncwarp();
     if (r == 0) wh[d] = b + __popc(peers);
+    __syncwarp();
     rk[i] = (uint16_t)(b + r);
   }
   __syncthreads();
