@@ -190,3 +190,32 @@ def test_fof_ids_labels_are_min_id_per_cluster(sp, oracle):
         gc = out.core_flags.cpu().numpy() if mem == "device" else out.core_flags
         assert np.array_equal(got, want.astype(np.int32)), mem
         assert np.array_equal(gc, core), mem
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_fof_cells_boundary_and_degenerate_inputs(sp, oracle, dim):
+    # The cell pipeline's shortcuts (a cell is one set; only cells <= 2 apart
+    # can touch) must reproduce the exact predicate at the boundary: pairs at
+    # float distance exactly eps and one ulp beyond, axis-aligned and
+    # diagonal, on a lattice of spacing eps; identical points; negative and
+    # large-magnitude coordinates.
+    rng = np.random.default_rng(11 + dim)
+    eps = np.float32(0.01)
+    cases = []
+    g = np.arange(12, dtype=np.float32) * eps  # spacing exactly eps
+    grid = np.stack(np.meshgrid(*([g] * dim), indexing="ij"), -1).reshape(-1, dim)
+    cases.append(grid)
+    cases.append(grid * np.float32(1.0000001))  # just beyond eps
+    diag = np.float32(eps / np.sqrt(dim))
+    line = (np.arange(200, dtype=np.float32)[:, None] * diag) * np.ones((1, dim), np.float32)
+    cases.append(line)
+    same = np.tile(rng.random((1, dim), dtype=np.float32), (500, 1))
+    cases.append(np.concatenate([same, rng.random((300, dim), dtype=np.float32)]))
+    cases.append((rng.random((5000, dim), dtype=np.float32) - 0.5) * 0.3 - 7.0)  # negative coordinates
+    cases.append(rng.random((5000, dim), dtype=np.float32) * 0.2 + 1000.0)  # large magnitude, coarse ulps
+    for t, pts in enumerate(cases):
+        pts = np.ascontiguousarray(pts, np.float32)
+        out = sp.friends_of_friends(pts, float(eps))
+        lab, core = oracle.dbscan(pts, dim, float(eps), 2)
+        assert np.array_equal(out.labels, lab), (dim, t)
+        assert np.array_equal(out.core_flags, core), (dim, t)
