@@ -34,6 +34,10 @@
 
 namespace spb {
 
+#ifndef SPB_CORE_WINDOW
+#define SPB_CORE_WINDOW 4
+#endif
+
 namespace {
 
 // Host synchronisation point; SPB_DEBUG_SYNC=1 logs the host time spent before
@@ -1193,9 +1197,24 @@ __global__ void __launch_bounds__(128) k_cells_core(const float4 *__restrict__ n
   if (k >= n) return;
   const int32_t own = cell_of[k];
   int32_t cnt = (int32_t)(cell_end(cell_start, m, n, own) - cell_start[own]);
+  const float4 me = cpts[k];
+  const int64_t first_leaf = m - 1;
+  // Morton-neighbour cells first (key order is spatial order): in dense
+  // regions they usually hold the missing neighbours and the tree walk is
+  // skipped; the walk below does not count them again.
+  const int64_t w_lo = own - SPB_CORE_WINDOW > 0 ? own - SPB_CORE_WINDOW : 0;
+  const int64_t w_hi = own + SPB_CORE_WINDOW < m - 1 ? own + SPB_CORE_WINDOW : m - 1;
+  for (int64_t b = w_lo; b <= w_hi && cnt < min_pts; ++b) {
+    if (b == own) continue;
+    const float4 lo = ld_node(nodes, 2 * (first_leaf + b)), hi = ld_node(nodes, 2 * (first_leaf + b) + 1);
+    if (!hit_box(R, me.x, me.y, me.z, lo, hi)) continue;
+    const int64_t e = cell_end(cell_start, m, n, b);
+    for (int64_t j = cell_start[b]; j < e && cnt < min_pts; ++j) {
+      const float4 q = cpts[j];
+      cnt += hit_point(R, me.x, me.y, me.z, q.x, q.y, q.z);
+    }
+  }
   if (cnt < min_pts) {
-    const float4 me = cpts[k];
-    const int64_t first_leaf = m - 1;
     int32_t cur = 0;  // root: internal 0, or leaf 0 when m == 1
     while (cur != kSentinel) {
       const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
@@ -1205,7 +1224,7 @@ __global__ void __launch_bounds__(128) k_cells_core(const float4 *__restrict__ n
       }
       const int64_t b = cur - first_leaf;
       cur = node_rope(hi);
-      if (b == own || !hit_box(R, me.x, me.y, me.z, lo, hi)) continue;
+      if ((b >= w_lo && b <= w_hi) || !hit_box(R, me.x, me.y, me.z, lo, hi)) continue;
       const int64_t e = cell_end(cell_start, m, n, b);
       for (int64_t j = cell_start[b]; j < e && cnt < min_pts; ++j) {
         const float4 q = cpts[j];
