@@ -36,7 +36,32 @@ __global__ void __launch_bounds__(128) k_core_flags(const float4 *__restrict__ n
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const float4 me = ld_node(leafpt, p);
-  corep[p] = count_sphere(nodes, leafpt, n, me.x, me.y, me.z, R, min_pts) >= min_pts;
+  // Morton neighbours (leaf order) first; the walk from the root skips them.
+  // Counts include the point itself and stop at min_pts.
+  constexpr int W = 8;
+  const int64_t w_lo = p - W > 0 ? p - W : 0, w_hi = p + W < n - 1 ? p + W : n - 1;
+  int32_t c = 0;
+  for (int64_t q = w_lo; q <= w_hi && c < min_pts; ++q) {
+    const float4 L = ld_node(leafpt, q);
+    c += hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z);
+  }
+  if (c < min_pts) {
+    const int64_t first_leaf = n - 1;
+    int32_t cur = 0;  // root (a leaf when n == 1)
+    while (cur != kSentinel) {
+      if (cur >= first_leaf) {
+        const int64_t q = cur - first_leaf;
+        const float4 L = ld_node(leafpt, q);
+        cur = __float_as_int(L.w);
+        if (q >= w_lo && q <= w_hi) continue;
+        if (hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z) && ++c == min_pts) break;
+      } else {
+        const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+        cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
+      }
+    }
+  }
+  corep[p] = c >= min_pts;
 }
 
 // The merge rule for one close pair (p's leaf precedes q's).  FOF: every
