@@ -30,9 +30,11 @@ __global__ void k_iota(int32_t *a, int64_t n) {
 // run in leaf order, which is the order sort_queries gives the same points
 // (traversal.hpp:209-218).  Counts include the point itself and stop at
 // min_pts, so count = min(hits, min_pts) whatever the visiting order.
-__global__ void __launch_bounds__(128) k_core_flags(const float4 *__restrict__ nodes,
+template <bool FAST>
+__global__ void __launch_bounds__(128, 1) k_core_flags(const float4 *__restrict__ nodes,
                                                     const float4 *__restrict__ leafpt, int64_t n, Radius R,
                                                     int32_t min_pts, uint8_t *__restrict__ corep) {
+  R.fast = FAST ? 1 : 0;  // as the host checked: one form of the filters compiles
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const float4 me = ld_node(leafpt, p);
@@ -96,11 +98,12 @@ __device__ __forceinline__ void merge_pair(int32_t p, int32_t q, bool core_p, in
 // leaves are examined and each close pair is seen exactly once.  Leaves are
 // read as one 16-byte {x,y,z,rope}; internal nodes take the conservative
 // fp32 test, leaves the exact one.
-template <bool FOF>
-__global__ void __launch_bounds__(128) k_merge_pairs(const float4 *__restrict__ nodes,
+template <bool FOF, bool FAST>
+__global__ void __launch_bounds__(128, 1) k_merge_pairs(const float4 *__restrict__ nodes,
                                                      const float4 *__restrict__ leafpt, int64_t n, Radius R,
                                                      int32_t *parent, const uint8_t *__restrict__ corep,
                                                      uint32_t *claims) {
+  R.fast = FAST ? 1 : 0;
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int64_t first_leaf = n - 1;
@@ -217,7 +220,8 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
   DevBuf<int32_t> parent((size_t)n, c.stream), minobj((size_t)n, c.stream);
   DevBuf<uint32_t> claims(count_phase ? (size_t)((n + 31) / 32) : 0, c.stream);
   if (count_phase) {
-    k_core_flags<<<g128, 128, 0, c.stream>>>(t.nodes, t.leafpt, n, R, min_pts, corep.get());
+    (R.fast ? k_core_flags<true> : k_core_flags<false>)<<<g128, 128, 0, c.stream>>>(t.nodes, t.leafpt, n, R, min_pts,
+                                                                                   corep.get());
     SPB_LAUNCHED();
     mark(c, "core");
   } else {
@@ -228,10 +232,11 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
   SPB_LAUNCHED();
   if (count_phase) {
     SPB_CUDA(cudaMemsetAsync(claims.get(), 0, claims.n * sizeof(uint32_t), c.stream));
-    k_merge_pairs<false><<<g128, 128, 0, c.stream>>>(t.nodes, t.leafpt, n, R, parent.get(), corep.get(),
-                                                     claims.get());
+    (R.fast ? k_merge_pairs<false, true> : k_merge_pairs<false, false>)<<<g128, 128, 0, c.stream>>>(
+        t.nodes, t.leafpt, n, R, parent.get(), corep.get(), claims.get());
   } else {
-    k_merge_pairs<true><<<g128, 128, 0, c.stream>>>(t.nodes, t.leafpt, n, R, parent.get(), corep.get(), nullptr);
+    (R.fast ? k_merge_pairs<true, true> : k_merge_pairs<true, false>)<<<g128, 128, 0, c.stream>>>(
+        t.nodes, t.leafpt, n, R, parent.get(), corep.get(), nullptr);
   }
   SPB_LAUNCHED();
   SPB_CUDA(cudaEventRecord(ev[3], c.stream));

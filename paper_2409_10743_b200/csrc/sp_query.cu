@@ -48,8 +48,10 @@ void query_order(Ctx &c, const float *preds, int64_t nq, int dim, int kind, int3
 // mode 0: spheres of one radius over centres float[nq*dim]
 // mode 1: spheres with per-query radius float[nq*(dim+1)]
 // mode 2: boxes float[nq*2*dim]
+// MODE 0: one radius; 1: per-query radius; 2: box queries; 3: one radius
+// that admits the fp32 filter (compiled without the double box test).
 template <int MODE>
-__global__ void __launch_bounds__(128) k_range_count(const float4 *__restrict__ nodes,
+__global__ void __launch_bounds__(128, 1) k_range_count(const float4 *__restrict__ nodes,
                                                      const float4 *__restrict__ leafpt, int64_t n,
                                                      const float *__restrict__ preds, int dim,
                                                      const int32_t *__restrict__ order, int64_t nq, Radius R0,
@@ -58,11 +60,12 @@ __global__ void __launch_bounds__(128) k_range_count(const float4 *__restrict__ 
   if (qi >= nq) return;
   const int64_t q = order ? order[qi] : qi;
   int32_t c;
-  if (MODE < 2) {
-    const int stride = MODE == 0 ? dim : dim + 1;
+  if (MODE != 2) {
+    const int stride = MODE == 1 ? dim + 1 : dim;
     const float *p = preds + q * stride;
     float cx = p[0], cy = p[1], cz = dim == 3 ? p[2] : 0.f;
-    const Radius R = MODE == 0 ? R0 : make_radius(p[dim]);
+    Radius R = MODE == 1 ? make_radius(p[dim]) : R0;
+    if (MODE == 3) R.fast = 1;
     c = count_sphere(nodes, leafpt, n, cx, cy, cz, R, cap);
   } else {
     float b[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -108,7 +111,10 @@ void range_count(Ctx &c, const Tree &t, int kind, const float *preds, int64_t nq
   unsigned g = (unsigned)((nq + 127) / 128);
   const Radius R = make_radius(radius);
   if (kind == RQ_RADIUS) {
-    k_range_count<0><<<g, 128, 0, c.stream>>>(t.nodes, t.leafpt, t.n, preds, t.dim, ord, nq, R, cap, counts);
+    if (R.fast)
+      k_range_count<3><<<g, 128, 0, c.stream>>>(t.nodes, t.leafpt, t.n, preds, t.dim, ord, nq, R, cap, counts);
+    else
+      k_range_count<0><<<g, 128, 0, c.stream>>>(t.nodes, t.leafpt, t.n, preds, t.dim, ord, nq, R, cap, counts);
   } else if (kind == RQ_SPHERES) {
     k_range_count<1><<<g, 128, 0, c.stream>>>(t.nodes, t.leafpt, t.n, preds, t.dim, ord, nq, R, cap, counts);
   } else {
