@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -49,6 +50,10 @@ std::vector<TraceEv> &trace() {
   static std::vector<TraceEv> t;
   return t;
 }
+std::mutex &trace_mu() {
+  static std::mutex mu;
+  return mu;
+}
 bool tracing() {
   static const bool on = getenv("SPB_DEBUG_E2E") != nullptr;
   return on;
@@ -58,10 +63,13 @@ void trace_ev(spb::Ctx &c, const char *what, cudaStream_t s) {
   cudaEvent_t e;
   cudaEventCreate(&e);
   cudaEventRecord(e, s);
+  std::lock_guard<std::mutex> g(trace_mu());
   trace().push_back({what, c.calls, e});
 }
 void trace_dump() {
-  if (!tracing() || trace().empty()) return;
+  if (!tracing()) return;
+  std::lock_guard<std::mutex> g(trace_mu());
+  if (trace().empty()) return;
   cudaEvent_t t0 = trace().front().e;
   for (auto &t : trace()) {
     float ms = 0.f;
