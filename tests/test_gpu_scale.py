@@ -63,3 +63,45 @@ def test_bench_field_properties(sp):
     assert bool((lab[lab[core].long()] == lab[core]).all())  # the label point is its own cluster's root
     b = sp.friends_of_friends(p, eps)
     assert bool((a.labels == b.labels).all())
+
+
+@pytest.mark.parametrize("shape", ["uniform", "field", "plane", "line", "shell", "dups"])
+@pytest.mark.parametrize("mult", [0.05, 0.3, 1.0, 3.0])
+def test_fof_cells_equal_point_pipeline(sp, shape, mult):
+    # Two independent exact FoF algorithms on the GPU: the grid-cell pipeline
+    # (cells united at their first close member pair) and the point pipeline
+    # (pair traversal over the point LBVH), on 2^20 points of several shapes
+    # and eps from 0.05x to 3x the mean spacing: labels and core flags must be
+    # bit-identical.
+    import os
+    import torch
+    n = 1 << 20
+    g = torch.Generator().manual_seed(["uniform", "field", "plane", "line", "shell", "dups"].index(shape) * 10 +
+                                      [0.05, 0.3, 1.0, 3.0].index(mult))
+    if shape == "uniform":
+        p = torch.rand(n, 3, generator=g)
+    elif shape == "field":
+        p = sp.generate_field(n, seed=7).cpu()
+    elif shape == "plane":
+        p = torch.rand(n, 3, generator=g)
+        p[:, 2] = 0.5
+    elif shape == "line":
+        p = torch.zeros(n, 3)
+        p[:, 0] = torch.rand(n, generator=g)
+    elif shape == "shell":
+        v = torch.randn(n, 3, generator=g)
+        p = v / v.norm(dim=1, keepdim=True) * 0.4 + 0.5
+    else:
+        p = torch.rand(n // 64, 3, generator=g).repeat_interleave(64, 0)
+    p = p.float().contiguous().cuda()
+    spacing = (1.0 / n) ** (1.0 / 3.0) if shape in ("uniform", "field", "shell", "dups") else \
+        ((1.0 / n) ** 0.5 if shape == "plane" else 1.0 / n)
+    eps = float(np.float32(mult * spacing))
+    a = sp.friends_of_friends(p, eps)
+    os.environ["SPB_FOF_POINTS"] = "1"
+    try:
+        b = sp.friends_of_friends(p, eps)
+    finally:
+        del os.environ["SPB_FOF_POINTS"]
+    assert torch.equal(a.labels, b.labels), (shape, mult)
+    assert torch.equal(a.core_flags, b.core_flags), (shape, mult)
