@@ -243,6 +243,7 @@ def run_ours(args, rank, world, local_rank):
     cells = ctx.counter("fof_cells")
     key_bits = 3 * max(1, int(np.ceil(np.log2(1.0 / (eps / np.sqrt(3.0) * (1 - 1e-6)) + 1))))
     pairs_per_pt = None
+    bvh_build = None
     if not slabs:
         b = sp.Bvh.build(pts, ctx=ctx)
         import ctypes
@@ -250,6 +251,22 @@ def run_ours(args, rank, world, local_rank):
         ctx._check(sp._lib.sp_pair_list(ctx.h, b.h, ctypes.c_float(eps), None, 0, ctypes.byref(tot), sp.SP_MEM_DEVICE))
         pairs_per_pt = tot.value / n
         del b
+        # Bvh::build over the same points (the BASELINE "BVH build Mpts/s"),
+        # separately timed: 3 warm builds, events on the context stream
+        bt = []
+        for _ in range(4):
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            b = sp.Bvh.build(pts, ctx=ctx)
+            a1.record(stream)
+            torch.cuda.synchronize(dev)
+            bt.append(a0.elapsed_time(a1))
+            del b
+        bms = statistics.median(bt[1:])
+        peak_b, _ = measured_peak()
+        bvh_build = {"ms": round(bms, 3), "mpts_s": n / (bms / 1e3) / 1e6,
+                     "hbm_frac": round(368.0 * n / (bms / 1e3) / (peak_b * 1e9), 4),
+                     "bytes_model": "368 B/point (SURVEY 8(d): bounds 12 + Morton 24 + sort 192 + hierarchy 140)"}
 
     # ---- device-resident timed region ----
     phase_acc = {}
@@ -369,7 +386,9 @@ def run_ours(args, rank, world, local_rank):
         "roofline": roofline,
         "cpu_baseline": cpu,
         "clocks": clocks,
-        "bvh_build_mpts_s": (n / (build_ms / 1e3) / 1e6) if build_ms else None,
+        "bvh_build_mpts_s": bvh_build["mpts_s"] if bvh_build else None,
+        "bvh_build": bvh_build,
+        "fof_grid_build_mpts_s": (n / (build_ms / 1e3) / 1e6) if build_ms else None,
         "phases_ms": {k: round(v, 3) for k, v in phases.items()},
         "close_pairs_per_point": pairs_per_pt,
         "fof_cells": cells,
