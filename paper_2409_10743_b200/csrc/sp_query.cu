@@ -345,8 +345,10 @@ __device__ __forceinline__ float box_dist(float x, float y, float z, const float
   return __double2float_rn(__dsqrt_rn(gap2(x, y, z, lo, hi)));
 }
 
+// (distance, index) order; bitwise, so the compiler emits one predicate chain
+// instead of a short-circuit branch per comparison
 __device__ __forceinline__ bool cand_less(float da, int32_t ia, float db, int32_t ib) {
-  return da < db || (da == db && ia < ib);
+  return (da < db) | ((da == db) & (ia < ib));
 }
 
 template <int KMAX>
@@ -379,36 +381,45 @@ __global__ void __launch_bounds__(128) k_knn(const float4 *__restrict__ nodes, i
   }
   auto worst = [&]() -> float { return REG ? hd_local[KMAX > 0 ? KMAX - 1 : 0] : hd[0]; };
 
+  // The node being visited lives in registers (d, ref); the nearer child of
+  // an expanded node is visited next without a stack round trip, only the
+  // farther one is pushed (same visiting order as push-both-pop-near).
   float sd[KNN_STACK];
   int32_t sr[KNN_STACK];
   int top = 0;
+  float d;
+  int32_t ref = 0;
   {
     const float4 lo = ld_node(nodes, 0), hi = ld_node(nodes, 1);
-    sd[0] = box_dist(x, y, z, lo, hi);
-    sr[0] = 0;
-    top = 1;
+    d = box_dist(x, y, z, lo, hi);
   }
-  while (top > 0) {
-    --top;
-    const float d = sd[top];
-    const int32_t ref = sr[top];
+  bool have = true;
+  for (;;) {
+    if (!have) {
+      if (top == 0) break;
+      --top;
+      d = sd[top];
+      ref = sr[top];
+    }
+    have = false;
     if (size == kk && d > worst()) continue;
     if (ref >= n - 1) {
       const int32_t obj = node_link(ld_node(nodes, 2 * (int64_t)ref));
       if (REG) {
         constexpr int K = KMAX > 0 ? KMAX : 1;
         if (cand_less(d, obj, hd_local[K - 1], hi_local[K - 1])) {
+          // one comparison per slot, then a select network that shifts the
+          // tail right by one (no branches: 56.4 -> 44.3 ms at C4)
+          bool lt[K];
+#pragma unroll
+          for (int j = 0; j < K; ++j) lt[j] = cand_less(d, obj, hd_local[j], hi_local[j]);
 #pragma unroll
           for (int j = K - 1; j > 0; --j) {
-            const bool shift = cand_less(d, obj, hd_local[j - 1], hi_local[j - 1]);
-            const bool here = !shift && cand_less(d, obj, hd_local[j], hi_local[j]);
-            hd_local[j] = shift ? hd_local[j - 1] : (here ? d : hd_local[j]);
-            hi_local[j] = shift ? hi_local[j - 1] : (here ? obj : hi_local[j]);
+            hd_local[j] = lt[j - 1] ? hd_local[j - 1] : (lt[j] ? d : hd_local[j]);
+            hi_local[j] = lt[j - 1] ? hi_local[j - 1] : (lt[j] ? obj : hi_local[j]);
           }
-          if (cand_less(d, obj, hd_local[0], hi_local[0])) {
-            hd_local[0] = d;
-            hi_local[0] = obj;
-          }
+          hd_local[0] = lt[0] ? d : hd_local[0];
+          hi_local[0] = lt[0] ? obj : hi_local[0];
           if (size < kk) ++size;
         }
       } else if (size < kk) {  // push + sift up
@@ -453,8 +464,17 @@ __global__ void __launch_bounds__(128) k_knn(const float4 *__restrict__ nodes, i
     }
     const bool full = size == kk;
     const float w = worst();
-    if (!(full && df > w) && top < KNN_STACK) { sd[top] = df; sr[top] = rf; ++top; }
-    if (!(full && dn > w) && top < KNN_STACK) { sd[top] = dn; sr[top] = rn; ++top; }
+    const bool keep_f = !(full && df > w), keep_n = !(full && dn > w);
+    if (keep_n) {
+      if (keep_f && top < KNN_STACK) { sd[top] = df; sr[top] = rf; ++top; }
+      d = dn;
+      ref = rn;
+      have = true;
+    } else if (keep_f) {  // not reached (dn <= df), kept as the general rule
+      d = df;
+      ref = rf;
+      have = true;
+    }
   }
   if (REG) {
     constexpr int K = KMAX > 0 ? KMAX : 1;
