@@ -383,7 +383,10 @@ __global__ void __launch_bounds__(128) k_knn(const float4 *__restrict__ nodes, i
 
   // The node being visited lives in registers (d, ref); the nearer child of
   // an expanded node is visited next without a stack round trip, only the
-  // farther one is pushed (same visiting order as push-both-pop-near).
+  // farther one is pushed (same visiting order as push-both-pop-near).  An
+  // entry carries what its node's box load already gave: ref = the left child
+  // of an internal node, or ~object for a leaf, so a pop never re-reads the
+  // node itself (42.6 -> 41.3 ms at C4).
   float sd[KNN_STACK];
   int32_t sr[KNN_STACK];
   int top = 0;
@@ -392,6 +395,7 @@ __global__ void __launch_bounds__(128) k_knn(const float4 *__restrict__ nodes, i
   {
     const float4 lo = ld_node(nodes, 0), hi = ld_node(nodes, 1);
     d = box_dist(x, y, z, lo, hi);
+    ref = n == 1 ? ~node_link(lo) : node_link(lo);
   }
   bool have = true;
   for (;;) {
@@ -403,8 +407,8 @@ __global__ void __launch_bounds__(128) k_knn(const float4 *__restrict__ nodes, i
     }
     have = false;
     if (size == kk && d > worst()) continue;
-    if (ref >= n - 1) {
-      const int32_t obj = node_link(ld_node(nodes, 2 * (int64_t)ref));
+    if (ref < 0) {
+      const int32_t obj = ~ref;
       if (REG) {
         constexpr int K = KMAX > 0 ? KMAX : 1;
         if (cand_less(d, obj, hd_local[K - 1], hi_local[K - 1])) {
@@ -451,13 +455,13 @@ __global__ void __launch_bounds__(128) k_knn(const float4 *__restrict__ nodes, i
       }
       continue;
     }
-    const float4 lo = ld_node(nodes, 2 * (int64_t)ref);
-    const int32_t left = node_link(lo);
+    const int32_t left = ref;
     const float4 llo = ld_node(nodes, 2 * (int64_t)left), lhi = ld_node(nodes, 2 * (int64_t)left + 1);
     const int32_t right = node_rope(lhi);
     const float4 rlo = ld_node(nodes, 2 * (int64_t)right), rhi = ld_node(nodes, 2 * (int64_t)right + 1);
     float dn = box_dist(x, y, z, llo, lhi), df = box_dist(x, y, z, rlo, rhi);
-    int32_t rn = left, rf = right;
+    int32_t rn = left >= n - 1 ? ~node_link(llo) : node_link(llo);
+    int32_t rf = right >= n - 1 ? ~node_link(rlo) : node_link(rlo);
     if (df < dn) {
       float td = dn; dn = df; df = td;
       int32_t tr = rn; rn = rf; rf = tr;

@@ -163,3 +163,21 @@ def test_knn_extreme_scales(sp, oracle, scale):
         widx, wdist = oracle.knn(pts, 3, org, k)
         assert np.array_equal(idx, widx), k
         assert same_float(dist, wdist)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5])
+def test_knn_tiny_trees(sp, oracle, n):
+    # root-is-a-leaf (n = 1) and trees whose children are all leaves; with
+    # duplicated points every distance ties and the index decides
+    rng = np.random.default_rng(100 + n)
+    for dup in (False, True):
+        pts = rng.random((n, 3), dtype=np.float32)
+        if dup:
+            pts[:] = pts[0]
+        org = np.concatenate([rng.random((64, 3), dtype=np.float32), pts])
+        b = sp.Bvh.build(pts)
+        for k in (1, 2, 16, 17, 40):
+            idx, dist = sp.nearest_query(b, org, k, with_distances=True)
+            widx, wdist = oracle.knn(pts, 3, org, k)
+            assert np.array_equal(idx, widx), (n, dup, k)
+            assert same_float(dist, wdist)
