@@ -198,4 +198,49 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
 }
 
 
+
+// ---- SM-affine work schedule ---------------------------------------------------
+// For items sorted in space-filling-curve order (queries, cells): [0, total)
+// is cut into one contiguous slice per SM and every warp takes 32-item chunks
+// from the slice of the SM it runs on, then (once that is drained) from the
+// others.  All warps resident on an SM then walk the same neighbourhood of a
+// tree and share its nodes in L1, instead of the 10-16 distant windows that
+// round-robin block dispatch puts on one SM.  Launch a grid that is fully
+// resident (SmSlices::grid); a lane's item is -1 past the end of a chunk.
+__device__ __forceinline__ uint32_t sm_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+struct SmSliceWalk {
+  int64_t total, per;
+  unsigned long long *ctr;
+  int nslices, own, t = 0;
+  __device__ SmSliceWalk(int64_t total_, unsigned long long *ctr_, int nslices_)
+      : total(total_), per((total_ + nslices_ - 1) / nslices_), ctr(ctr_), nslices(nslices_),
+        own((int)(sm_id() % (uint32_t)nslices_)) {}
+  // Next item of this lane (warp-uniform return: false when all are done).
+  __device__ bool next(int64_t &item) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    while (t < nslices) {
+      const int s = own + t < nslices ? own + t : own + t - nslices;
+      const int64_t lo = (int64_t)s * per, hi = lo + per < total ? lo + per : total;
+      if (lo < hi && (int64_t) * (volatile unsigned long long *)(ctr + s) < hi - lo) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(ctr + s, 32ull);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if ((int64_t)base < hi - lo) {
+          const int64_t i = lo + (int64_t)base + lane;
+          item = i < hi ? i : -1;
+          return true;
+        }
+      }
+      ++t;
+    }
+    return false;
+  }
+};
+
 }  // namespace spb

@@ -704,13 +704,15 @@ __device__ __forceinline__ int32_t cells_leaf(const int64_t *__restrict__ cell_s
 // skipped early when b already hangs off a's root (root hint).
 // FAST: the radius admits the fp32 filter (Radius::fast), so the kernel is
 // compiled without the double-precision box test (merge 29.6 -> 28.0 ms).
+#ifndef SPB_MERGE_SM
+#define SPB_MERGE_SM 1
+#endif
+
 template <bool FAST>
-__global__ void __launch_bounds__(128, 1) k_fof_cells_merge(const float4 *__restrict__ nodes, int64_t m,
-                                                         const int64_t *__restrict__ cell_start, int64_t n,
-                                                         const float4 *__restrict__ cpts, Radius R, int32_t *parent) {
-  R.fast = FAST ? 1 : 0;  // as the host checked: one form of the filters compiles
-  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= m) return;
+__device__ __forceinline__ void fof_cell_walk(const float4 *__restrict__ nodes, int64_t m,
+                                              const int64_t *__restrict__ cell_start, int64_t n,
+                                              const float4 *__restrict__ cpts, const Radius &R, int32_t *parent,
+                                              int64_t a) {
   const int64_t first_leaf = m - 1;
   const float4 qlo = ld_node(nodes, 2 * (first_leaf + a)), qhi = ld_node(nodes, 2 * (first_leaf + a) + 1);
   const int64_t sa = cell_start[a], ea = a + 1 < m ? cell_start[a + 1] : n;
@@ -729,6 +731,29 @@ __global__ void __launch_bounds__(128, 1) k_fof_cells_merge(const float4 *__rest
     root = cells_leaf(cell_start, m, n, cpts, R, parent, sa, ea, root, (int32_t)(cur - first_leaf));
     cur = node_rope(hi);
   }
+}
+
+template <bool FAST>
+__global__ void __launch_bounds__(128, 1) k_fof_cells_merge(const float4 *__restrict__ nodes, int64_t m,
+                                                         const int64_t *__restrict__ cell_start, int64_t n,
+                                                         const float4 *__restrict__ cpts, Radius R, int32_t *parent) {
+  R.fast = FAST ? 1 : 0;  // as the host checked: one form of the filters compiles
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= m) return;
+  fof_cell_walk<FAST>(nodes, m, cell_start, n, cpts, R, parent, a);
+}
+
+// The same walks on the SM-affine schedule (sm_slices, sp_common.cuh).
+template <bool FAST>
+__global__ void __launch_bounds__(128, 1) k_fof_cells_merge_sm(const float4 *__restrict__ nodes, int64_t m,
+                                                            const int64_t *__restrict__ cell_start, int64_t n,
+                                                            const float4 *__restrict__ cpts, Radius R,
+                                                            int32_t *parent, unsigned long long *slices,
+                                                            int nslices) {
+  R.fast = FAST ? 1 : 0;
+  SmSliceWalk w(m, slices, nslices);
+  for (int64_t a; w.next(a);)
+    if (a >= 0) fof_cell_walk<FAST>(nodes, m, cell_start, n, cpts, R, parent, a);
 }
 
 // cells: core iff the cell has two points or its set spans several cells
@@ -1117,7 +1142,15 @@ bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t 
   SPB_LAUNCHED();
   {
     const Radius R = make_radius(eps);
-    if (R.fast)
+    if (SPB_MERGE_SM) {
+      SmSlices sl(c, m);
+      if (R.fast)
+        k_fof_cells_merge_sm<true><<<sl.grid(k_fof_cells_merge_sm<true>, 128), 128, 0, c.stream>>>(
+            g.t.nodes, m, g.cell_start.get(), n, g.cpts.get(), R, parent.get(), sl.ctr.get(), sl.nsm);
+      else
+        k_fof_cells_merge_sm<false><<<sl.grid(k_fof_cells_merge_sm<false>, 128), 128, 0, c.stream>>>(
+            g.t.nodes, m, g.cell_start.get(), n, g.cpts.get(), R, parent.get(), sl.ctr.get(), sl.nsm);
+    } else if (R.fast)
       k_fof_cells_merge<true><<<(unsigned)((m + 127) / 128), 128, 0, c.stream>>>(g.t.nodes, m, g.cell_start.get(), n,
                                                                                  g.cpts.get(), R, parent.get());
     else

@@ -156,4 +156,24 @@ void build_sorted_hierarchy(Ctx &c, const uint64_t *keys, int64_t m, int dim, co
 // sort_queries: the stable 64-bit Morton order of points against their scene.
 void sort_points(Ctx &c, const float *pts, int64_t n, int dim, int32_t *order);
 
+
+// Host side of the SM-affine schedule (SmSliceWalk, sp_common.cuh): one
+// zeroed chunk counter per SM and a fully resident grid.
+struct SmSlices {
+  int nsm = 0;
+  DevBuf<unsigned long long> ctr;
+  SmSlices(Ctx &c, int64_t total) {
+    (void)total;
+    SPB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
+    ctr = DevBuf<unsigned long long>((size_t)nsm, c.stream);
+    SPB_CUDA(cudaMemsetAsync(ctr.get(), 0, (size_t)nsm * sizeof(unsigned long long), c.stream));
+  }
+  template <class K>
+  unsigned grid(K kernel, int threads) const {
+    int per_sm = 0;
+    SPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0));
+    return (unsigned)(nsm * (per_sm > 0 ? per_sm : 1));
+  }
+};
+
 }  // namespace spb
