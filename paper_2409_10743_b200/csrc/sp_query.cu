@@ -50,12 +50,6 @@ void query_order(Ctx &c, const float *preds, int64_t nq, int dim, int kind, int3
 // mode 2: boxes float[nq*2*dim]
 // MODE 0: one radius; 1: per-query radius; 2: box queries; 3: one radius
 // that admits the fp32 filter (compiled without the double box test).
-#ifndef SPB_RC_BS
-#define SPB_RC_BS 128
-#endif
-#ifndef SPB_RC_SM
-#define SPB_RC_SM 1
-#endif
 template <int MODE>
 __device__ __forceinline__ void range_count_one(const float4 *__restrict__ nodes, const float4 *__restrict__ leafpt,
                                                 int64_t n, const float *__restrict__ preds, int dim,
@@ -93,19 +87,9 @@ __device__ __forceinline__ void range_count_one(const float4 *__restrict__ nodes
   counts[q] = c;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(SPB_RC_BS > 128 ? SPB_RC_BS : 128, 1) k_range_count(const float4 *__restrict__ nodes,
-                                                     const float4 *__restrict__ leafpt, int64_t n,
-                                                     const float *__restrict__ preds, int dim,
-                                                     const int32_t *__restrict__ order, int64_t nq, Radius R0,
-                                                     int32_t cap, int32_t *__restrict__ counts) {
-  const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (qi >= nq) return;
-  range_count_one<MODE>(nodes, leafpt, n, preds, dim, order, qi, R0, cap, counts);
-}
-
-// C2-style fixed-radius counts on the SM-affine schedule (sp_common.cuh):
-// 15.7 -> 13.6 ms at 2^24 (512-thread blocks alone: 14.0 ms).
+// Range counts, one query per thread on the SM-affine schedule (sp_common.cuh):
+// C2 query 15.7 -> 12.8 ms at 2^24 (128-thread blocks in plain order: 15.7,
+// 512-thread blocks alone: 14.0).
 template <int MODE>
 __global__ void __launch_bounds__(512, 1) k_range_count_sm(const float4 *__restrict__ nodes,
                                                            const float4 *__restrict__ leafpt, int64_t n,
@@ -136,21 +120,18 @@ void range_count(Ctx &c, const Tree &t, int kind, const float *preds, int64_t nq
     }
     ord = order.get();
   }
-  unsigned g = (unsigned)((nq + 127) / 128);
   const Radius R = make_radius(radius);
-  if (kind == RQ_RADIUS) {
-    if (R.fast && SPB_RC_SM) {
-      SmSlices sl(c, nq);
-      k_range_count_sm<3><<<sl.grid(k_range_count_sm<3>, 512), 512, 0, c.stream>>>(
-          t.nodes, t.leafpt, t.n, preds, t.dim, ord, nq, R, cap, counts, sl.ctr.get(), sl.nsm);
-    } else if (R.fast)
-      k_range_count<3><<<(unsigned)((nq + SPB_RC_BS - 1) / SPB_RC_BS), SPB_RC_BS, 0, c.stream>>>(t.nodes, t.leafpt, t.n, preds, t.dim, ord, nq, R, cap, counts);
-    else
-      k_range_count<0><<<g, 128, 0, c.stream>>>(t.nodes, t.leafpt, t.n, preds, t.dim, ord, nq, R, cap, counts);
-  } else if (kind == RQ_SPHERES) {
-    k_range_count<1><<<g, 128, 0, c.stream>>>(t.nodes, t.leafpt, t.n, preds, t.dim, ord, nq, R, cap, counts);
-  } else {
-    k_range_count<2><<<g, 128, 0, c.stream>>>(t.nodes, t.leafpt, t.n, preds, t.dim, ord, nq, R, cap, counts);
+  const int mode = kind == RQ_RADIUS ? (R.fast ? 3 : 0) : (kind == RQ_SPHERES ? 1 : 2);
+  SmSlices sl(c, nq);
+  auto launch = [&](auto kern) {
+    kern<<<sl.grid(kern, 512), 512, 0, c.stream>>>(t.nodes, t.leafpt, t.n, preds, t.dim, ord, nq, R, cap, counts,
+                                                   sl.ctr.get(), sl.nsm);
+  };
+  switch (mode) {
+    case 3: launch(k_range_count_sm<3>); break;
+    case 0: launch(k_range_count_sm<0>); break;
+    case 1: launch(k_range_count_sm<1>); break;
+    default: launch(k_range_count_sm<2>); break;
   }
   SPB_LAUNCHED();
 }
