@@ -114,4 +114,31 @@ void cache_free(void *p, cudaStream_t s) {
   }
 }
 
+
+int sm_count(int device) {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(device);
+  if (it != cache.end()) return it->second;
+  int v = 0;
+  SPB_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+  cache[device] = v;
+  return v;
+}
+
+int resident_blocks(const void *kernel, int threads) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, int> cache;
+  std::lock_guard<std::mutex> g(mu);
+  const auto key = std::make_pair(kernel, threads);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int v = 0;
+  SPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel, threads, 0));
+  if (v < 1) v = 1;
+  cache[key] = v;
+  return v;
+}
+
 }  // namespace spb

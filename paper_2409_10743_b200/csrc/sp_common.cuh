@@ -221,21 +221,34 @@ struct SmSliceWalk {
       : total(total_), per((total_ + nslices_ - 1) / nslices_), ctr(ctr_), nslices(nslices_),
         own((int)(sm_id() % (uint32_t)nslices_)) {}
   // Next item of this lane (warp-uniform return: false when all are done).
+  // The lanes probe 32 slices' counters at once, so finding work elsewhere
+  // after the own slice is drained costs one round trip per 32 slices.
   __device__ bool next(int64_t &item) {
     const int lane = threadIdx.x & 31;
     __syncwarp();
     while (t < nslices) {
+      const int tl = t + lane;
+      bool avail = false;
+      if (tl < nslices) {
+        const int s = own + tl < nslices ? own + tl : own + tl - nslices;
+        const int64_t lo = (int64_t)s * per, hi = lo + per < total ? lo + per : total;
+        avail = lo < hi && (int64_t) * (volatile unsigned long long *)(ctr + s) < hi - lo;
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, avail);
+      if (!mask) {
+        t += 32;
+        continue;
+      }
+      t += __ffs(mask) - 1;
       const int s = own + t < nslices ? own + t : own + t - nslices;
       const int64_t lo = (int64_t)s * per, hi = lo + per < total ? lo + per : total;
-      if (lo < hi && (int64_t) * (volatile unsigned long long *)(ctr + s) < hi - lo) {
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(ctr + s, 32ull);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if ((int64_t)base < hi - lo) {
-          const int64_t i = lo + (int64_t)base + lane;
-          item = i < hi ? i : -1;
-          return true;
-        }
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(ctr + s, 32ull);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if ((int64_t)base < hi - lo) {
+        const int64_t i = lo + (int64_t)base + lane;
+        item = i < hi ? i : -1;
+        return true;
       }
       ++t;
     }

@@ -707,6 +707,11 @@ __device__ __forceinline__ int32_t cells_leaf(const int64_t *__restrict__ cell_s
 #ifndef SPB_MERGE_SM
 #define SPB_MERGE_SM 1
 #endif
+// below ~4M cells the schedule's tail outweighs the locality (C1, 1M points:
+// 0.63 vs 0.59 ms)
+#ifndef SPB_SM_MIN_ITEMS
+#define SPB_SM_MIN_ITEMS (1 << 22)
+#endif
 
 template <bool FAST>
 __device__ __forceinline__ void fof_cell_walk(const float4 *__restrict__ nodes, int64_t m,
@@ -1142,7 +1147,7 @@ bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t 
   SPB_LAUNCHED();
   {
     const Radius R = make_radius(eps);
-    if (SPB_MERGE_SM) {
+    if (SPB_MERGE_SM && m >= SPB_SM_MIN_ITEMS) {
       SmSlices sl(c, m);
       if (R.fast)
         k_fof_cells_merge_sm<true><<<sl.grid(k_fof_cells_merge_sm<true>, 128), 128, 0, c.stream>>>(

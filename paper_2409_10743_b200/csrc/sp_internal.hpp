@@ -158,22 +158,23 @@ void sort_points(Ctx &c, const float *pts, int64_t n, int dim, int32_t *order);
 
 
 // Host side of the SM-affine schedule (SmSliceWalk, sp_common.cuh): one
-// zeroed chunk counter per SM and a fully resident grid.
+// zeroed chunk counter per SM and a fully resident grid.  The SM count and
+// each kernel's residency are queried once per process (device 0 of the pool
+// and every B200 agree), not per call.
+int sm_count(int device);
+int resident_blocks(const void *kernel, int threads);
 struct SmSlices {
   int nsm = 0;
   DevBuf<unsigned long long> ctr;
   SmSlices(Ctx &c, int64_t total) {
     (void)total;
-    SPB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
+    nsm = sm_count(c.device);
     ctr = DevBuf<unsigned long long>((size_t)nsm, c.stream);
     SPB_CUDA(cudaMemsetAsync(ctr.get(), 0, (size_t)nsm * sizeof(unsigned long long), c.stream));
   }
   template <class K>
   unsigned grid(K kernel, int threads) const {
-    int per_sm = 0;
-    SPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0));
-    return (unsigned)(nsm * (per_sm > 0 ? per_sm : 1));
+    return (unsigned)(nsm * resident_blocks(reinterpret_cast<const void *>(kernel), threads));
   }
 };
-
 }  // namespace spb
