@@ -33,10 +33,12 @@ __global__ void k_iota(int32_t *a, int64_t n) {
 template <bool FAST>
 __global__ void __launch_bounds__(128, 1) k_core_flags(const float4 *__restrict__ nodes,
                                                     const float4 *__restrict__ leafpt, int64_t n, Radius R,
-                                                    int32_t min_pts, uint8_t *__restrict__ corep) {
+                                                    int32_t min_pts, uint8_t *__restrict__ corep,
+                                                    unsigned long long *slices, int nslices) {
   R.fast = FAST ? 1 : 0;  // as the host checked: one form of the filters compiles
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
+  SmSliceWalk w(n, slices, nslices);
+  for (int64_t p; w.next(p);) {
+  if (p < 0) continue;
   const float4 me = ld_node(leafpt, p);
   // Morton neighbours (leaf order) first; the walk from the root skips them.
   // Counts include the point itself and stop at min_pts.
@@ -64,6 +66,7 @@ __global__ void __launch_bounds__(128, 1) k_core_flags(const float4 *__restrict_
     }
   }
   corep[p] = c >= min_pts;
+  }
 }
 
 // The merge rule for one close pair (p's leaf precedes q's).  FOF: every
@@ -102,10 +105,11 @@ template <bool FOF, bool FAST>
 __global__ void __launch_bounds__(128, 1) k_merge_pairs(const float4 *__restrict__ nodes,
                                                      const float4 *__restrict__ leafpt, int64_t n, Radius R,
                                                      int32_t *parent, const uint8_t *__restrict__ corep,
-                                                     uint32_t *claims) {
+                                                     uint32_t *claims, unsigned long long *slices, int nslices) {
   R.fast = FAST ? 1 : 0;
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
+  SmSliceWalk w(n, slices, nslices);
+  for (int64_t p; w.next(p);) {
+  if (p < 0) continue;
   const int64_t first_leaf = n - 1;
   const float4 me = ld_node(leafpt, p);
   int32_t cur = __float_as_int(me.w);
@@ -123,6 +127,7 @@ __global__ void __launch_bounds__(128, 1) k_merge_pairs(const float4 *__restrict
       const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
       cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
     }
+  }
   }
 }
 
@@ -215,13 +220,16 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
   SPB_CUDA(cudaEventRecord(ev[1], c.stream));
   const Radius R = make_radius(eps);
   const bool count_phase = min_pts > 2;
-  const unsigned g128 = (unsigned)((n + 127) / 128), g256 = (unsigned)((n + 255) / 256);
+  const unsigned g256 = (unsigned)((n + 255) / 256);
   DevBuf<uint8_t> corep((size_t)n, c.stream);
   DevBuf<int32_t> parent((size_t)n, c.stream), minobj((size_t)n, c.stream);
   DevBuf<uint32_t> claims(count_phase ? (size_t)((n + 31) / 32) : 0, c.stream);
+  // both walks run on the SM-affine schedule (sp_common.cuh)
   if (count_phase) {
-    (R.fast ? k_core_flags<true> : k_core_flags<false>)<<<g128, 128, 0, c.stream>>>(t.nodes, t.leafpt, n, R, min_pts,
-                                                                                   corep.get());
+    SmSlices sl(c, n);
+    auto kern = R.fast ? k_core_flags<true> : k_core_flags<false>;
+    kern<<<sl.grid(kern, 128), 128, 0, c.stream>>>(t.nodes, t.leafpt, n, R, min_pts, corep.get(), sl.ctr.get(),
+                                                   sl.nsm);
     SPB_LAUNCHED();
     mark(c, "core");
   } else {
@@ -230,13 +238,13 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
   SPB_CUDA(cudaEventRecord(ev[2], c.stream));
   k_iota<<<grid_for(n, 256, 148 * 16), 256, 0, c.stream>>>(parent.get(), n);
   SPB_LAUNCHED();
-  if (count_phase) {
-    SPB_CUDA(cudaMemsetAsync(claims.get(), 0, claims.n * sizeof(uint32_t), c.stream));
-    (R.fast ? k_merge_pairs<false, true> : k_merge_pairs<false, false>)<<<g128, 128, 0, c.stream>>>(
-        t.nodes, t.leafpt, n, R, parent.get(), corep.get(), claims.get());
-  } else {
-    (R.fast ? k_merge_pairs<true, true> : k_merge_pairs<true, false>)<<<g128, 128, 0, c.stream>>>(
-        t.nodes, t.leafpt, n, R, parent.get(), corep.get(), nullptr);
+  {
+    SmSlices sl(c, n);
+    if (count_phase) SPB_CUDA(cudaMemsetAsync(claims.get(), 0, claims.n * sizeof(uint32_t), c.stream));
+    auto kern = count_phase ? (R.fast ? k_merge_pairs<false, true> : k_merge_pairs<false, false>)
+                            : (R.fast ? k_merge_pairs<true, true> : k_merge_pairs<true, false>);
+    kern<<<sl.grid(kern, 128), 128, 0, c.stream>>>(t.nodes, t.leafpt, n, R, parent.get(), corep.get(),
+                                                   count_phase ? claims.get() : nullptr, sl.ctr.get(), sl.nsm);
   }
   SPB_LAUNCHED();
   SPB_CUDA(cudaEventRecord(ev[3], c.stream));
