@@ -218,9 +218,11 @@ __global__ void __launch_bounds__(128) k_range_fill(const float4 *__restrict__ n
                                                     const float *__restrict__ preds, int dim,
                                                     const int32_t *__restrict__ order, int64_t nq,
                                                     const int64_t *__restrict__ offsets,
-                                                    uint64_t *__restrict__ keyed) {
-  const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (qi >= nq) return;
+                                                    uint64_t *__restrict__ keyed, unsigned long long *slices,
+                                                    int nslices) {
+  SmSliceWalk sw(nq, slices, nslices);  // SM-affine schedule (sp_common.cuh)
+  for (int64_t qi; sw.next(qi);) {
+  if (qi < 0) continue;
   const int64_t q = order[qi];
   int64_t w = offsets[q];
   float b[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -251,6 +253,7 @@ __global__ void __launch_bounds__(128) k_range_fill(const float4 *__restrict__ n
       cur = hit ? node_link(lo) : node_rope(hi);
     }
   }
+  }
 }
 
 __global__ void k_low_words(const uint64_t *__restrict__ keys, int64_t m, int32_t *__restrict__ out) {
@@ -274,11 +277,13 @@ int64_t range_crs(Ctx &c, const Tree &t, int kind, const float *preds, int64_t n
   if (total == 0 || t.n == 0) return total;
   DevBuf<uint64_t> k0((size_t)total, c.stream), k1((size_t)total, c.stream);
   DevBuf<uint32_t> v0((size_t)total, c.stream), v1((size_t)total, c.stream);
-  unsigned g = (unsigned)((nq + 127) / 128);
+  SmSlices sl(c, nq);
   if (kind == RQ_SPHERES)
-    k_range_fill<1><<<g, 128, 0, c.stream>>>(t.nodes, t.n, preds, t.dim, order.get(), nq, offsets, k0.get());
+    k_range_fill<1><<<sl.grid(k_range_fill<1>, 128), 128, 0, c.stream>>>(t.nodes, t.n, preds, t.dim, order.get(), nq,
+                                                                         offsets, k0.get(), sl.ctr.get(), sl.nsm);
   else
-    k_range_fill<2><<<g, 128, 0, c.stream>>>(t.nodes, t.n, preds, t.dim, order.get(), nq, offsets, k0.get());
+    k_range_fill<2><<<sl.grid(k_range_fill<2>, 128), 128, 0, c.stream>>>(t.nodes, t.n, preds, t.dim, order.get(), nq,
+                                                                         offsets, k0.get(), sl.ctr.get(), sl.nsm);
   SPB_LAUNCHED();
   int qbits = 1;
   while (qbits < 31 && (1LL << qbits) < nq) ++qbits;
