@@ -235,6 +235,21 @@ def _out(like_device: bool, shape, np_dtype, torch_dtype=None, device=None):
     return arr, arr.ctypes.data_as(C.c_void_p)
 
 
+def _given_out(a, shape, itemsize: int, dev: bool):
+    """Pointer of a caller-supplied output buffer (numpy array or tensor, e.g.
+    a reusable pinned host tensor): contiguous, in the inputs' memory space,
+    with the expected shape and element size."""
+    if _is_cuda(a) != dev:
+        raise ValueError("out must live in the same memory space as the inputs")
+    if tuple(a.shape) != tuple(shape):
+        raise ValueError("out has shape %s, expected %s" % (tuple(a.shape), tuple(shape)))
+    size = a.element_size() if _is_torch(a) else a.itemsize
+    contiguous = a.is_contiguous() if _is_torch(a) else a.flags["C_CONTIGUOUS"]
+    if size != itemsize or not contiguous:
+        raise ValueError("out must be contiguous with %d-byte elements" % itemsize)
+    return a, _ptr(a)
+
+
 def _dim_of(a) -> int:
     s = tuple(a.shape)
     if len(s) != 2 or s[1] not in (2, 3):
@@ -383,19 +398,23 @@ def validate_arrays(e: dict, n: int, dim: int) -> tuple:
 
 
 # ---- queries ----------------------------------------------------------------------
-def range_count(bvh: Bvh, predicates, kind: str = "sphere", cap: int = 0, radius: Optional[float] = None):
+def range_count(bvh: Bvh, predicates, kind: str = "sphere", cap: int = 0, radius: Optional[float] = None,
+                out=None):
     """range_query with a counting callback (traversal.hpp:67-87).
 
     kind="sphere": predicates (nq, d+1) = centre, radius; or (nq, d) centres
     with a shared `radius`.  kind="box": (nq, 2d) boxes.  cap > 0 terminates a
-    query at cap matches (detect_core_counts, dbscan.hpp:146-170)."""
+    query at cap matches (detect_core_counts, dbscan.hpp:146-170).  out: an
+    optional int32 (nq,) buffer to write the counts into (returned)."""
     ctx = bvh.ctx
     nq = int(predicates.shape[0])
     p, mem, keep = _in(predicates, np.float32)
     dev = mem == SP_MEM_DEVICE
-    import_torch = dev
-    counts, cp = _out(dev, (nq,), np.int32, _torch_dtype("int32") if import_torch else None,
-                      predicates.device if dev else None)
+    if out is not None:
+        counts, cp = _given_out(out, (nq,), 4, dev)
+    else:
+        counts, cp = _out(dev, (nq,), np.int32, _torch_dtype("int32") if dev else None,
+                          predicates.device if dev else None)
     if radius is not None:
         ctx._check(_lib.sp_range_count_radius(ctx.h, bvh.h, p, nq, float(radius), int(cap), cp, mem))
     else:
@@ -423,19 +442,28 @@ def query_crs(bvh: Bvh, predicates, kind: str = "sphere", max_total_matches: Opt
     return offsets, values[:total]
 
 
-def nearest_query(bvh: Bvh, origins, k: int, with_distances: bool = False):
+def nearest_query(bvh: Bvh, origins, k: int, with_distances: bool = False, out=None):
     """nearest_query (traversal.hpp:93-156): (nq, k) object indices ascending
-    by (distance, index), padded with -1 beyond min(k, n)."""
+    by (distance, index), padded with -1 beyond min(k, n).  out: optional
+    (nq, k) int32 index buffer, or (indices, distances) with with_distances."""
     ctx = bvh.ctx
     nq = int(origins.shape[0])
     kk = max(int(k), 0)
     p, mem, keep = _in(origins, np.float32)
     dev = mem == SP_MEM_DEVICE
-    idx, ip = _out(dev, (nq, kk), np.int32, _torch_dtype("int32") if dev else None, origins.device if dev else None)
+    out_idx, out_dist = (out if with_distances else (out, None)) if out is not None else (None, None)
+    if out_idx is not None:
+        idx, ip = _given_out(out_idx, (nq, kk), 4, dev)
+    else:
+        idx, ip = _out(dev, (nq, kk), np.int32, _torch_dtype("int32") if dev else None,
+                       origins.device if dev else None)
     dist, dp = (None, None)
     if with_distances:
-        dist, dp = _out(dev, (nq, kk), np.float32, _torch_dtype("float32") if dev else None,
-                        origins.device if dev else None)
+        if out_dist is not None:
+            dist, dp = _given_out(out_dist, (nq, kk), 4, dev)
+        else:
+            dist, dp = _out(dev, (nq, kk), np.float32, _torch_dtype("float32") if dev else None,
+                            origins.device if dev else None)
     if kk > 0 and nq > 0:
         ctx._check(_lib.sp_knn(ctx.h, bvh.h, p, nq, kk, ip, dp, mem))
     return (idx, dist) if with_distances else idx

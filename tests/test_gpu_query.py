@@ -181,3 +181,30 @@ def test_knn_tiny_trees(sp, oracle, n):
             widx, wdist = oracle.knn(pts, 3, org, k)
             assert np.array_equal(idx, widx), (n, dup, k)
             assert same_float(dist, wdist)
+
+
+def test_query_out_buffers(sp):
+    # caller-supplied (pinned host or device) result buffers give the same
+    # results as the allocated ones; wrong shape / dtype / memory space raise
+    import torch
+    rng = np.random.default_rng(31)
+    pts = rng.random((5000, 3), dtype=np.float32)
+    b = sp.Bvh.build(pts)
+    want_c = sp.range_count(b, pts, radius=0.05)
+    want_i, want_d = sp.nearest_query(b, pts, 8, with_distances=True)
+    hc = torch.empty(5000, dtype=torch.int32, pin_memory=True)
+    assert sp.range_count(b, pts, radius=0.05, out=hc) is hc
+    assert np.array_equal(hc.numpy(), want_c)
+    hi = torch.empty((5000, 8), dtype=torch.int32, pin_memory=True)
+    hd = torch.empty((5000, 8), dtype=torch.float32, pin_memory=True)
+    sp.nearest_query(b, pts, 8, with_distances=True, out=(hi, hd))
+    assert np.array_equal(hi.numpy(), want_i) and np.array_equal(hd.numpy(), want_d)
+    dpts = torch.from_numpy(pts).cuda()
+    db = sp.Bvh.build(dpts)
+    di = torch.empty((5000, 8), dtype=torch.int32, device="cuda")
+    sp.nearest_query(db, dpts, 8, out=di)
+    assert np.array_equal(di.cpu().numpy(), want_i)
+    with pytest.raises(ValueError):
+        sp.nearest_query(b, pts, 8, out=di)  # device buffer for host inputs
+    with pytest.raises(ValueError):
+        sp.range_count(b, pts, radius=0.05, out=np.empty(4999, np.int32))
