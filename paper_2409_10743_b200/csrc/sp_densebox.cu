@@ -801,7 +801,7 @@ __global__ void __launch_bounds__(256) k_fof_cells_labels(int64_t n, const int32
   const int32_t cl = cell_of[k];
   const int32_t o = (int32_t)order[k];
   const bool c = multi[cl] != 0;
-  labels[o] = c ? minobj[uf_root(parent, cl)] : -1;
+  labels[o] = c ? minobj[parent[cl]] : -1;  // parent is flat after k_fof_cells_core_min
 }
 
 // FoF core flags in input order: core <=> the point has a label (every member
