@@ -208,3 +208,19 @@ def test_query_out_buffers(sp):
         sp.nearest_query(b, pts, 8, out=di)  # device buffer for host inputs
     with pytest.raises(ValueError):
         sp.range_count(b, pts, radius=0.05, out=np.empty(4999, np.int32))
+
+
+@pytest.mark.parametrize("nq", [1, 31, 32, 33, 148 * 32 - 1, 148 * 32 + 5, 148 * 512 + 77])
+def test_range_counts_every_query_once(sp, oracle, nq):
+    # the SM-affine schedule (per-SM slices, 32-query chunks, stealing) must
+    # write every count exactly once for totals around its chunk and slice sizes
+    import torch
+    rng = np.random.default_rng(nq)
+    pts = rng.random((3000, 3), dtype=np.float32)
+    qs = rng.random((nq, 3), dtype=np.float32)
+    b = sp.Bvh.build(pts)
+    want = oracle.range_count(pts, 3, spheres_of(qs, np.float32(0.06)))
+    assert np.array_equal(sp.range_count(b, qs, radius=0.06), want)
+    out = torch.full((nq,), -7, dtype=torch.int32, device="cuda")
+    sp.range_count(sp.Bvh.build(torch.from_numpy(pts).cuda()), torch.from_numpy(qs).cuda(), radius=0.06, out=out)
+    assert np.array_equal(out.cpu().numpy(), want)
