@@ -754,7 +754,8 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
   mark(c, "hierarchy");
 }
 
-void build_sorted_hierarchy(Ctx &c, const uint64_t *keys, int64_t m, int dim, const float *boxes, Tree &t) {
+void build_sorted_hierarchy(Ctx &c, const uint64_t *keys, int64_t m, int dim, const float *boxes, Tree &t,
+                            DevBuf<int32_t> *delta_in) {
   t.n = m;
   t.dim = dim;
   t.width = 64;
@@ -763,10 +764,14 @@ void build_sorted_hierarchy(Ctx &c, const uint64_t *keys, int64_t m, int dim, co
   if (m == 0) return;
   t.nodes = static_cast<decltype(t.nodes)>(cache_alloc((size_t)(2 * m - 1) * 2 * sizeof(float4), c.stream));
   t.perm = static_cast<decltype(t.perm)>(cache_alloc((size_t)m * sizeof(int32_t), c.stream));
-  DevBuf<int32_t> delta(m > 1 ? m - 1 : 1, c.stream), flags(m > 1 ? m - 1 : 1, c.stream);
+  DevBuf<int32_t> own_delta, flags(m > 1 ? m - 1 : 1, c.stream);
+  DevBuf<int32_t> &delta = delta_in ? *delta_in : own_delta;
+  if (!delta_in) own_delta = DevBuf<int32_t>(m > 1 ? m - 1 : 1, c.stream);
   if (m > 1) {
-    k_delta<<<grid_for(m, 256, 148 * 16), 256, 0, c.stream>>>(keys, nullptr, m, 64, delta.get());
-    SPB_LAUNCHED();
+    if (!delta_in) {
+      k_delta<<<grid_for(m, 256, 148 * 16), 256, 0, c.stream>>>(keys, nullptr, m, 64, delta.get());
+      SPB_LAUNCHED();
+    }
     SPB_CUDA(cudaMemsetAsync(flags.get(), 0xff, (size_t)(m - 1) * sizeof(int32_t), c.stream));
   }
   ClimbQueue q(c, m, 6);

@@ -651,10 +651,13 @@ __global__ void k_dense_core(const int32_t *__restrict__ point_cell, int64_t n, 
 // close pair, which unions the two cells.  Labels are canonical, so the result
 // equals the point-based FoF bit for bit.
 // ---------------------------------------------------------------------------
+// ckeys == nullptr: write the hierarchy's split array instead (delta[j] =
+// the common-prefix length of cell keys j and j + 1, k_delta's value for
+// distinct 64-bit keys), so the cell keys need not be stored and re-read.
 __global__ void k_cell_ranges(const int64_t *__restrict__ cell_start, int64_t m, int64_t n,
                               const uint64_t *__restrict__ skeys, const float4 *__restrict__ cpts, int dim,
                               uint64_t *__restrict__ ckeys, float *__restrict__ boxes, int32_t *__restrict__ cell_of,
-                              uint8_t *__restrict__ multi) {
+                              uint8_t *__restrict__ multi, int32_t *__restrict__ delta) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride) {
     const int64_t s = cell_start[j], e = j + 1 < m ? cell_start[j + 1] : n;
@@ -670,7 +673,8 @@ __global__ void k_cell_ranges(const int64_t *__restrict__ cell_start, int64_t m,
       boxes[j * 2 * dim + k] = lo[k];
       boxes[j * 2 * dim + dim + k] = hi[k];
     }
-    ckeys[j] = skeys[s];
+    if (ckeys) ckeys[j] = skeys[s];
+    if (delta && j + 1 < m) delta[j] = __clzll((long long)(skeys[s] ^ skeys[e]));
     multi[j] = (e - s) > 1;
   }
 }
@@ -1113,13 +1117,14 @@ bool build_cell_grid(Ctx &c, const float *pts, int64_t n, int dim, float eps, Ce
     fprintf(stderr, "[grid] n %lld scene %g %g %g .. %g %g %g bits %d cells %lld\n", (long long)n, hs[0], hs[1], hs[2],
             hs[3], hs[4], hs[5], bits, (long long)m);
   g.m = m;
-  DevBuf<uint64_t> ckeys((size_t)m, c.stream);
+  DevBuf<int32_t> delta(m > 1 ? m - 1 : 1, c.stream);
   DevBuf<float> boxes((size_t)m * 2 * dim, c.stream);
   g.multi = DevBuf<uint8_t>((size_t)m, c.stream);
   k_cell_ranges<<<grid_for(m, 256, 148 * 16), 256, 0, c.stream>>>(g.cell_start.get(), m, n, ka, g.cpts.get(), dim,
-                                                                   ckeys.get(), boxes.get(), nullptr, g.multi.get());
+                                                                   nullptr, boxes.get(), nullptr, g.multi.get(),
+                                                                   delta.get());
   SPB_LAUNCHED();
-  build_sorted_hierarchy(c, ckeys.get(), m, dim, boxes.get(), g.t);
+  build_sorted_hierarchy(c, nullptr, m, dim, boxes.get(), g.t, &delta);
   mark(c, "hierarchy");
   return true;
 }

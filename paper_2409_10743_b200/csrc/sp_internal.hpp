@@ -152,7 +152,10 @@ void radix_sort_pairs(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_
 void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, int width, Tree &t);
 // LBVH over m objects already in key order (strictly increasing keys): leaf p
 // is object p with box boxes[p] (2*dim floats); no sort, identity permutation.
-void build_sorted_hierarchy(Ctx &c, const uint64_t *keys, int64_t m, int dim, const float *boxes, Tree &t);
+// delta_in: the key-split array (m - 1 entries, k_delta's values) when the
+// caller already computed it; keys are then not read.
+void build_sorted_hierarchy(Ctx &c, const uint64_t *keys, int64_t m, int dim, const float *boxes, Tree &t,
+                            DevBuf<int32_t> *delta_in = nullptr);
 // sort_queries: the stable 64-bit Morton order of points against their scene.
 void sort_points(Ctx &c, const float *pts, int64_t n, int dim, int32_t *order);
 
