@@ -38,34 +38,34 @@ __global__ void __launch_bounds__(128, 1) k_core_flags(const float4 *__restrict_
   R.fast = FAST ? 1 : 0;  // as the host checked: one form of the filters compiles
   SmSliceWalk w(n, slices, nslices);
   for (int64_t p; w.next(p);) {
-  if (p < 0) continue;
-  const float4 me = ld_node(leafpt, p);
-  // Morton neighbours (leaf order) first; the walk from the root skips them.
-  // Counts include the point itself and stop at min_pts.
-  constexpr int W = 8;
-  const int64_t w_lo = p - W > 0 ? p - W : 0, w_hi = p + W < n - 1 ? p + W : n - 1;
-  int32_t c = 0;
-  for (int64_t q = w_lo; q <= w_hi && c < min_pts; ++q) {
-    const float4 L = ld_node(leafpt, q);
-    c += hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z);
-  }
-  if (c < min_pts) {
-    const int64_t first_leaf = n - 1;
-    int32_t cur = 0;  // root (a leaf when n == 1)
-    while (cur != kSentinel) {
-      if (cur >= first_leaf) {
-        const int64_t q = cur - first_leaf;
-        const float4 L = ld_node(leafpt, q);
-        cur = __float_as_int(L.w);
-        if (q >= w_lo && q <= w_hi) continue;
-        if (hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z) && ++c == min_pts) break;
-      } else {
-        const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
-        cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
+    if (p < 0) continue;
+    const float4 me = ld_node(leafpt, p);
+    // Morton neighbours (leaf order) first; the walk from the root skips them.
+    // Counts include the point itself and stop at min_pts.
+    constexpr int W = 8;
+    const int64_t w_lo = p - W > 0 ? p - W : 0, w_hi = p + W < n - 1 ? p + W : n - 1;
+    int32_t c = 0;
+    for (int64_t q = w_lo; q <= w_hi && c < min_pts; ++q) {
+      const float4 L = ld_node(leafpt, q);
+      c += hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z);
+    }
+    if (c < min_pts) {
+      const int64_t first_leaf = n - 1;
+      int32_t cur = 0;  // root (a leaf when n == 1)
+      while (cur != kSentinel) {
+        if (cur >= first_leaf) {
+          const int64_t q = cur - first_leaf;
+          const float4 L = ld_node(leafpt, q);
+          cur = __float_as_int(L.w);
+          if (q >= w_lo && q <= w_hi) continue;
+          if (hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z) && ++c == min_pts) break;
+        } else {
+          const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+          cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
+        }
       }
     }
-  }
-  corep[p] = c >= min_pts;
+    corep[p] = c >= min_pts;
   }
 }
 
@@ -109,25 +109,25 @@ __global__ void __launch_bounds__(128, 1) k_merge_pairs(const float4 *__restrict
   R.fast = FAST ? 1 : 0;
   SmSliceWalk w(n, slices, nslices);
   for (int64_t p; w.next(p);) {
-  if (p < 0) continue;
-  const int64_t first_leaf = n - 1;
-  const float4 me = ld_node(leafpt, p);
-  int32_t cur = __float_as_int(me.w);
-  int32_t root_p = (int32_t)p;
-  const bool core_p = FOF ? true : corep[p] != 0;
-  while (cur != kSentinel) {
-    if (cur >= first_leaf) {
-      const int32_t q = (int32_t)(cur - first_leaf);
-      const float4 L = ld_node(leafpt, q);
-      if (hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z))
-        merge_pair<FOF>((int32_t)p, q, core_p, root_p, parent, corep, claims);
-      cur = __float_as_int(L.w);
-    } else {
-      const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
-      const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
-      cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
+    if (p < 0) continue;
+    const int64_t first_leaf = n - 1;
+    const float4 me = ld_node(leafpt, p);
+    int32_t cur = __float_as_int(me.w);
+    int32_t root_p = (int32_t)p;
+    const bool core_p = FOF ? true : corep[p] != 0;
+    while (cur != kSentinel) {
+      if (cur >= first_leaf) {
+        const int32_t q = (int32_t)(cur - first_leaf);
+        const float4 L = ld_node(leafpt, q);
+        if (hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z))
+          merge_pair<FOF>((int32_t)p, q, core_p, root_p, parent, corep, claims);
+        cur = __float_as_int(L.w);
+      } else {
+        const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
+        const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+        cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
+      }
     }
-  }
   }
 }
 

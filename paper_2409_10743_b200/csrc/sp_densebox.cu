@@ -1255,46 +1255,46 @@ __global__ void __launch_bounds__(128) k_cells_core(const float4 *__restrict__ n
   R.fast = FAST ? 1 : 0;
   SmSliceWalk w(n, slices, nslices);
   for (int64_t k; w.next(k);) {
-  if (k < 0) continue;
-  const int32_t own = cell_of[k];
-  int32_t cnt = (int32_t)(cell_end(cell_start, m, n, own) - cell_start[own]);
-  const float4 me = cpts[k];
-  const int64_t first_leaf = m - 1;
-  // Morton-neighbour cells first (key order is spatial order): in dense
-  // regions they usually hold the missing neighbours and the tree walk is
-  // skipped; the walk below does not count them again.
-  const int64_t w_lo = own - SPB_CORE_WINDOW > 0 ? own - SPB_CORE_WINDOW : 0;
-  const int64_t w_hi = own + SPB_CORE_WINDOW < m - 1 ? own + SPB_CORE_WINDOW : m - 1;
-  for (int64_t b = w_lo; b <= w_hi && cnt < min_pts; ++b) {
-    if (b == own) continue;
-    const float4 lo = ld_node(nodes, 2 * (first_leaf + b)), hi = ld_node(nodes, 2 * (first_leaf + b) + 1);
-    if (!hit_box(R, me.x, me.y, me.z, lo, hi)) continue;
-    const int64_t e = cell_end(cell_start, m, n, b);
-    for (int64_t j = cell_start[b]; j < e && cnt < min_pts; ++j) {
-      const float4 q = cpts[j];
-      cnt += hit_point(R, me.x, me.y, me.z, q.x, q.y, q.z);
-    }
-  }
-  if (cnt < min_pts) {
-    int32_t cur = 0;  // root: internal 0, or leaf 0 when m == 1
-    while (cur != kSentinel) {
-      const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
-      if (cur < first_leaf) {
-        cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
-        continue;
-      }
-      const int64_t b = cur - first_leaf;
-      cur = node_rope(hi);
-      if ((b >= w_lo && b <= w_hi) || !hit_box(R, me.x, me.y, me.z, lo, hi)) continue;
+    if (k < 0) continue;
+    const int32_t own = cell_of[k];
+    int32_t cnt = (int32_t)(cell_end(cell_start, m, n, own) - cell_start[own]);
+    const float4 me = cpts[k];
+    const int64_t first_leaf = m - 1;
+    // Morton-neighbour cells first (key order is spatial order): in dense
+    // regions they usually hold the missing neighbours and the tree walk is
+    // skipped; the walk below does not count them again.
+    const int64_t w_lo = own - SPB_CORE_WINDOW > 0 ? own - SPB_CORE_WINDOW : 0;
+    const int64_t w_hi = own + SPB_CORE_WINDOW < m - 1 ? own + SPB_CORE_WINDOW : m - 1;
+    for (int64_t b = w_lo; b <= w_hi && cnt < min_pts; ++b) {
+      if (b == own) continue;
+      const float4 lo = ld_node(nodes, 2 * (first_leaf + b)), hi = ld_node(nodes, 2 * (first_leaf + b) + 1);
+      if (!hit_box(R, me.x, me.y, me.z, lo, hi)) continue;
       const int64_t e = cell_end(cell_start, m, n, b);
       for (int64_t j = cell_start[b]; j < e && cnt < min_pts; ++j) {
         const float4 q = cpts[j];
         cnt += hit_point(R, me.x, me.y, me.z, q.x, q.y, q.z);
       }
-      if (cnt >= min_pts) break;
     }
-  }
-  corep[k] = cnt >= min_pts;
+    if (cnt < min_pts) {
+      int32_t cur = 0;  // root: internal 0, or leaf 0 when m == 1
+      while (cur != kSentinel) {
+        const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+        if (cur < first_leaf) {
+          cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
+          continue;
+        }
+        const int64_t b = cur - first_leaf;
+        cur = node_rope(hi);
+        if ((b >= w_lo && b <= w_hi) || !hit_box(R, me.x, me.y, me.z, lo, hi)) continue;
+        const int64_t e = cell_end(cell_start, m, n, b);
+        for (int64_t j = cell_start[b]; j < e && cnt < min_pts; ++j) {
+          const float4 q = cpts[j];
+          cnt += hit_point(R, me.x, me.y, me.z, q.x, q.y, q.z);
+        }
+        if (cnt >= min_pts) break;
+      }
+    }
+    corep[k] = cnt >= min_pts;
   }
 }
 
@@ -1324,46 +1324,46 @@ __global__ void __launch_bounds__(128) k_cells_core_merge(const float4 *__restri
   uint64_t checks = 0;
   SmSliceWalk w(m, slices, nslices);
   for (int64_t a; w.next(a);)
-  if (a >= 0 && hascore[a]) {
-    const int64_t first_leaf = m - 1;
-    const float4 qlo = ld_node(nodes, 2 * (first_leaf + a)), qhi = ld_node(nodes, 2 * (first_leaf + a) + 1);
-    const int64_t sa = cell_start[a], ea = cell_end(cell_start, m, n, a);
-    int32_t root = (int32_t)a;
-    int32_t cur = node_rope(qhi);
-    while (cur != kSentinel) {
-      const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
-      if (cells_far(R, qlo, qhi, lo, hi)) {
+    if (a >= 0 && hascore[a]) {
+      const int64_t first_leaf = m - 1;
+      const float4 qlo = ld_node(nodes, 2 * (first_leaf + a)), qhi = ld_node(nodes, 2 * (first_leaf + a) + 1);
+      const int64_t sa = cell_start[a], ea = cell_end(cell_start, m, n, a);
+      int32_t root = (int32_t)a;
+      int32_t cur = node_rope(qhi);
+      while (cur != kSentinel) {
+        const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+        if (cells_far(R, qlo, qhi, lo, hi)) {
+          cur = node_rope(hi);
+          continue;
+        }
+        if (cur < first_leaf) {
+          cur = node_link(lo);
+          continue;
+        }
+        const int32_t b = (int32_t)(cur - first_leaf);
         cur = node_rope(hi);
-        continue;
-      }
-      if (cur < first_leaf) {
-        cur = node_link(lo);
-        continue;
-      }
-      const int32_t b = (int32_t)(cur - first_leaf);
-      cur = node_rope(hi);
-      if (!hascore[b] || parent[b] == root) continue;
-      const int32_t ra = uf_find(parent, root), rb = uf_find(parent, b);
-      root = ra;
-      if (ra == rb) continue;
-      const int64_t sb = cell_start[b], eb = cell_end(cell_start, m, n, b);
-      bool found = false;
-      for (int64_t i = sa; i < ea && !found; ++i) {
-        if (!corep[i]) continue;
-        const float4 x = cpts[i];
-        for (int64_t j = sb; j < eb; ++j) {
-          if (!corep[j]) continue;
-          const float4 y = cpts[j];
-          ++checks;
-          if (hit_point(R, x.x, x.y, x.z, y.x, y.y, y.z)) {
-            found = true;
-            break;
+        if (!hascore[b] || parent[b] == root) continue;
+        const int32_t ra = uf_find(parent, root), rb = uf_find(parent, b);
+        root = ra;
+        if (ra == rb) continue;
+        const int64_t sb = cell_start[b], eb = cell_end(cell_start, m, n, b);
+        bool found = false;
+        for (int64_t i = sa; i < ea && !found; ++i) {
+          if (!corep[i]) continue;
+          const float4 x = cpts[i];
+          for (int64_t j = sb; j < eb; ++j) {
+            if (!corep[j]) continue;
+            const float4 y = cpts[j];
+            ++checks;
+            if (hit_point(R, x.x, x.y, x.z, y.x, y.y, y.z)) {
+              found = true;
+              break;
+            }
           }
         }
+        if (found) root = uf_union(parent, ra, rb);
       }
-      if (found) root = uf_union(parent, ra, rb);
     }
-  }
   add_checks(checks, checks_total);
 }
 

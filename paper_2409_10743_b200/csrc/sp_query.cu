@@ -222,37 +222,37 @@ __global__ void __launch_bounds__(128) k_range_fill(const float4 *__restrict__ n
                                                     int nslices) {
   SmSliceWalk sw(nq, slices, nslices);  // SM-affine schedule (sp_common.cuh)
   for (int64_t qi; sw.next(qi);) {
-  if (qi < 0) continue;
-  const int64_t q = order[qi];
-  int64_t w = offsets[q];
-  float b[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  float cx = 0.f, cy = 0.f, cz = 0.f;
-  Radius R{0.0, 0.f, 0.f, 0};
-  if (MODE == 1) {
-    const float *p = preds + q * (dim + 1);
-    cx = p[0]; cy = p[1]; cz = dim == 3 ? p[2] : 0.f;
-    R = make_radius(p[dim]);
-  } else {
-    for (int k = 0; k < dim; ++k) {
-      b[k] = preds[q * 2 * dim + k];
-      b[3 + k] = preds[q * 2 * dim + dim + k];
-    }
-  }
-  int32_t cur = 0;
-  while (cur != kSentinel) {
-    const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
-    const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
-    const bool leaf = cur >= n - 1;
-    const bool hit = MODE == 1 ? (leaf ? hit_box(R, cx, cy, cz, lo, hi) : maybe_box(R, cx, cy, cz, lo, hi))
-                               : box_touch(lo, hi, b);
-    if (leaf) {
-      // key = (query << 32) | object; sorting the keys orders each row by object
-      if (hit) keyed[w++] = ((uint64_t)q << 32) | (uint32_t)node_link(lo);
-      cur = node_rope(hi);
+    if (qi < 0) continue;
+    const int64_t q = order[qi];
+    int64_t w = offsets[q];
+    float b[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float cx = 0.f, cy = 0.f, cz = 0.f;
+    Radius R{0.0, 0.f, 0.f, 0};
+    if (MODE == 1) {
+      const float *p = preds + q * (dim + 1);
+      cx = p[0]; cy = p[1]; cz = dim == 3 ? p[2] : 0.f;
+      R = make_radius(p[dim]);
     } else {
-      cur = hit ? node_link(lo) : node_rope(hi);
+      for (int k = 0; k < dim; ++k) {
+        b[k] = preds[q * 2 * dim + k];
+        b[3 + k] = preds[q * 2 * dim + dim + k];
+      }
     }
-  }
+    int32_t cur = 0;
+    while (cur != kSentinel) {
+      const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
+      const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+      const bool leaf = cur >= n - 1;
+      const bool hit = MODE == 1 ? (leaf ? hit_box(R, cx, cy, cz, lo, hi) : maybe_box(R, cx, cy, cz, lo, hi))
+                                 : box_touch(lo, hi, b);
+      if (leaf) {
+        // key = (query << 32) | object; sorting the keys orders each row by object
+        if (hit) keyed[w++] = ((uint64_t)q << 32) | (uint32_t)node_link(lo);
+        cur = node_rope(hi);
+      } else {
+        cur = hit ? node_link(lo) : node_rope(hi);
+      }
+    }
   }
 }
 
