@@ -145,6 +145,7 @@ class Context:
             raise CudaError("sp_ctx_create(device=%d) failed (status %d): no usable CUDA device" % (device, rc))
         self.h = h
         self.device = device
+        self.stream = stream  # the caller's stream handle, or None (own stream)
 
     def close(self):
         if self.h:
@@ -159,6 +160,7 @@ class Context:
 
     def set_stream(self, stream: Optional[int]):
         self._check(_lib.sp_ctx_set_stream(self.h, _stream_arg(stream)))
+        self.stream = stream
 
     def synchronize(self):
         self._check(_lib.sp_ctx_synchronize(self.h))

@@ -70,9 +70,13 @@ def _device_fof(ctx):
 
     def run(points: torch.Tensor, eps: float, gids: torch.Tensor):
         # the torch ops that produced `points` ran on torch's current stream;
-        # a context on another stream must not start before they finish
+        # a context on another stream must not start before they finish (a
+        # context on that same stream is ordered already, and a host wait
+        # there would stop the host from queueing the next step ahead)
         if ctx is not None and points.is_cuda:
-            torch.cuda.current_stream(points.device).synchronize()
+            cur = torch.cuda.current_stream(points.device)
+            if getattr(ctx, "stream", None) is None or int(ctx.stream) != int(cur.cuda_stream):
+                cur.synchronize()
         out = sp.friends_of_friends_ids(points, eps, gids.to(torch.int32).contiguous(), ctx=ctx)
         return out.labels, out.core_flags
 
