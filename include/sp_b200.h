@@ -48,8 +48,13 @@ typedef enum {
 enum { SP_MEM_HOST = 0, SP_MEM_DEVICE = 1 };
 enum { SP_FLAG_ASYNC = 1 };
 
-/* DBSCAN family selector (dbscan.hpp:277-301, 456-504). */
-enum { SP_ALGO_FDBSCAN = 0, SP_ALGO_FOF = 1, SP_ALGO_DENSEBOX = 2 };
+/* DBSCAN family selector (dbscan.hpp:277-301, 456-504).  FDBSCAN and FOF
+ * cluster over grid cells when min_pts = 2; FOF_POINTS is
+ * friends_of_friends by pair traversal over the point hierarchy, the
+ * reference's own algorithm (dbscan.hpp:229-292), with identical results;
+ * DENSEBOX_MIXED is fdbscan_densebox over the reference's mixed tree of dense
+ * cells and sparse points (dbscan.hpp:298-449), equivalent results. */
+enum { SP_ALGO_FDBSCAN = 0, SP_ALGO_FOF = 1, SP_ALGO_DENSEBOX = 2, SP_ALGO_FOF_POINTS = 3, SP_ALGO_DENSEBOX_MIXED = 4 };
 
 /* Range predicate kinds (traversal.hpp:25-28: variant<Sphere, Aabb>). */
 enum { SP_PRED_SPHERE = 0, SP_PRED_BOX = 1 };
@@ -217,6 +222,12 @@ int sp_generate_field(sp_ctx *ctx, int64_t n_total, int64_t first, int64_t count
  * gaussian_clusters(n, dim, k, sigma, extent, seed).  Host memory. */
 int sp_generate_reference(int kind, int64_t n, int dim, int32_t k, double sigma, double extent, uint64_t seed,
                           float *out);
+/* Rows [first, first+count) of the SURVEY §8(d) field H(n_total): the
+ * reference generator's uniform(n_total/4, 3, 1.0, seed 2409) followed by
+ * gaussian_clusters(n_total - n_total/4, 3, max((n_total-n_total/4)/8192, 1),
+ * 0.001*cbrt(2^26/n_total), 1.0, seed 2410), bit-identical to generate()
+ * (generate.cpp:17-66).  Host memory, float[count*3]. */
+int sp_generate_reference_field(int64_t n_total, int64_t first, int64_t count, float *out);
 /* Uniform points in [0,1)^dim from the same Philox stream. */
 int sp_generate_uniform(sp_ctx *ctx, int64_t n, int dim, uint64_t seed, float *out, int mem);
 

@@ -7,6 +7,7 @@
 // restatement in oracle/oracle.cpp, and (b) by bench.py --impl reference and
 // the cpu_baseline leg, to time the reference's own CPU path.
 // ============================================================================
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -183,6 +184,60 @@ int ref_knn(const float *pts, int64_t n, const float *origins, int64_t nq, int32
   });
   double t2 = now_ms();
   if (ms) { ms[0] = t1 - t0; ms[1] = t2 - t1; }
+  return 0;
+}
+
+// friends_of_friends (dbscan.hpp:286-292) on the SURVEY §8(d) field H(n) =
+// U(n/4, 2409) ++ gaussian_clusters(n - n/4, 3, (n - n/4)/8192,
+// 0.001*cbrt(2^26/n), 1, 2410), both drawn by the reference's generate()
+// (generate.cpp), eps = float(0.168*cbrt(1/n)).  Everything stays in this
+// process (no Python copies), so H(2^30) fits a ~200 GB host.  Outputs:
+// out[0..2] = FNV-1a-64 of the points, labels and core flags (SURVEY §8(c)
+// hash); out[3] = the bench checksum sum((label+1) * (i % 65521 + 1)) mod
+// 2^63; cnt[0..2] = clusters, noise, core; secs[0..1] = generate, FoF.
+int ref_fof_field(int64_t n, uint64_t *out, int64_t *cnt, double *secs) {
+  auto fnv = [](const void *data, size_t bytes, uint64_t h) {
+    const unsigned char *b = static_cast<const unsigned char *>(data);
+    for (size_t i = 0; i < bytes; ++i) h = (h ^ b[i]) * 1099511628211ull;
+    return h;
+  };
+  const uint64_t basis = 1469598103934665603ull;
+  double t0 = now_ms();
+  const int64_t nbg = n / 4, nh = n - nbg;
+  std::vector<Point<3>> pts((size_t)n);
+  uint64_t hp = basis;
+  {
+    auto bg = generate(UniformSpec{nbg, 3, 1.0, 2409});
+    std::memcpy(pts.data(), bg.values.data(), (size_t)nbg * 12);
+  }
+  {
+    const int32_t k = (int32_t)std::max<int64_t>(nh / 8192, 1);
+    auto h = generate(GaussianClustersSpec{nh, 3, k, 0.001 * std::cbrt(67108864.0 / (double)n), 1.0, 2410});
+    std::memcpy(pts.data() + nbg, h.values.data(), (size_t)nh * 12);
+  }
+  hp = fnv(pts.data(), (size_t)n * 12, hp);
+  double t1 = now_ms();
+  const float eps = (float)(0.168 * std::cbrt(1.0 / (double)n));
+  DbscanOutput o = friends_of_friends(std::span<const Point<3>>(pts), eps);
+  double t2 = now_ms();
+  out[0] = hp;
+  out[1] = fnv(o.labels.data(), o.labels.size() * 4, basis);
+  out[2] = fnv(o.core_flags.data(), o.core_flags.size(), basis);
+  uint64_t ck = 0;
+  int64_t clusters = 0, noise = 0, core = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t l = o.labels[(size_t)i];
+    ck += (uint64_t)((int64_t)l + 1) * (uint64_t)(i % 65521 + 1);
+    clusters += l == i;
+    noise += l == -1;
+    core += o.core_flags[(size_t)i] != 0;
+  }
+  out[3] = ck & 0x7fffffffffffffffull;
+  cnt[0] = clusters;
+  cnt[1] = noise;
+  cnt[2] = core;
+  secs[0] = (t1 - t0) / 1e3;
+  secs[1] = (t2 - t1) / 1e3;
   return 0;
 }
 

@@ -38,14 +38,14 @@ __all__ = [
     "Bvh", "DbscanOutput", "DbscanParams", "DbscanTimings", "DbscanStats", "InvalidArgument", "CapacityError",
     "CudaError", "range_count", "query_crs", "nearest_query", "pair_traversal", "sort_queries", "morton_codes",
     "fdbscan", "friends_of_friends", "fdbscan_densebox", "adjacency_graph_dbscan", "dbscan_reference",
-    "check_equivalence", "generate_reference_uniform", "generate_reference_gaussian", "generate_field", "generate_uniform",
+    "check_equivalence", "generate_reference_uniform", "generate_reference_gaussian", "generate_reference_field", "generate_field", "generate_uniform",
     "Context",
     "default_context", "library_path",
 ]
 
 SP_OK, SP_EINVAL, SP_ECAPACITY, SP_ECUDA, SP_ENOMEM, SP_ENCCL = range(6)
 SP_MEM_HOST, SP_MEM_DEVICE = 0, 1
-SP_ALGO_FDBSCAN, SP_ALGO_FOF, SP_ALGO_DENSEBOX = 0, 1, 2
+SP_ALGO_FDBSCAN, SP_ALGO_FOF, SP_ALGO_DENSEBOX, SP_ALGO_FOF_POINTS, SP_ALGO_DENSEBOX_MIXED = 0, 1, 2, 3, 4
 SP_PRED_SPHERE, SP_PRED_BOX = 0, 1
 kNoiseLabel = -1
 
@@ -104,6 +104,7 @@ def _load() -> C.CDLL:
         "sp_dbscan_adjacency": (C.c_int, [vp, vp, i64, C.c_int, f32, C.c_int, i64, vp, vp, vp, C.c_int]),
         "sp_check_equivalence": (C.c_int, [vp, vp, i64, C.c_int, f32, vp, vp, vp, vp, C.POINTER(i64),
                                            C.POINTER(C.c_int), C.c_int]),
+        "sp_generate_reference_field": (C.c_int, [i64, i64, i64, vp]),
         "sp_generate_field": (C.c_int, [vp, i64, i64, i64, C.c_uint64, vp, C.c_int]),
         "sp_generate_uniform": (C.c_int, [vp, i64, C.c_int, C.c_uint64, vp, C.c_int]),
     }
@@ -194,14 +195,30 @@ class Context:
         raise CudaError("status %d: %s" % (rc, msg))
 
 
-_default: Optional[Context] = None
+_defaults: dict = {}
 
 
-def default_context() -> Context:
-    global _default
-    if _default is None:
-        _default = Context(0)
-    return _default
+def _device_of(a):
+    """(device, stream) for the implicit context of a call on `a`: a CUDA
+    tensor runs on its device and on torch's current stream there (so the call
+    is ordered after the torch work that produced it); host arrays use device
+    0 and a context-owned stream."""
+    if _is_cuda(a):
+        import torch
+        d = int(a.device.index if a.device.index is not None else torch.cuda.current_device())
+        return d, int(torch.cuda.current_stream(d).cuda_stream)
+    return 0, None
+
+
+def default_context(device=0, stream: Optional[int] = None) -> Context:
+    """The process-wide context of (device, stream), made on first use;
+    `device` may also be a (device, stream) pair from _device_of."""
+    if isinstance(device, tuple):
+        device, stream = device
+    key = (device, stream)
+    if key not in _defaults:
+        _defaults[key] = Context(device, stream=stream)
+    return _defaults[key]
 
 
 # ---- array plumbing -----------------------------------------------------------
@@ -275,7 +292,7 @@ class Bvh:
 
         objects: (n, d) points (point boxes) or (n, 2, d) / (n, 2d) boxes with
         points=False.  Raises InvalidArgument on non-finite coordinates."""
-        ctx = ctx or default_context()
+        ctx = ctx or default_context(_device_of(objects))
         shape = tuple(objects.shape)
         if points is None:
             points = len(shape) == 2
@@ -410,6 +427,11 @@ def range_count(bvh: Bvh, predicates, kind: str = "sphere", cap: int = 0, radius
     optional int32 (nq,) buffer to write the counts into (returned)."""
     ctx = bvh.ctx
     nq = int(predicates.shape[0])
+    d = bvh.dim
+    want = d if radius is not None else (2 * d if kind == "box" else d + 1)
+    if len(predicates.shape) != 2 or int(predicates.shape[1]) != want:
+        raise InvalidArgument("predicates must have shape (nq, %d) for kind=%r%s" %
+                              (want, kind, " with radius" if radius is not None else ""))
     p, mem, keep = _in(predicates, np.float32)
     dev = mem == SP_MEM_DEVICE
     if out is not None:
@@ -430,6 +452,9 @@ def query_crs(bvh: Bvh, predicates, kind: str = "sphere", max_total_matches: Opt
     ctx = bvh.ctx
     preds = np.ascontiguousarray(predicates, np.float32)
     nq = preds.shape[0]
+    want = 2 * bvh.dim if kind == "box" else bvh.dim + 1
+    if preds.ndim != 2 or preds.shape[1] != want:
+        raise InvalidArgument("predicates must have shape (nq, %d) for kind=%r" % (want, kind))
     k = SP_PRED_BOX if kind == "box" else SP_PRED_SPHERE
     offsets = np.empty(nq + 1, np.int64)
     pv = preds.ctypes.data_as(C.c_void_p)
@@ -450,6 +475,8 @@ def nearest_query(bvh: Bvh, origins, k: int, with_distances: bool = False, out=N
     (nq, k) int32 index buffer, or (indices, distances) with with_distances."""
     ctx = bvh.ctx
     nq = int(origins.shape[0])
+    if len(origins.shape) != 2 or int(origins.shape[1]) != bvh.dim:
+        raise InvalidArgument("origins must have shape (nq, %d)" % bvh.dim)
     kk = max(int(k), 0)
     p, mem, keep = _in(origins, np.float32)
     dev = mem == SP_MEM_DEVICE
@@ -487,7 +514,7 @@ def pair_traversal(bvh: Bvh, eps: float) -> np.ndarray:
 
 def sort_queries(points, ctx: Optional[Context] = None):
     """sort_queries over point representatives (traversal.hpp:209-218)."""
-    ctx = ctx or default_context()
+    ctx = ctx or default_context(_device_of(points))
     dim = _dim_of(points)
     n = int(points.shape[0])
     p, mem, keep = _in(points, np.float32)
@@ -499,7 +526,7 @@ def sort_queries(points, ctx: Optional[Context] = None):
 
 def morton_codes(objects, width: int = 64, points: bool = True, ctx: Optional[Context] = None):
     """code_of(centroid(object), scene) for every object (morton.hpp:106-109)."""
-    ctx = ctx or default_context()
+    ctx = ctx or default_context(_device_of(objects))
     arr = np.ascontiguousarray(objects, np.float32)
     n = arr.shape[0]
     dim = arr.shape[1] if points else arr.shape[1] // 2
@@ -543,17 +570,15 @@ class DbscanOutput:
 
 
 def _dbscan(points, eps, min_pts, algo, width, ctx, out=None):
-    ctx = ctx or default_context()
+    ctx = ctx or default_context(_device_of(points))
     dim = _dim_of(points)
     n = int(points.shape[0])
     p, mem, keep = _in(points, np.float32)
     dev = mem == SP_MEM_DEVICE
     if out is not None:
-        labels, core = out
-        if _is_cuda(labels) != dev or _is_cuda(core) != dev:
-            # one memory-space flag covers every pointer of the call (sp_b200.h)
-            raise ValueError("out arrays must live in the same memory space as the points")
-        lp, cp = _ptr(labels), _ptr(core)
+        # one memory-space flag covers every pointer of the call (sp_b200.h)
+        labels, lp = _given_out(out[0], (n,), 4, dev)
+        core, cp = _given_out(out[1], (n,), 1, dev)
     else:
         labels, lp = _out(dev, (n,), np.int32, _torch_dtype("int32") if dev else None, points.device if dev else None)
         core, cp = _out(dev, (n,), np.uint8, _torch_dtype("uint8") if dev else None, points.device if dev else None)
@@ -569,9 +594,14 @@ def fdbscan(points, params: DbscanParams, width: int = 64, ctx: Optional[Context
     return _dbscan(points, params.eps, params.min_pts, SP_ALGO_FDBSCAN, width, ctx, out)
 
 
-def friends_of_friends(points, eps: float, width: int = 64, ctx: Optional[Context] = None, out=None) -> DbscanOutput:
-    """friends_of_friends (dbscan.hpp:286-292): FDBSCAN with min_pts = 2."""
-    return _dbscan(points, eps, 2, SP_ALGO_FOF, width, ctx, out)
+def friends_of_friends(points, eps: float, width: int = 64, ctx: Optional[Context] = None, out=None,
+                       algorithm: str = "cells") -> DbscanOutput:
+    """friends_of_friends (dbscan.hpp:286-292): FDBSCAN with min_pts = 2.
+    algorithm="cells" (default) clusters over grid cells (DESIGN.md §3.5);
+    "points" runs the reference's own pair traversal over the point
+    hierarchy.  Both give identical labels and core flags."""
+    algo = {"cells": SP_ALGO_FOF, "points": SP_ALGO_FOF_POINTS}[algorithm]
+    return _dbscan(points, eps, 2, algo, width, ctx, out)
 
 
 def friends_of_friends_ids(points, eps: float, ids, ctx: Optional[Context] = None, out=None):
@@ -579,17 +609,19 @@ def friends_of_friends_ids(points, eps: float, ids, ctx: Optional[Context] = Non
     cluster (-1 = noise) instead of the smallest index: the per-slab step of the
     multi-GPU FoF, which passes global indices (sp_fof_ids).  ids: int32, one
     per point, distinct, >= 0, in the same memory space as the points."""
-    ctx = ctx or default_context()
+    ctx = ctx or default_context(_device_of(points))
     dim = _dim_of(points)
     n = int(points.shape[0])
     p, mem, keep = _in(points, np.float32)
     dev = mem == SP_MEM_DEVICE
     if _is_cuda(ids) != dev:
         raise ValueError("ids must live in the same memory space as the points")
+    if tuple(ids.shape) != (n,):
+        raise InvalidArgument("ids must have shape (n,)")
     ip, _, keep_ids = _in(ids, np.int32)
     if out is not None:
-        labels, core = out
-        lp, cp = _ptr(labels), _ptr(core)
+        labels, lp = _given_out(out[0], (n,), 4, dev)
+        core, cp = _given_out(out[1], (n,), 1, dev)
     else:
         labels, lp = _out(dev, (n,), np.int32, _torch_dtype("int32") if dev else None, points.device if dev else None)
         core, cp = _out(dev, (n,), np.uint8, _torch_dtype("uint8") if dev else None, points.device if dev else None)
@@ -598,9 +630,12 @@ def friends_of_friends_ids(points, eps: float, ids, ctx: Optional[Context] = Non
 
 
 def fdbscan_densebox(points, params: DbscanParams, width: int = 64, ctx: Optional[Context] = None,
-                     out=None) -> DbscanOutput:
-    """fdbscan_densebox (dbscan.hpp:298-449)."""
-    return _dbscan(points, params.eps, params.min_pts, SP_ALGO_DENSEBOX, width, ctx, out)
+                     out=None, algorithm: str = "cells") -> DbscanOutput:
+    """fdbscan_densebox (dbscan.hpp:298-449).  algorithm="cells" (default)
+    runs the all-cells pipeline; "mixed" the reference's
+    mixed tree of dense cells and sparse points.  Equivalent clusterings."""
+    algo = {"cells": SP_ALGO_DENSEBOX, "mixed": SP_ALGO_DENSEBOX_MIXED}[algorithm]
+    return _dbscan(points, params.eps, params.min_pts, algo, width, ctx, out)
 
 
 def adjacency_graph_dbscan(points, eps: float, width: int = 64, max_adjacency: Optional[int] = None,
@@ -608,7 +643,7 @@ def adjacency_graph_dbscan(points, eps: float, width: int = 64, max_adjacency: O
     """adjacency_graph_dbscan (dbscan.hpp:456-504): the historical baseline
     that materialises the neighbour CRS; raises CapacityError past
     max_adjacency."""
-    ctx = ctx or default_context()
+    ctx = ctx or default_context(_device_of(points))
     dim = _dim_of(points)
     n = int(points.shape[0])
     p, mem, keep = _in(points, np.float32)
@@ -624,7 +659,7 @@ def adjacency_graph_dbscan(points, eps: float, width: int = 64, max_adjacency: O
 def dbscan_reference(points, params: DbscanParams, ctx: Optional[Context] = None) -> DbscanOutput:
     """dbscan_reference (dbscan.hpp:188-222): brute-force O(n^2) DBSCAN on the
     device, independent of the tree (for verification of small inputs)."""
-    ctx = ctx or default_context()
+    ctx = ctx or default_context(_device_of(points))
     dim = _dim_of(points)
     n = int(points.shape[0])
     p, mem, keep = _in(points, np.float32)
@@ -651,10 +686,26 @@ def generate_reference_gaussian(n: int, dim: int, k: int, sigma: float, extent: 
     return out[: n * dim].reshape(n, dim)
 
 
+def generate_reference_field(n_total: int, first: int = 0, count: Optional[int] = None, out=None):
+    """Rows [first, first+count) of the SURVEY §8(d) field H(n_total), drawn
+    exactly as the reference's generate() draws them (generate.cpp:17-66):
+    25% uniform background (seed 2409) then Gaussian halos of 8192 points
+    (seed 2410).  Host memory: a numpy array, or `out` (e.g. a pinned CPU
+    tensor of shape (count, 3), float32)."""
+    count = n_total - first if count is None else count
+    if out is None:
+        out = np.empty((max(count, 0), 3), np.float32)
+    if tuple(out.shape) != (count, 3) or _is_cuda(out):
+        raise ValueError("out must be a host (count, 3) float32 array")
+    if _lib.sp_generate_reference_field(n_total, first, count, _ptr(out)) != SP_OK:
+        raise InvalidArgument("generate: bad field slice")
+    return out
+
+
 def check_equivalence(points, eps: float, got: DbscanOutput, want: DbscanOutput, ctx: Optional[Context] = None):
     """check_equivalence (verify.hpp:21-61): None when equivalent, else a
     message naming the first violating point."""
-    ctx = ctx or default_context()
+    ctx = ctx or default_context(_device_of(points))
     dim = _dim_of(points)
     n = int(points.shape[0])
     p, mem, keep = _in(points, np.float32)

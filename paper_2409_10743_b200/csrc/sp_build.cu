@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <mutex>
 #include <cstdlib>
 
 #include "sp_common.cuh"
@@ -506,30 +507,32 @@ void onesweep_passes(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_a
                      int npass, bool vals_iota) {
   constexpr int TILE = THREADS * ITEMS;
   constexpr size_t SMEM = rs_smem_bytes<ITEMS, THREADS>();
-  static bool attr_set = false;
-  if (!attr_set) {
-    SPB_CUDA(cudaFuncSetAttribute(k_rs_onesweep<ITEMS, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)SMEM));
-    attr_set = true;
+  // the dynamic shared-memory opt-in is per device (and per kernel)
+  static std::mutex mu;
+  static uint64_t opted = 0;  // bit d: set on device d
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (c.device >= 64 || !((opted >> c.device) & 1)) {
+      SPB_CUDA(cudaFuncSetAttribute(k_rs_onesweep<ITEMS, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)SMEM));
+      if (c.device < 64) opted |= 1ull << c.device;
+    }
   }
   const int64_t ntiles = (n + TILE - 1) / TILE;
   DevBuf<uint32_t> hist((size_t)npass * RS_BINS + npass, c.stream);
   DevBuf<unsigned long long> lookback((size_t)ntiles * RS_BINS, c.stream);
   SPB_CUDA(cudaMemsetAsync(hist.get(), 0, hist.n * sizeof(uint32_t), c.stream));
   SPB_CUDA(cudaMemsetAsync(lookback.get(), 0, lookback.n * sizeof(unsigned long long), c.stream));
-  if (getenv("SPB_SORT_MARKS")) mark(c, "sort_setup");
   k_rs_hist<<<grid_for(n, 256, 148 * 4), 256, 0, c.stream>>>(*keys, n, npass, hist.get());
   SPB_LAUNCHED();
   k_rs_scan<<<npass, RS_BINS, 0, c.stream>>>(hist.get());
   SPB_LAUNCHED();
-  if (getenv("SPB_SORT_MARKS")) mark(c, "sort_hist");
   uint32_t *ctr = hist.get() + (size_t)npass * RS_BINS;
   for (int p = 0; p < npass; ++p) {
     k_rs_onesweep<ITEMS, THREADS><<<(unsigned)ntiles, THREADS, SMEM, c.stream>>>(
         *keys, (p == 0 && vals_iota) ? nullptr : *vals, *keys_alt, *vals_alt, n, 8 * p,
         hist.get() + (size_t)p * RS_BINS, lookback.get(), ctr + p, (uint32_t)(2 * p + 1));
     SPB_LAUNCHED();
-    if (getenv("SPB_SORT_MARKS")) mark(c, "sort_pass");
     std::swap(*keys, *keys_alt);
     std::swap(*vals, *vals_alt);
   }
@@ -594,12 +597,13 @@ __device__ __forceinline__ bool climb(const HierView &H, int64_t &l, int64_t &r,
   for (int level = 0; level < max_levels; ++level) {
     const bool L = H.is_left(l, r);
     const int64_t a = L ? r : l - 1;  // the parent's split position
-    // Release-exchange: this node's box stores are performed before the flag
-    // changes hands.  The second arrival reads the sibling box with L2-coherent
-    // loads whose addresses depend on the exchanged value, so no acquire
-    // fence (and no L1 invalidation) is needed.
+    // Acquire-release exchange: the release half orders this node's box
+    // stores before the flag changes hands; the acquire half orders the second
+    // arrival's reads of the sibling box after the first arrival's stores (the
+    // PTX memory model gives no ordering through the address dependency
+    // alone).  The sibling box is read with L2-coherent loads.
     int32_t other;
-    asm volatile("atom.release.gpu.global.exch.b32 %0, [%1], %2;"
+    asm volatile("atom.acq_rel.gpu.global.exch.b32 %0, [%1], %2;"
                  : "=r"(other)
                  : "l"(flags + a), "r"((int32_t)(L ? l : r))
                  : "memory");

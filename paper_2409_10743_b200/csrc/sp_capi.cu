@@ -39,47 +39,6 @@ void stream_after(cudaStream_t waiter, cudaStream_t producer) {
   SPB_CUDA(cudaEventDestroy(e));
 }
 
-// SPB_DEBUG_E2E=1: timestamp the copies and the compute of every call with
-// events and print the timeline at sp_ctx_synchronize (pipeline diagnostics).
-struct TraceEv {
-  const char *what;
-  int64_t call;
-  cudaEvent_t e;
-};
-std::vector<TraceEv> &trace() {
-  static std::vector<TraceEv> t;
-  return t;
-}
-std::mutex &trace_mu() {
-  static std::mutex mu;
-  return mu;
-}
-bool tracing() {
-  static const bool on = getenv("SPB_DEBUG_E2E") != nullptr;
-  return on;
-}
-void trace_ev(spb::Ctx &c, const char *what, cudaStream_t s) {
-  if (!tracing()) return;
-  cudaEvent_t e;
-  cudaEventCreate(&e);
-  cudaEventRecord(e, s);
-  std::lock_guard<std::mutex> g(trace_mu());
-  trace().push_back({what, c.calls, e});
-}
-void trace_dump() {
-  if (!tracing()) return;
-  std::lock_guard<std::mutex> g(trace_mu());
-  if (trace().empty()) return;
-  cudaEvent_t t0 = trace().front().e;
-  for (auto &t : trace()) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, t0, t.e);
-    fprintf(stderr, "[e2e] call %lld %-12s %9.2f ms\n", (long long)t.call, t.what, ms);
-  }
-  for (auto &t : trace()) cudaEventDestroy(t.e);
-  trace().clear();
-}
-
 spb::Ctx::Staging &stage(spb::Ctx &c, bool input, size_t bytes) {
   const int parity = (int)(c.calls & 1);
   int &used = input ? c.in_used : c.out_used;
@@ -115,11 +74,8 @@ struct In {
     st = &stage(c, true, count * sizeof(T));
     ctx = &c;
     SPB_CUDA(cudaStreamWaitEvent(c.h2d, st->done, 0));
-    trace_ev(c, "h2d begin", c.h2d);
     SPB_CUDA(cudaMemcpyAsync(st->p, src, count * sizeof(T), cudaMemcpyHostToDevice, c.h2d));
-    trace_ev(c, "h2d end", c.h2d);
     stream_after(c.stream, c.h2d);
-    trace_ev(c, "compute go", c.stream);
     p = static_cast<const T *>(st->p);
   }
   ~In() {
@@ -149,11 +105,8 @@ struct Out {
   }
   void flush(spb::Ctx &c) {
     if (!host) return;
-    trace_ev(c, "compute end", c.stream);
     stream_after(c.d2h, c.stream);
-    trace_ev(c, "d2h begin", c.d2h);
     SPB_CUDA(cudaMemcpyAsync(host, st->p, count * sizeof(T), cudaMemcpyDeviceToHost, c.d2h));
-    trace_ev(c, "d2h end", c.d2h);
     SPB_CUDA(cudaEventRecord(st->done, c.d2h));
   }
 };
@@ -313,7 +266,6 @@ int sp_ctx_set_stream(sp_ctx *ctx, void *stream) {
 int sp_ctx_synchronize(sp_ctx *ctx) {
   return guarded(ctx, [&](spb::Ctx &c) {
     sync_all(c);
-    trace_dump();
     int err = 0;
     SPB_CUDA(cudaMemcpy(&err, c.d_err, sizeof(int), cudaMemcpyDeviceToHost));
     if (err) {
@@ -586,7 +538,7 @@ int sp_dbscan(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, i
               int code_width, int32_t *labels, uint8_t *core, sp_timings *timings, sp_stats *stats, int mem) {
   return guarded(ctx, [&](spb::Ctx &c) {
     check_dim(dim);
-    if (algo < 0 || algo > 2) throw spb::InvalidArgument("unknown algorithm");
+    if (algo < 0 || algo > 4) throw spb::InvalidArgument("unknown algorithm");
     if (code_width != 32 && code_width != 64) throw spb::InvalidArgument("code width must be 32 or 64");
     if (n < 0 || n > (1LL << 30)) throw spb::InvalidArgument("point count out of range");
     In<float> p(c, points, (size_t)n * dim, mem);

@@ -187,19 +187,23 @@ __global__ void __launch_bounds__(256) k_final_labels(int64_t n, const int32_t *
 void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t min_pts, int algo, int width,
             int32_t *labels, uint8_t *core, DbscanResult *res, const int32_t *ids) {
   if (!(eps > 0.f) || !std::isfinite(eps)) throw InvalidArgument("dbscan: eps must be positive and finite");
-  if (algo == 1) min_pts = 2;
+  // algo: 0 fdbscan, 1 friends_of_friends, 2 fdbscan_densebox (sp_b200.h
+  // SP_ALGO_*); 3 friends_of_friends by pair traversal over the point
+  // hierarchy (the reference's own algorithm, no grid); 4 fdbscan_densebox
+  // over the reference's mixed tree of dense cells and sparse points.
+  if (algo == 1 || algo == 3) min_pts = 2;
   if (min_pts < 2) throw InvalidArgument("dbscan: min_pts must be at least 2");
   if (n == 0) return;
-  if (min_pts == 2 && !getenv("SPB_FOF_POINTS")) {
+  if (min_pts == 2 && (algo == 0 || algo == 1)) {
     // friends-of-friends over grid cells (the DenseBox shortcut)
     extern bool fof_cells(Ctx &, const float *, int64_t, int, float, int32_t *, uint8_t *, DbscanResult *,
                           const int32_t *);
-    if (algo != 2 && fof_cells(c, points, n, dim, eps, labels, core, res, ids)) return;
+    if (fof_cells(c, points, n, dim, eps, labels, core, res, ids)) return;
   }
-  if (algo == 2) {
+  if (algo == 2 || algo == 4) {
     extern void densebox(Ctx &, const float *, int64_t, int, float, int32_t, int, int32_t *, uint8_t *,
-                         DbscanResult *);
-    densebox(c, points, n, dim, eps, min_pts, width, labels, core, res);
+                         DbscanResult *, bool);
+    densebox(c, points, n, dim, eps, min_pts, width, labels, core, res, algo == 2);
     return;
   }
   cudaEvent_t ev[5];
@@ -226,7 +230,7 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
   DevBuf<uint32_t> claims(count_phase ? (size_t)((n + 31) / 32) : 0, c.stream);
   // both walks run on the SM-affine schedule (sp_common.cuh)
   if (count_phase) {
-    SmSlices sl(c, n);
+    SmSlices sl(c);
     auto kern = R.fast ? k_core_flags<true> : k_core_flags<false>;
     kern<<<sl.grid(kern, 128), 128, 0, c.stream>>>(t.nodes, t.leafpt, n, R, min_pts, corep.get(), sl.ctr.get(),
                                                    sl.nsm);
@@ -239,7 +243,7 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
   k_iota<<<grid_for(n, 256, 148 * 16), 256, 0, c.stream>>>(parent.get(), n);
   SPB_LAUNCHED();
   {
-    SmSlices sl(c, n);
+    SmSlices sl(c);
     if (count_phase) SPB_CUDA(cudaMemsetAsync(claims.get(), 0, claims.n * sizeof(uint32_t), c.stream));
     auto kern = count_phase ? (R.fast ? k_merge_pairs<false, true> : k_merge_pairs<false, false>)
                             : (R.fast ? k_merge_pairs<true, true> : k_merge_pairs<true, false>);

@@ -40,22 +40,11 @@ namespace spb {
 
 namespace {
 
-// Host synchronisation point; SPB_DEBUG_SYNC=1 logs the host time spent before
-// and inside each wait (diagnostics for idle gaps between phases).
+// Host synchronisation point (the few phases that size a buffer from a
+// device count).
 void host_sync(Ctx &c, int line) {
-  static const bool dbg = getenv("SPB_DEBUG_SYNC") != nullptr;
-  if (!dbg) {
-    SPB_CUDA(cudaStreamSynchronize(c.stream));
-    return;
-  }
-  static auto last = std::chrono::steady_clock::now();
-  const auto t0 = std::chrono::steady_clock::now();
+  (void)line;
   SPB_CUDA(cudaStreamSynchronize(c.stream));
-  const auto t1 = std::chrono::steady_clock::now();
-  fprintf(stderr, "[sync line %d] host-before %.2f ms wait %.2f ms\n", line,
-          std::chrono::duration<double, std::milli>(t0 - last).count(),
-          std::chrono::duration<double, std::milli>(t1 - t0).count());
-  last = t1;
 }
 
 __device__ __forceinline__ uint64_t spread3_21(uint64_t v) {
@@ -815,7 +804,8 @@ __global__ void __launch_bounds__(256) k_fof_core_from_labels(int64_t n, const i
                                                               uint8_t *__restrict__ core) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
-    if (i + 4 <= n && ((reinterpret_cast<uintptr_t>(labels + i) | reinterpret_cast<uintptr_t>(core + i)) & 3) == 0) {
+    if (i + 4 <= n && (reinterpret_cast<uintptr_t>(labels + i) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(core + i) & 3) == 0) {
       const int4 l = *reinterpret_cast<const int4 *>(labels + i);
       const uint32_t packed = (uint32_t)(l.x >= 0) | ((uint32_t)(l.y >= 0) << 8) | ((uint32_t)(l.z >= 0) << 16) |
                               ((uint32_t)(l.w >= 0) << 24);
@@ -835,8 +825,8 @@ bool dbscan_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32
 // applies; otherwise the reference's mixed tree of dense cells and sparse
 // points below.
 void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t min_pts, int width, int32_t *labels,
-              uint8_t *core_out, DbscanResult *res) {
-  if (!getenv("SPB_DENSEBOX_OBJECTS") && dbscan_cells(c, pts, n, dim, eps, min_pts, labels, core_out, res)) return;
+              uint8_t *core_out, DbscanResult *res, bool cells) {
+  if (cells && dbscan_cells(c, pts, n, dim, eps, min_pts, labels, core_out, res)) return;
   cudaEvent_t ev[5];
   for (auto &e : ev) SPB_CUDA(cudaEventCreate(&e));
   SPB_CUDA(cudaEventRecord(ev[0], c.stream));
@@ -1113,9 +1103,6 @@ bool build_cell_grid(Ctx &c, const float *pts, int64_t n, int dim, float eps, Ce
     SPB_LAUNCHED();
     peek(c, {{total.get(), &m, sizeof(int64_t)}});
   }
-  if (getenv("SPB_DEBUG_PEEK"))
-    fprintf(stderr, "[grid] n %lld scene %g %g %g .. %g %g %g bits %d cells %lld\n", (long long)n, hs[0], hs[1], hs[2],
-            hs[3], hs[4], hs[5], bits, (long long)m);
   g.m = m;
   DevBuf<int32_t> delta(m > 1 ? m - 1 : 1, c.stream);
   DevBuf<float> boxes((size_t)m * 2 * dim, c.stream);
@@ -1155,7 +1142,7 @@ bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t 
   {
     const Radius R = make_radius(eps);
     if (SPB_MERGE_SM && m >= SPB_SM_MIN_ITEMS) {
-      SmSlices sl(c, m);
+      SmSlices sl(c);
       if (R.fast)
         k_fof_cells_merge_sm<true><<<sl.grid(k_fof_cells_merge_sm<true>, 128), 128, 0, c.stream>>>(
             g.t.nodes, m, g.cell_start.get(), n, g.cpts.get(), R, parent.get(), sl.ctr.get(), sl.nsm);
@@ -1479,7 +1466,7 @@ bool dbscan_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32
   SPB_CUDA(cudaEventRecord(ev[1], c.stream));
   DevBuf<uint8_t> corep((size_t)n, c.stream), hascore((size_t)m, c.stream);
   {
-    SmSlices sl(c, n);
+    SmSlices sl(c);
     auto kern = R.fast ? k_cells_core<true> : k_cells_core<false>;
     kern<<<sl.grid(kern, 128), 128, 0, c.stream>>>(g.t.nodes, m, g.cell_start.get(), n, g.cell_of.get(), g.cpts.get(),
                                                    R, min_pts, corep.get(), sl.ctr.get(), sl.nsm);
@@ -1493,7 +1480,7 @@ bool dbscan_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32
   k_iota32<<<Gm, 256, 0, c.stream>>>(parent.get(), m);
   SPB_LAUNCHED();
   {
-    SmSlices sl(c, m);
+    SmSlices sl(c);
     auto kern = R.fast ? k_cells_core_merge<true> : k_cells_core_merge<false>;
     kern<<<sl.grid(kern, 128), 128, 0, c.stream>>>(g.t.nodes, m, g.cell_start.get(), n, g.cpts.get(), corep.get(),
                                                    hascore.get(), R, parent.get(), st.get() + 2, sl.ctr.get(), sl.nsm);

@@ -169,8 +169,7 @@ int resident_blocks(const void *kernel, int threads);
 struct SmSlices {
   int nsm = 0;
   DevBuf<unsigned long long> ctr;
-  SmSlices(Ctx &c, int64_t total) {
-    (void)total;
+  explicit SmSlices(Ctx &c) {
     nsm = sm_count(c.device);
     ctr = DevBuf<unsigned long long>((size_t)nsm, c.stream);
     SPB_CUDA(cudaMemsetAsync(ctr.get(), 0, (size_t)nsm * sizeof(unsigned long long), c.stream));

@@ -38,7 +38,6 @@ __global__ void k_representatives(const float *__restrict__ preds, int64_t nq, i
 
 void query_order(Ctx &c, const float *preds, int64_t nq, int dim, int kind, int32_t *order) {
   if (nq <= 0) return;
-  if (kind == 0 && false) return;
   DevBuf<float> reps((size_t)nq * dim, c.stream);
   k_representatives<<<grid_for(nq, 256, 148 * 16), 256, 0, c.stream>>>(preds, nq, dim, kind, reps.get());
   SPB_LAUNCHED();
@@ -122,7 +121,7 @@ void range_count(Ctx &c, const Tree &t, int kind, const float *preds, int64_t nq
   }
   const Radius R = make_radius(radius);
   const int mode = kind == RQ_RADIUS ? (R.fast ? 3 : 0) : (kind == RQ_SPHERES ? 1 : 2);
-  SmSlices sl(c, nq);
+  SmSlices sl(c);
   auto launch = [&](auto kern) {
     kern<<<sl.grid(kern, 512), 512, 0, c.stream>>>(t.nodes, t.leafpt, t.n, preds, t.dim, ord, nq, R, cap, counts,
                                                    sl.ctr.get(), sl.nsm);
@@ -277,7 +276,7 @@ int64_t range_crs(Ctx &c, const Tree &t, int kind, const float *preds, int64_t n
   if (total == 0 || t.n == 0) return total;
   DevBuf<uint64_t> k0((size_t)total, c.stream), k1((size_t)total, c.stream);
   DevBuf<uint32_t> v0((size_t)total, c.stream), v1((size_t)total, c.stream);
-  SmSlices sl(c, nq);
+  SmSlices sl(c);
   if (kind == RQ_SPHERES)
     k_range_fill<1><<<sl.grid(k_range_fill<1>, 128), 128, 0, c.stream>>>(t.nodes, t.n, preds, t.dim, order.get(), nq,
                                                                          offsets, k0.get(), sl.ctr.get(), sl.nsm);

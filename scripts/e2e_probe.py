@@ -20,7 +20,7 @@ for mode in ("sync", "async"):
         sp.friends_of_friends(hp, eps, ctx=c2, out=(hl, hc))
     c2.synchronize()
     torch.cuda.synchronize()
-    print(os.environ.get("SPB_FOF_POINTS", "cells"), mode, "%.1f ms/step" % ((time.perf_counter() - t) / 5 * 1e3))
+    print("cells", mode, "%.1f ms/step" % ((time.perf_counter() - t) / 5 * 1e3))
     c2.set_async(False)
 t = time.perf_counter()
 x = hp.cuda(); torch.cuda.synchronize(); print("h2d %.1f ms" % ((time.perf_counter() - t) * 1e3))

@@ -1,5 +1,5 @@
 """1.07 B-point FoF on one B200: the grid-cell pipeline against the point
-pipeline (pair traversal over the point LBVH, SPB_FOF_POINTS) on the same
+pipeline (pair traversal over the point LBVH, algorithm="points") on the same
 input — two independent algorithms must give bit-identical labels and core
 flags.  (The CPU reference cannot run at this size here: ~165 GB of RAM.)"""
 import sys, os, time
@@ -14,14 +14,11 @@ labels = torch.empty(n, dtype=torch.int32, device="cuda")
 core = torch.empty(n, dtype=torch.uint8, device="cuda")
 res = {}
 for mode in ("cells", "points"):
-    if mode == "points":
-        os.environ["SPB_FOF_POINTS"] = "1"
     torch.cuda.synchronize(); t = time.perf_counter()
-    sp.friends_of_friends(p, eps, ctx=ctx, out=(labels, core))
+    sp.friends_of_friends(p, eps, ctx=ctx, out=(labels, core), algorithm=mode)
     torch.cuda.synchronize(); dt = time.perf_counter() - t
     res[mode] = (labels.cpu().numpy(), core.cpu().numpy())
     print(mode, "%.1f ms" % (dt * 1e3), [(k, round(v, 1)) for k, v in ctx.phases()], flush=True)
-    ctx.close() if False else None
 same = np.array_equal(res["cells"][0], res["points"][0]) and np.array_equal(res["cells"][1], res["points"][1])
 lab, core = res["cells"]
 print("n=%d eps=%r: labels and core flags identical between the two pipelines: %s; clusters %d, core %d, noise %d"

@@ -73,7 +73,6 @@ def test_fof_cells_equal_point_pipeline(sp, shape, mult):
     # (pair traversal over the point LBVH), on 2^20 points of several shapes
     # and eps from 0.05x to 3x the mean spacing: labels and core flags must be
     # bit-identical.
-    import os
     import torch
     n = 1 << 20
     g = torch.Generator().manual_seed(["uniform", "field", "plane", "line", "shell", "dups"].index(shape) * 10 +
@@ -98,10 +97,6 @@ def test_fof_cells_equal_point_pipeline(sp, shape, mult):
         ((1.0 / n) ** 0.5 if shape == "plane" else 1.0 / n)
     eps = float(np.float32(mult * spacing))
     a = sp.friends_of_friends(p, eps)
-    os.environ["SPB_FOF_POINTS"] = "1"
-    try:
-        b = sp.friends_of_friends(p, eps)
-    finally:
-        del os.environ["SPB_FOF_POINTS"]
+    b = sp.friends_of_friends(p, eps, algorithm="points")
     assert torch.equal(a.labels, b.labels), (shape, mult)
     assert torch.equal(a.core_flags, b.core_flags), (shape, mult)
