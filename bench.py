@@ -3,10 +3,14 @@
 "FoF/DBSCAN points/sec at 1/2/4/8 B200 + % HBM roofline; BVH build Mpts/s").
 
 Default workload ("fof_field", SURVEY §8(d) C5 shape, weak scaling):
-friends-of-friends (DBSCAN minPts = 2) on a HACC-like clustered 3-D fp32 field
-— 25% uniform background + Gaussian halos of 8192 points, sigma =
-0.001*cbrt(2^26/n) — with 2^27 points per GPU (the per-GPU share of the C5
-1-billion-point run on 8 GPUs), eps = 0.168 * mean spacing of the whole field.
+friends-of-friends (DBSCAN minPts = 2) on the SURVEY field H(n_total) — 25%
+uniform background + Gaussian halos of 8192 points, sigma =
+0.001*cbrt(2^26/n), drawn by the reference's own generator (generate.cpp,
+bit-identical host restatement) — with 2^27 points per GPU (the per-GPU share
+of the C5 1-billion-point run on 8 GPUs), eps = 0.168 * mean spacing of the
+whole field.  Before timing, the labels are checked against the unmodified
+reference's labels on the same input (tests/golden/golden_hashes.json
+"H_2^k", pinned by scripts/ref_pin*.py) where a pin exists.
 One step = one full pass of the path: scene bounds, Morton codes, radix sort,
 hierarchy + refit + ropes, pair traversal fused with union-find, label
 finalisation (N > 1 adds the slab exchange and the distributed merge).
@@ -49,6 +53,30 @@ def measured_peak():
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
     except Exception:
         return PEAK_FALLBACK_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def golden():
+    with open(os.path.join(ROOT, "tests", "golden", "golden_hashes.json")) as f:
+        return json.load(f)
+
+
+def labels_checksum(labels, first: int) -> int:
+    """sum((label + 1) * (i % 65521 + 1)) mod 2^63 over rows i = first.. of a
+    device label tensor (the reference-side value comes from
+    oracle/_ref's ref_fof_field / scripts/ref_pin.py)."""
+    import torch
+    i = torch.arange(first, first + labels.numel(), dtype=torch.int64, device=labels.device)
+    return int(((labels.to(torch.int64) + 1) * (i % 65521 + 1)).sum().item())
+
+
+def reference_field_pinned(n_total: int, first: int, count: int):
+    """Rows [first, first+count) of H(n_total) from the reference generator,
+    in pinned host memory (the e2e leg's host input)."""
+    import torch
+    import paper_2409_10743_b200 as sp
+    host = torch.empty((count, 3), dtype=torch.float32, pin_memory=True)
+    sp.generate_reference_field(n_total, first, count, out=host)
+    return host
 
 
 # ---------------------------------------------------------------------------
@@ -177,7 +205,12 @@ def run_reference_arm(args, rank, world):
         return
     n_sample = args.cpu_sample_n
     v, kind, cores, secs = reference_sample(n_sample, args.steps, args.warmup)
-    cfg = workload_config(args, world)
+    cfg = {"workload": "fof_field SAMPLE: friends_of_friends on H(%d) (the same field shape at %d points; the "
+                       "2^27-point per-GPU workload takes ~56 s per run on this host's CPU, "
+                       "profiles/r02/ref_pin.json)" % (n_sample, n_sample),
+           "points_per_gpu": n_sample, "points_total": n_sample, "eps": eps_for(n_sample), "min_pts": 2,
+           "parallelism": "reference CPU (OpenMP, %d host threads)" % cores,
+           "sample_of": workload_config(args, world)["workload"]}
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "points/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs), "higher_is_better": True,
@@ -200,6 +233,7 @@ def workload_config(args, world):
                         "%d points per GPU (C5 per-GPU share), eps = 0.168*n_total^(-1/3)" % n,
             "points_per_gpu": n, "points_total": n * world, "eps": eps_for(n * world), "min_pts": 2,
             "parallelism": "x-slabs over %d GPU(s) with eps ghost layers" % world if (world > 1 or args.slabs) else "single GPU",
+            "input": "H(%d) rows of this rank, reference generator" % (n * world),
             "l2": "inputs (%.1f GB) larger than L2 (126 MB); no flush needed" % (n * 12 / 1e9)}
 
 
@@ -221,14 +255,18 @@ def run_ours(args, rank, world, local_rank):
     n_total = n * world
     eps = eps_for(n_total)
     slabs = world > 1 or args.slabs
+    # this rank's rows of H(n_total), reference generator, pinned host memory
+    host_pts = reference_field_pinned(n_total, rank * n, n)
+    pts = host_pts.to(dev)
+    labels = torch.empty(n, dtype=torch.int32, device=dev)
+    core = torch.empty(n, dtype=torch.uint8, device=dev)
     if slabs:
         from paper_2409_10743_b200 import distributed as spd
-        pts = sp.generate_field(n_total, first=rank * n, count=n, seed=args.seed, ctx=ctx)
-        step = lambda: spd.fof_slabs(pts, eps, first_index=rank * n, ctx=ctx)
+        comm = spd.SlabComm.from_process_group(ctx)
+
+        def step():
+            spd.fof_slabs(pts, eps, first_index=rank * n, ctx=ctx, comm=comm, out=(labels, core))
     else:
-        pts = sp.generate_field(n_total, first=0, count=n, seed=args.seed, ctx=ctx)
-        labels = torch.empty(n, dtype=torch.int32, device=dev)
-        core = torch.empty(n, dtype=torch.uint8, device=dev)
         step = lambda: sp.friends_of_friends(pts, eps, ctx=ctx, out=(labels, core))
 
     def barrier():
@@ -237,6 +275,33 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize(dev)
 
     for _ in range(args.warmup):
+        step()
+    # parity before timing: the labels of this input against the unmodified
+    # reference's (oracle/_ref friends_of_friends on the same H(n_total))
+    torch.cuda.synchronize(dev)
+    ck = torch.tensor([labels_checksum(labels, rank * n), int((labels == -1).sum()), int(core.sum()),
+                       int((labels == torch.arange(rank * n, rank * n + n, device=dev, dtype=torch.int32)).sum())],
+                      dtype=torch.int64, device=dev)
+    if slabs:
+        dist.all_reduce(ck)
+    ck = [int(v) for v in ck.tolist()]
+    pin = golden().get("H_2^%d" % (n_total.bit_length() - 1)) if n_total & (n_total - 1) == 0 else None
+    parity = {"checked_against": None, "labels_checksum": ck[0] & ((1 << 63) - 1), "noise": ck[1], "core": ck[2],
+              "clusters": ck[3]}
+    if pin is not None:
+        parity["checked_against"] = "oracle/_ref friends_of_friends on H(%d) (%s)" % (n_total, pin["labels_hash"])
+        parity["match"] = (parity["labels_checksum"] == pin["labels_checksum"] and ck[1] == pin["noise"] and
+                           ck[2] == pin["core"] and ck[3] == pin["clusters"])
+        if not parity["match"]:
+            raise SystemExit("PARITY FAILURE against the reference on H(%d): %s vs %s" % (n_total, parity, pin))
+    # node-visit rate of the merge: one diagnostic pass (SP_FLAG_STATS)
+    # counts the visits and member-pair tests of the same walks, untimed
+    visits = tests = None
+    if not slabs:
+        ctx.set_stats(True)
+        step()
+        visits, tests = ctx.counter("merge_node_visits"), ctx.counter("merge_pair_tests")
+        ctx.set_stats(False)
         step()
     # workload statistics for the byte models, outside timing: non-empty grid
     # cells of the FoF pipeline, their key width, and close pairs per point
@@ -302,8 +367,6 @@ def run_ours(args, rank, world, local_rank):
         # SP_FLAG_ASYNC: uploads/downloads go on its copy streams, so step
         # i+1's upload and step i-1's download overlap step i's kernels
         # (include/sp_b200.h).
-        host_pts = torch.empty((n, 3), dtype=torch.float32, pin_memory=True)
-        host_pts.copy_(pts)
         cstream = torch.cuda.Stream(dev)
         ectx = sp.Context(local_rank, stream=cstream.cuda_stream)
         host_labels = torch.empty(n, dtype=torch.int32, pin_memory=True)
@@ -325,17 +388,11 @@ def run_ours(args, rank, world, local_rank):
     else:
         # each rank uploads its pinned host slice, runs the slab FoF over NCCL
         # and downloads its labels + core flags, copies inside the timed region
-        from paper_2409_10743_b200 import distributed as spd
-        host_pts = torch.empty((n, 3), dtype=torch.float32, pin_memory=True)
-        host_pts.copy_(pts)
         host_labels = torch.empty(n, dtype=torch.int32, pin_memory=True)
         host_core = torch.empty(n, dtype=torch.uint8, pin_memory=True)
 
         def e2e_step():
-            d = host_pts.to(dev, non_blocking=True)
-            lab, cor = spd.fof_slabs(d, eps, first_index=rank * n, ctx=ctx)
-            host_labels.copy_(lab, non_blocking=True)
-            host_core.copy_(cor, non_blocking=True)
+            spd.fof_slabs(host_pts, eps, first_index=rank * n, ctx=ctx, comm=comm, out=(host_labels, host_core))
 
         e2e_step()
         barrier()
@@ -364,22 +421,49 @@ def run_ours(args, rank, world, local_rank):
     else:
         build_ms = None
 
+    merge_ms = phases.get("merge")
+    visit_rate = None
+    if visits and merge_ms:
+        visit_rate = {"merge_node_visits_per_step": visits, "merge_pair_tests_per_step": tests,
+                      "visits_per_cell": round(visits / max(cells, 1), 2),
+                      "node_visits_per_s": visits / (merge_ms / 1e3),
+                      "how": "one untimed SP_FLAG_STATS pass of the same walks; rate = visits / timed merge ms"}
+
     if rank != 0:
         return
+    # free this run's device memory before the extra configs (C5 at 2^30 needs
+    # ~146 GB) run in their own processes
+    del pts, labels, core
+    if not slabs:
+        del ectx
+    ctx.close()
+    torch.cuda.synchronize(dev)
+    torch.cuda.empty_cache()
+    extra = {}
+    if world == 1 and not args.no_extra:
+        for w, steps in (("c3", 5), ("c5", 3)):
+            extra[w] = run_extra(w, steps)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         v, kind, cores, secs = reference_sample(args.cpu_sample_n, 2, 0)
+        full = golden().get("H_2^%d" % (n_total.bit_length() - 1), {})
         cpu = {"value": v, "unit": "points/s", "cores": cores, "kind": kind,
                "sample": "friends_of_friends on H(%d) (same field shape, reference generator), %d runs, "
-                         "median %.2f s" % (args.cpu_sample_n, len(secs), statistics.median(secs))}
+                         "median %.2f s" % (args.cpu_sample_n, len(secs), statistics.median(secs)),
+               "full_size": ({"n": full["n"], "seconds": full["ref_seconds"],
+                              "points_per_s": full["n"] / full["ref_seconds"], "threads": full.get("threads"),
+                              "source": "oracle/_ref on the GPU host, profiles/r02/ref_pin.json (one run)"}
+                             if full.get("ref_seconds") else None)}
     line = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": value / ARBORX_A100_PTS_S,
         "vs_baseline_ref": "ArborX on 1x A100: ~37M HACC particles FoF in < 0.15 s (PAPER.md:489-493) = %.3g points/s"
                            % ARBORX_A100_PTS_S,
-        "dtype": "f32 (exact f64 distance predicate)", "data": "synthetic (device Philox HACC-like field)",
+        "dtype": "f32 (exact f64 distance predicate)",
+        "data": "synthetic: the SURVEY field H(n) from the reference generator (generate.cpp:17-66)",
         "config": workload_config(args, world),
+        "parity": parity,
         "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d * world,
                 "d2h_bytes_per_step": d2h * world},
         "gpu_launches": launches,
@@ -392,8 +476,26 @@ def run_ours(args, rank, world, local_rank):
         "phases_ms": {k: round(v, 3) for k, v in phases.items()},
         "close_pairs_per_point": pairs_per_pt,
         "fof_cells": cells,
+        "merge_visits": visit_rate,
+        "configs": extra or None,
     }
     print(json.dumps(line), flush=True)
+
+
+def run_extra(w: str, steps: int) -> dict:
+    """One other SURVEY §8(d) config in its own process (bench.py --workload),
+    reduced to the keys the headline line carries."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--workload", w, "--steps", str(steps), "--warmup", "1",
+           "--no-cpu-baseline"]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # reported, not fatal: the headline stands on its own
+        return {"error": "%s: %s" % (type(e).__name__, str(e)[:200])}
+    keep = ("metric", "value", "unit", "ms_per_step", "steps", "parts_ms", "parity", "e2e", "gpu_launches", "clocks")
+    out = {k: d.get(k) for k in keep}
+    out["workload"] = d.get("config", {}).get("workload")
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -411,6 +513,44 @@ CONFIGS = {
 }
 
 
+def config_parity(sp, w, n, pts, qs, eps, r2, ctx) -> dict:
+    """The config's result on its reference-generator input against the
+    unmodified reference's (tests/golden/golden_hashes.json: SURVEY §8(c) and
+    the scripts/ref_pin*.py pins), before timing.  Counts and checksums on the
+    device; the FNV hashes are checked by tests/ (-m gpu)."""
+    import torch
+    g = golden()
+    key = {"c1": "C1", "c2": "C2", "c3": "C3", "c4": "C4"}.get(w, "H_2^%d" % (n.bit_length() - 1))
+    pin = g.get(key) if (w != "c5" or n & (n - 1) == 0) else None
+    if pin is None or pin.get("n") != n:
+        return {"checked_against": None}
+    got = {}
+    if w in ("c1", "c3", "c5"):
+        out = (sp.fdbscan_densebox(pts, sp.DbscanParams(eps, 5), ctx=ctx) if w == "c3" else
+               sp.friends_of_friends(pts, eps, ctx=ctx))
+        lab, core = out.labels, out.core_flags
+        idx = torch.arange(n, device=lab.device, dtype=torch.int32)
+        got = {"noise": int((lab == -1).sum()), "core": int(core.sum())}
+        if w == "c3":  # min_pts > 2 labels are not unique; the core partition is
+            got["clusters"] = int(torch.unique(lab[core.bool()]).numel())
+        else:
+            got["clusters"] = int((lab == idx).sum())
+        if w == "c5":
+            got["labels_checksum"] = labels_checksum(lab, 0) & ((1 << 63) - 1)
+        del out, lab, core
+    elif w == "c2":
+        got = {"total_matches": int(sp.range_count(sp.Bvh.build(pts, ctx=ctx), qs, radius=r2).to(torch.int64).sum())}
+    else:
+        _, d = sp.nearest_query(sp.Bvh.build(pts, ctx=ctx), qs, 16, with_distances=True)
+        got = {"mean_16th_dist": float(d[:, 15].double().mean())}
+    ok = True
+    for k, v in got.items():
+        ok &= (abs(v - pin[k]) < 1e-9) if isinstance(v, float) else (v == pin[k])
+    if not ok:
+        raise SystemExit("PARITY FAILURE (%s) against %s: %s vs %s" % (w, key, got, pin))
+    return {"checked_against": "oracle/_ref (%s)" % key, "match": True, **got}
+
+
 def run_config(args):
     import numpy as np
     import torch
@@ -421,11 +561,22 @@ def run_config(args):
     ctx = sp.Context(0, stream=stream.cuda_stream)
     w = args.workload
     n = args.n if args.n != (1 << 27) else CONFIGS[w][0]
+    # SURVEY §8(d) inputs from the reference generator: U(n, 2409) (C1, C2,
+    # C4 points), U(n, 2410) (C4 queries), H(n) (C3, C5); pinned host copies
+    # are the e2e leg's inputs
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.float32, pin_memory=True)
+        t.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+        return t
+
     if w in ("c1", "c2", "c4"):
-        pts = sp.generate_uniform(n, 3, seed=args.seed, ctx=ctx)
+        host_pts = pinned(sp.generate_reference_uniform(n, 3, 1.0, 2409))
     else:
-        pts = sp.generate_field(n, seed=args.seed, ctx=ctx)
-    qs = sp.generate_uniform(n, 3, seed=args.seed + 1, ctx=ctx) if w == "c4" else pts
+        host_pts = reference_field_pinned(n, 0, n)
+    host_qs = pinned(sp.generate_reference_uniform(n, 3, 1.0, 2410)) if w == "c4" else host_pts
+    pts = host_pts.to(dev)
+    qs = host_qs.to(dev) if w == "c4" else pts
     eps = eps_for(n)
     r2 = float(np.float32(np.cbrt(30.0 / (n * 4.18879020478639))))
     times = {}
@@ -463,6 +614,7 @@ def run_config(args):
         step()
     torch.cuda.synchronize(dev)
     times.clear()
+    parity = config_parity(sp, w, n, pts, qs, eps, r2, ctx)
     sampler = ClockSampler(0)
     sampler.start()
     launches0 = ctx.kernel_launches
@@ -481,12 +633,6 @@ def run_config(args):
     # workloads run asynchronously (SP_FLAG_ASYNC: the next call's upload and
     # the previous call's download overlap the kernels, as in the headline);
     # build + query workloads are synchronous calls.
-    host_pts = torch.empty((n, 3), dtype=torch.float32, pin_memory=True)
-    host_pts.copy_(pts)
-    host_qs = host_pts
-    if w == "c4":
-        host_qs = torch.empty((n, 3), dtype=torch.float32, pin_memory=True)
-        host_qs.copy_(qs)
     clustering = w in ("c1", "c3", "c5")
     # reusable pinned result buffers, as a serving loop would hold them
     h_counts = torch.empty(n, dtype=torch.int32, pin_memory=True) if w == "c2" else None
@@ -563,6 +709,7 @@ def run_config(args):
                 "note": ("asynchronous calls (SP_FLAG_ASYNC) with pinned host buffers" if w in ("c1", "c3", "c5")
                          else "synchronous calls, pinned host inputs and reused pinned result buffers")},
         "gpu_launches": launches, "cpu_baseline": cpu, "clocks": clocks,
+        "parity": parity,
         "parts_ms": {k: round(v, 3) for k, v in parts.items()},
     }
     if w in ("c2", "c4"):
@@ -578,8 +725,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=1 << 27, help="points per GPU")
     ap.add_argument("--seed", type=int, default=2409)
-    ap.add_argument("--cpu-sample-n", type=int, default=1 << 22)
+    ap.add_argument("--cpu-sample-n", type=int, default=1 << 24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C3 / C5 (2^30) extra configs of the headline line")
     ap.add_argument("--slabs", action="store_true",
                     help="run the multi-GPU slab path (NCCL) even at one rank (tests the N > 1 code on one GPU)")
     ap.add_argument("--workload", default="fof_field", choices=["fof_field"] + sorted(CONFIGS),

@@ -42,11 +42,11 @@ typedef enum {
   SP_ECAPACITY = 2,  /* CapacityError : std::bad_alloc (traversal.hpp:229-231, 250-251) */
   SP_ECUDA = 3,      /* a CUDA runtime error (no reference counterpart) */
   SP_ENOMEM = 4,     /* device allocation failure */
-  SP_ENCCL = 5       /* reserved for the multi-GPU path */
+  SP_ENCCL = 5       /* an NCCL error (multi-GPU slab path) */
 } sp_status;
 
 enum { SP_MEM_HOST = 0, SP_MEM_DEVICE = 1 };
-enum { SP_FLAG_ASYNC = 1 };
+enum { SP_FLAG_ASYNC = 1, SP_FLAG_STATS = 2 };
 
 /* DBSCAN family selector (dbscan.hpp:277-301, 456-504).  FDBSCAN and FOF
  * cluster over grid cells when min_pts = 2; FOF_POINTS is
@@ -61,6 +61,7 @@ enum { SP_PRED_SPHERE = 0, SP_PRED_BOX = 1 };
 
 typedef struct sp_ctx sp_ctx;
 typedef struct sp_bvh sp_bvh;
+typedef struct sp_comm sp_comm;
 
 /* DbscanTimings (dbscan.hpp:29-36): device-event times per phase, ms. */
 typedef struct {
@@ -90,7 +91,10 @@ int sp_ctx_synchronize(sp_ctx *ctx);
  * stream (host<->device copies included) and return; host buffers must stay
  * valid and untouched until sp_ctx_synchronize.  Two contexts on two streams
  * then pipeline consecutive calls (one call's copies overlap the other's
- * kernels).  Timings are not collected in this mode. */
+ * kernels).  Timings are not collected in this mode.
+ * SP_FLAG_STATS: diagnostic twins of the traversal kernels also count their
+ * work into sp_ctx_counter ("merge_node_visits", "merge_pair_tests" for the
+ * FoF cell merge); slower, for measurement only. */
 int sp_ctx_set_flags(sp_ctx *ctx, int flags);
 const char *sp_last_error(const sp_ctx *ctx);
 /* Number of kernels this library launched on ctx since creation. */
@@ -186,6 +190,39 @@ int sp_dbscan(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, i
  * the multi-GPU slab FoF, which passes global indices (distributed.py). */
 int sp_fof_ids(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, const int32_t *ids,
                int32_t *labels, uint8_t *core, int mem);
+
+/* ---- multi-GPU friends-of-friends over x-slabs (SURVEY §8 row e) ----------
+ * The reference has no distributed search; this is the paper's
+ * ArborX-style partitioned FoF with one process (or
+ * context) per GPU.  Every rank passes the rows [first_index, first_index +
+ * n_local) of one global float[n_total*3] point array (3-D only,
+ * n_total < 2^31) and receives exactly those rows' labels: the smallest
+ * GLOBAL index of the point's cluster, or -1 for noise, and core flags — bit-
+ * identical to sp_dbscan(SP_ALGO_FOF) on the whole array (friends_of_friends,
+ * dbscan.hpp:286-292).  Each call is collective over the communicator.
+ * Steps: quantile x-splitters from an all-reduced sample histogram; one
+ * all-to-all of (xyz, global id) to the owner slab plus eps ghost copies to
+ * the neighbouring slabs; local FoF in global-id space; an all-gather of the
+ * (global id, label) links of every ghost copy; the same union-find on every
+ * rank; relabelled rows returned by a second all-to-all.  One host read (a
+ * G x 3G count matrix) sizes the exchanges. */
+/* NCCL unique id for sp_comm_create: made by one rank, passed to all. */
+int sp_comm_unique_id(uint8_t id[128]);
+/* ncclCommInitRank over nranks processes (one GPU each) on ctx's device. */
+int sp_comm_create(sp_ctx *ctx, int nranks, int rank, const uint8_t id[128], sp_comm **out);
+/* Use the caller's ncclComm_t (not owned: sp_comm_destroy leaves it open). */
+int sp_comm_wrap(sp_ctx *ctx, void *nccl_comm, sp_comm **out);
+int sp_comm_destroy(sp_comm *comm);
+int sp_comm_size(const sp_comm *comm);
+int sp_comm_rank(const sp_comm *comm);
+int sp_fof_slabs(sp_ctx *ctx, sp_comm *comm, const float *points, int64_t n_local, float eps, int64_t first_index,
+                 int32_t *labels, uint8_t *core, int mem);
+/* The same step with all nranks ranks in this process: ctxs[r] (one device
+ * each, or several contexts on one device) holds points[r] (n_local[r]
+ * rows; rank r's rows follow rank r-1's); exchanges are peer copies between
+ * the contexts' streams.  Errors are reported on ctxs[0]. */
+int sp_fof_slabs_multi(sp_ctx *const *ctxs, int nranks, const float *const *points, const int64_t *n_local, float eps,
+                       int32_t *const *labels, uint8_t *const *core, int mem);
 
 /* adjacency_graph_dbscan (dbscan.hpp:456-504): the legacy min_pts = 2
  * baseline that materialises the eps-neighbourhood CRS; SP_ECAPACITY when

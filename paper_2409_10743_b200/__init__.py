@@ -105,6 +105,14 @@ def _load() -> C.CDLL:
         "sp_check_equivalence": (C.c_int, [vp, vp, i64, C.c_int, f32, vp, vp, vp, vp, C.POINTER(i64),
                                            C.POINTER(C.c_int), C.c_int]),
         "sp_generate_reference_field": (C.c_int, [i64, i64, i64, vp]),
+        "sp_comm_unique_id": (C.c_int, [vp]),
+        "sp_comm_create": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
+        "sp_comm_wrap": (C.c_int, [vp, vp, vp]),
+        "sp_comm_destroy": (C.c_int, [vp]),
+        "sp_comm_size": (C.c_int, [vp]),
+        "sp_comm_rank": (C.c_int, [vp]),
+        "sp_fof_slabs": (C.c_int, [vp, vp, vp, i64, f32, i64, vp, vp, C.c_int]),
+        "sp_fof_slabs_multi": (C.c_int, [vp, C.c_int, vp, vp, f32, vp, vp, C.c_int]),
         "sp_generate_field": (C.c_int, [vp, i64, i64, i64, C.c_uint64, vp, C.c_int]),
         "sp_generate_uniform": (C.c_int, [vp, i64, C.c_int, C.c_uint64, vp, C.c_int]),
     }
@@ -145,6 +153,7 @@ class Context:
         if rc != SP_OK:
             raise CudaError("sp_ctx_create(device=%d) failed (status %d): no usable CUDA device" % (device, rc))
         self.h = h
+        self._flags = 0
         self.device = device
         self.stream = stream  # the caller's stream handle, or None (own stream)
 
@@ -169,7 +178,14 @@ class Context:
     def set_async(self, on: bool = True):
         """SP_FLAG_ASYNC: calls only enqueue work; call synchronize() before
         reading outputs or reusing host buffers."""
-        self._check(_lib.sp_ctx_set_flags(self.h, 1 if on else 0))
+        self._flags = (self._flags | 1) if on else (self._flags & ~1)
+        self._check(_lib.sp_ctx_set_flags(self.h, self._flags))
+
+    def set_stats(self, on: bool = True):
+        """SP_FLAG_STATS: diagnostic kernels count traversal work into
+        counter() ("merge_node_visits", "merge_pair_tests"); measurement only."""
+        self._flags = (self._flags | 2) if on else (self._flags & ~2)
+        self._check(_lib.sp_ctx_set_flags(self.h, self._flags))
 
     @property
     def kernel_launches(self) -> int:

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <string>
@@ -14,9 +15,14 @@
 #include "sp_common.cuh"
 #include "sp_internal.hpp"
 #include "sp_query.hpp"
+#include "sp_slabs.hpp"
 
 struct sp_ctx {
   spb::Ctx c;
+};
+
+struct sp_comm {
+  spb::SlabExchange *x = nullptr;
 };
 
 struct sp_bvh {
@@ -150,6 +156,9 @@ int guarded(sp_ctx *ctx, F &&f, bool fresh = true) {
   } catch (const spb::CapacityError &e) {
     ctx->c.last_error = e.what();
     rc = SP_ECAPACITY;
+  } catch (const spb::NcclError &e) {
+    ctx->c.last_error = e.what();
+    rc = SP_ENCCL;
   } catch (const spb::CudaError &e) {
     ctx->c.last_error = e.what();
     rc = strstr(e.what(), "allocation") ? SP_ENOMEM : SP_ECUDA;
@@ -566,6 +575,115 @@ int sp_dbscan(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, i
       stats->num_dense_cells = res.num_dense_cells;
       stats->num_dense_points = res.num_dense_points;
     }
+  });
+}
+
+// ---- multi-GPU slab FoF (SURVEY §8 row e; sp_slabs.cu) -----------------------
+int sp_comm_unique_id(uint8_t id[128]) {
+  if (!id) return SP_EINVAL;
+  try {
+    spb::nccl_unique_id(id);
+  } catch (const std::exception &) {
+    return SP_ENCCL;
+  }
+  return SP_OK;
+}
+
+int sp_comm_create(sp_ctx *ctx, int nranks, int rank, const uint8_t id[128], sp_comm **out) {
+  if (!out || !id) return SP_EINVAL;
+  *out = nullptr;
+  return guarded(ctx, [&](spb::Ctx &c) {
+    sp_comm *cm = new sp_comm;
+    try {
+      cm->x = spb::nccl_exchange_create(c.device, nranks, rank, id);
+    } catch (...) {
+      delete cm;
+      throw;
+    }
+    *out = cm;
+  });
+}
+
+int sp_comm_wrap(sp_ctx *ctx, void *nccl_comm, sp_comm **out) {
+  if (!out) return SP_EINVAL;
+  *out = nullptr;
+  return guarded(ctx, [&](spb::Ctx &) {
+    sp_comm *cm = new sp_comm;
+    try {
+      cm->x = spb::nccl_exchange_wrap(nccl_comm);
+    } catch (...) {
+      delete cm;
+      throw;
+    }
+    *out = cm;
+  });
+}
+
+int sp_comm_destroy(sp_comm *comm) {
+  if (!comm) return SP_EINVAL;
+  spb::exchange_destroy(comm->x);
+  delete comm;
+  return SP_OK;
+}
+
+int sp_comm_size(const sp_comm *comm) { return comm ? spb::exchange_size(comm->x) : -1; }
+int sp_comm_rank(const sp_comm *comm) { return comm ? spb::exchange_rank(comm->x) : -1; }
+
+int sp_fof_slabs(sp_ctx *ctx, sp_comm *comm, const float *points, int64_t n_local, float eps, int64_t first_index,
+                 int32_t *labels, uint8_t *core, int mem) {
+  if (!comm) return SP_EINVAL;
+  return guarded(ctx, [&](spb::Ctx &c) {
+    if (n_local < 0 || n_local > (1LL << 30)) throw spb::InvalidArgument("point count out of range");
+    if (n_local > 0 && (!points || !labels || !core)) throw spb::InvalidArgument("null array");
+    In<float> p(c, points, (size_t)n_local * 3, mem);
+    Out<int32_t> ol(c, labels, (size_t)n_local, mem);
+    Out<uint8_t> oc(c, core, (size_t)n_local, mem);
+    std::vector<spb::SlabInput> in(1);
+    in[0] = spb::SlabInput{&c, p.p, n_local, first_index, ol.p, oc.p};
+    spb::fof_slabs(in, *comm->x, eps);
+    ol.flush(c);
+    oc.flush(c);
+    sync_all(c);
+  });
+}
+
+int sp_fof_slabs_multi(sp_ctx *const *ctxs, int nranks, const float *const *points, const int64_t *n_local, float eps,
+                       int32_t *const *labels, uint8_t *const *core, int mem) {
+  if (!ctxs || nranks < 1 || !points || !n_local || !labels || !core) return SP_EINVAL;
+  for (int r = 0; r < nranks; ++r)
+    if (!ctxs[r]) return SP_EINVAL;
+  return guarded(ctxs[0], [&](spb::Ctx &c0) {
+    std::vector<std::unique_ptr<In<float>>> pin;
+    std::vector<std::unique_ptr<Out<int32_t>>> pl;
+    std::vector<std::unique_ptr<Out<uint8_t>>> pc;
+    std::vector<spb::SlabInput> in((size_t)nranks);
+    int64_t first = 0;
+    for (int r = 0; r < nranks; ++r) {
+      spb::Ctx &c = ctxs[r]->c;
+      if (n_local[r] < 0 || n_local[r] > (1LL << 30)) throw spb::InvalidArgument("point count out of range");
+      spb::ScopedDevice sd(c.device);
+      if (r > 0) {
+        spb::reset_marks(c);
+        c.in_used = c.out_used = 0;
+        c.counters.clear();
+        ++c.calls;
+      }
+      pin.emplace_back(new In<float>(c, points[r], (size_t)n_local[r] * 3, mem));
+      pl.emplace_back(new Out<int32_t>(c, labels[r], (size_t)n_local[r], mem));
+      pc.emplace_back(new Out<uint8_t>(c, core[r], (size_t)n_local[r], mem));
+      in[r] = spb::SlabInput{&c, pin[r]->p, n_local[r], first, pl[r]->p, pc[r]->p};
+      first += n_local[r];
+    }
+    spb::fof_slabs_multi(in, eps);
+    for (int r = 0; r < nranks; ++r) {
+      spb::Ctx &c = ctxs[r]->c;
+      spb::ScopedDevice sd(c.device);
+      pl[r]->flush(c);
+      pc[r]->flush(c);
+      sync_all(c);
+      if (r > 0 && c.marks_used) spb::resolve_marks(c);
+    }
+    (void)c0;
   });
 }
 

@@ -31,6 +31,9 @@ struct CudaError : std::runtime_error {
 struct InvalidArgument : std::invalid_argument {
   using std::invalid_argument::invalid_argument;
 };
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 struct CapacityError : std::runtime_error {
   CapacityError() : std::runtime_error("crs result exceeds capacity") {}
 };

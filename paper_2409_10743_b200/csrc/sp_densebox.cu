@@ -670,9 +670,12 @@ __global__ void k_cell_ranges(const int64_t *__restrict__ cell_start, int64_t m,
 
 // Union cell a's set (root hint `root`) with leaf cell b's when a member pair
 // is within eps; returns the updated hint.
+// STATS: count member-pair distance tests into *tests.
+template <bool STATS = false>
 __device__ __forceinline__ int32_t cells_leaf(const int64_t *__restrict__ cell_start, int64_t m, int64_t n,
                                               const float4 *__restrict__ cpts, const Radius &R, int32_t *parent,
-                                              int64_t sa, int64_t ea, int32_t root, int32_t b) {
+                                              int64_t sa, int64_t ea, int32_t root, int32_t b,
+                                              int64_t *tests = nullptr) {
   if (parent[b] == root) return root;
   const int32_t ra = uf_find(parent, root), rb = uf_find(parent, b);
   if (ra == rb) return ra;
@@ -682,6 +685,7 @@ __device__ __forceinline__ int32_t cells_leaf(const int64_t *__restrict__ cell_s
     const float4 x = cpts[i];
     for (int64_t j = sb; j < eb; ++j) {
       const float4 y = cpts[j];
+      if (STATS) ++*tests;
       if (hit_point(R, x.x, x.y, x.z, y.x, y.y, y.z)) {
         found = true;
         break;
@@ -706,17 +710,21 @@ __device__ __forceinline__ int32_t cells_leaf(const int64_t *__restrict__ cell_s
 #define SPB_SM_MIN_ITEMS (1 << 22)
 #endif
 
-template <bool FAST>
+// STATS: add this walk's node visits and member-pair tests to stats[0..1]
+// (diagnostic launch only, SP_FLAG_STATS; the timed kernel is STATS = false).
+template <bool FAST, bool STATS = false>
 __device__ __forceinline__ void fof_cell_walk(const float4 *__restrict__ nodes, int64_t m,
                                               const int64_t *__restrict__ cell_start, int64_t n,
                                               const float4 *__restrict__ cpts, const Radius &R, int32_t *parent,
-                                              int64_t a) {
+                                              int64_t a, unsigned long long *stats = nullptr) {
   const int64_t first_leaf = m - 1;
   const float4 qlo = ld_node(nodes, 2 * (first_leaf + a)), qhi = ld_node(nodes, 2 * (first_leaf + a) + 1);
   const int64_t sa = cell_start[a], ea = a + 1 < m ? cell_start[a + 1] : n;
   int32_t root = (int32_t)a;
   int32_t cur = node_rope(qhi);
+  int64_t visits = 0, tests = 0;
   while (cur != kSentinel) {
+    if (STATS) ++visits;
     const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
     if (cells_far(R, qlo, qhi, lo, hi)) {
       cur = node_rope(hi);
@@ -726,8 +734,12 @@ __device__ __forceinline__ void fof_cell_walk(const float4 *__restrict__ nodes, 
       cur = node_link(lo);
       continue;
     }
-    root = cells_leaf(cell_start, m, n, cpts, R, parent, sa, ea, root, (int32_t)(cur - first_leaf));
+    root = cells_leaf<STATS>(cell_start, m, n, cpts, R, parent, sa, ea, root, (int32_t)(cur - first_leaf), &tests);
     cur = node_rope(hi);
+  }
+  if (STATS) {
+    atomicAdd(stats, (unsigned long long)visits);
+    atomicAdd(stats + 1, (unsigned long long)tests);
   }
 }
 
@@ -752,6 +764,19 @@ __global__ void __launch_bounds__(128, 1) k_fof_cells_merge_sm(const float4 *__r
   SmSliceWalk w(m, slices, nslices);
   for (int64_t a; w.next(a);)
     if (a >= 0) fof_cell_walk<FAST>(nodes, m, cell_start, n, cpts, R, parent, a);
+}
+
+// Diagnostic twin of the merge (same walks and unions) that also counts node
+// visits and member-pair tests; launched instead of the merge only when the
+// context has SP_FLAG_STATS, never in a timed run.
+template <bool FAST>
+__global__ void __launch_bounds__(128, 1) k_fof_cells_merge_stats(const float4 *__restrict__ nodes, int64_t m,
+                                                               const int64_t *__restrict__ cell_start, int64_t n,
+                                                               const float4 *__restrict__ cpts, Radius R,
+                                                               int32_t *parent, unsigned long long *stats) {
+  R.fast = FAST ? 1 : 0;
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a < m) fof_cell_walk<FAST, true>(nodes, m, cell_start, n, cpts, R, parent, a, stats);
 }
 
 // cells: core iff the cell has two points or its set spans several cells;
@@ -1141,7 +1166,18 @@ bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t 
   SPB_LAUNCHED();
   {
     const Radius R = make_radius(eps);
-    if (SPB_MERGE_SM && m >= SPB_SM_MIN_ITEMS) {
+    if (c.stats()) {
+      DevBuf<unsigned long long> st(2, c.stream);
+      SPB_CUDA(cudaMemsetAsync(st.get(), 0, 2 * sizeof(unsigned long long), c.stream));
+      auto kern = R.fast ? k_fof_cells_merge_stats<true> : k_fof_cells_merge_stats<false>;
+      kern<<<(unsigned)((m + 127) / 128), 128, 0, c.stream>>>(g.t.nodes, m, g.cell_start.get(), n, g.cpts.get(), R,
+                                                              parent.get(), st.get());
+      SPB_LAUNCHED();
+      unsigned long long hs[2] = {0, 0};
+      peek(c, {{st.get(), hs, sizeof(hs)}});
+      c.count("merge_node_visits", (int64_t)hs[0]);
+      c.count("merge_pair_tests", (int64_t)hs[1]);
+    } else if (SPB_MERGE_SM && m >= SPB_SM_MIN_ITEMS) {
       SmSlices sl(c);
       if (R.fast)
         k_fof_cells_merge_sm<true><<<sl.grid(k_fof_cells_merge_sm<true>, 128), 128, 0, c.stream>>>(

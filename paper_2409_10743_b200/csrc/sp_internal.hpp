@@ -35,6 +35,8 @@ struct Ctx {
   int *d_err = nullptr;
   cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams for host buffers
   bool async() const { return (flags & 1) != 0; }
+  // SP_FLAG_STATS: diagnostic kernels count traversal work into counters
+  bool stats() const { return (flags & 2) != 0; }
   // Double-buffered device staging for host arrays (per call parity, per
   // argument position).  A slot is reused two calls later, after the event
   // recorded when its last consumer (kernels for inputs, the download for

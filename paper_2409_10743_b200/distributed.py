@@ -2,17 +2,25 @@
 
 The reference has no distributed search; the paper's
 ArborX runs FoF per MPI rank.  This is the B200 form:
-one process per GPU, `torch.distributed` (NCCL over NVLink on GPUs, gloo on
-CPU for the tests) for the data exchange, the local FoF on the device.
+one process per GPU.
 
-    labels, core = fof_slabs(points, eps, first_index=...)
+    comm = SlabComm.create(ctx)                 # NCCL, over the default group
+    labels, core = fof_slabs(points, eps, first_index=..., ctx=ctx, comm=comm)
 
 Every rank passes its slice of the global point array (rows
 [first_index, first_index + n_local) in input order) and receives the labels
 of exactly those rows: the smallest GLOBAL index of the point's cluster, or
 -1 for noise — identical to a single-GPU run on the whole array.
 
-Steps (each a collective over the default group):
+The product path is native: sp_fof_slabs (csrc/sp_slabs.cu) runs every step
+on the device with NCCL collectives and one host read of the exchange sizes;
+`fof_slabs_multi` drives several contexts from one process (sp_fof_slabs_multi,
+peer copies instead of NCCL).  `fof_slabs_torch` restates the same algorithm
+over torch.distributed collectives (any backend): with gloo and a CPU local
+FoF it is the world-size-2/3 CPU model of the exchange and merge logic the
+tests run without a GPU.
+
+Steps of fof_slabs_torch (each a collective over the default group):
   1. splitters  — all-gather per-rank x-quantiles; G-1 global x-splitters;
   2. partition  — all-to-all points + global indices to their slab owner;
   3. ghosts     — all-to-all copies of points within w = eps*(1+1e-6) of
@@ -32,6 +40,7 @@ from __future__ import annotations
 
 from typing import Callable, Optional, Tuple
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -69,15 +78,17 @@ def _device_fof(ctx):
     import paper_2409_10743_b200 as sp
 
     def run(points: torch.Tensor, eps: float, gids: torch.Tensor):
-        # the torch ops that produced `points` ran on torch's current stream;
-        # a context on another stream must not start before they finish (a
-        # context on that same stream is ordered already, and a host wait
-        # there would stop the host from queueing the next step ahead)
-        if ctx is not None and points.is_cuda:
+        ids = gids.to(torch.int32).contiguous()
+        c = ctx
+        if c is None:
+            # torch's current stream on the points' device: ordered after the
+            # torch ops (and collectives) that produced points and ids
+            c = sp.default_context(sp._device_of(points))
+        elif points.is_cuda:
             cur = torch.cuda.current_stream(points.device)
-            if getattr(ctx, "stream", None) is None or int(ctx.stream) != int(cur.cuda_stream):
-                cur.synchronize()
-        out = sp.friends_of_friends_ids(points, eps, gids.to(torch.int32).contiguous(), ctx=ctx)
+            if getattr(c, "stream", None) is None or int(c.stream) != int(cur.cuda_stream):
+                cur.synchronize()  # a context on another stream waits for them
+        out = sp.friends_of_friends_ids(points, eps, ids, ctx=c)
         return out.labels, out.core_flags
 
     run.global_ids = True
@@ -115,9 +126,11 @@ def label_components(keys: torch.Tensor, labels: torch.Tensor) -> Tuple[torch.Te
         parent = new
 
 
-def fof_slabs(points: torch.Tensor, eps: float, first_index: int = 0, ctx=None,
-              local_fof: Optional[Callable] = None, samples: int = 4096):
-    """Friends-of-friends over all ranks' points; see the module docstring.
+def fof_slabs_torch(points: torch.Tensor, eps: float, first_index: int = 0, ctx=None,
+                    local_fof: Optional[Callable] = None, samples: int = 4096):
+    """Friends-of-friends over all ranks' points with torch.distributed
+    collectives (the algorithm restated for any backend); see the module
+    docstring.
 
     points: (n_local, 3) float32 on this rank's device (CUDA for NCCL, CPU for
     gloo).  local_fof(points, eps) -> (labels int32, core uint8) with
@@ -126,18 +139,6 @@ def fof_slabs(points: torch.Tensor, eps: float, first_index: int = 0, ctx=None,
     world = dist.get_world_size()
     rank = dist.get_rank()
     dev = points.device
-    import os
-    import time
-    timing = os.environ.get("SPB_SLAB_TIMING") is not None
-    t_last = [time.perf_counter()]
-
-    def tick(name):
-        if timing:
-            if dev.type == "cuda":
-                torch.cuda.synchronize(dev)
-            now = time.perf_counter()
-            print("[slabs r%d] %-10s %8.2f ms" % (rank, name, (now - t_last[0]) * 1e3), flush=True)
-            t_last[0] = now
     run_local = local_fof or _device_fof(ctx)
     n_local = points.shape[0]
     gidx = torch.arange(first_index, first_index + n_local, dtype=torch.int64, device=dev)
@@ -162,7 +163,6 @@ def fof_slabs(points: torch.Tensor, eps: float, first_index: int = 0, ctx=None,
         pos = (torch.arange(1, world, device=dev, dtype=torch.float64) / world * (allq.numel() - 1)).round().long()
         splitters = allq[pos].float()
 
-    tick("splitters")
 
     # 2. partition: rank d owns x in [splitters[d-1], splitters[d]); the stable
     #    argsort runs on 16-bit slab ids (a one/two-pass radix sort)
@@ -178,7 +178,6 @@ def fof_slabs(points: torch.Tensor, eps: float, first_index: int = 0, ctx=None,
         order, send, recv = None, [n_local], [n_local]
         own_pts, own_gidx = points, gidx
 
-    tick("partition")
 
     # 3. ghosts: copies to every other slab within w of the point; only points
     #    within w of a splitter can have any
@@ -212,13 +211,9 @@ def fof_slabs(points: torch.Tensor, eps: float, first_index: int = 0, ctx=None,
         all_pts, all_gidx = own_pts, own_gidx
     sent_gidx = own_gidx[src]  # my points that live as ghosts elsewhere
 
-    tick("ghosts")
 
     # 4. local FoF over owned + ghosts; the cluster label becomes the minimum
     #    GLOBAL index of its local members (a segmented min over the labels)
-    if timing and os.environ.get("SPB_SLAB_INPUT"):
-        print("[slabs r%d] local input %s %s min %s max %s eps %r" % (rank, tuple(all_pts.shape), all_pts.dtype,
-              all_pts.min(0).values.tolist(), all_pts.max(0).values.tolist(), eps), flush=True)
     if getattr(run_local, "global_ids", False):
         lab, core_all = run_local(all_pts.contiguous(), eps, all_gidx)
         glab = lab.to(torch.int64)
@@ -232,7 +227,6 @@ def fof_slabs(points: torch.Tensor, eps: float, first_index: int = 0, ctx=None,
     core_all = core_all.to(dev)
     own_lab, own_core = glab[:m_own], core_all[:m_own]
 
-    tick("local")
 
     # 5. merge across slabs: (global index, label) of every ghost copy and of
     # the originals that were sent as ghosts
@@ -246,7 +240,6 @@ def fof_slabs(points: torch.Tensor, eps: float, first_index: int = 0, ctx=None,
         hit = (own_lab >= 0) & (u[idx] == own_lab)
         own_lab = torch.where(hit, f[idx], own_lab)
 
-    tick("merge")
 
     # 6. labels back to the input layout
     if world > 1:
@@ -258,5 +251,149 @@ def fof_slabs(points: torch.Tensor, eps: float, first_index: int = 0, ctx=None,
         core_out[order] = back_core
     else:
         labels, core_out = own_lab, own_core
-    tick("return")
     return labels.to(torch.int32), core_out.to(torch.uint8)
+
+
+# ---------------------------------------------------------------------------
+# native path (sp_fof_slabs / sp_fof_slabs_multi)
+# ---------------------------------------------------------------------------
+class SlabComm:
+    """An sp_comm: the NCCL communicator of the native slab FoF."""
+
+    def __init__(self, handle, ctx):
+        self.h = handle
+        self.ctx = ctx
+
+    @classmethod
+    def create(cls, ctx, group=None) -> "SlabComm":
+        """ncclCommInitRank over the ranks of `group` (default: the default
+        process group); rank 0's unique id travels by a torch.distributed
+        broadcast (any backend)."""
+        import ctypes as C
+        import paper_2409_10743_b200 as sp
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = (C.c_uint8 * 128)()
+        if rank == 0 and sp._lib.sp_comm_unique_id(uid) != sp.SP_OK:
+            raise sp.CudaError("sp_comm_unique_id failed (NCCL unavailable)")
+        dev = torch.device("cuda", ctx.device) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+        t = torch.tensor(bytearray(bytes(uid)), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        uid = (C.c_uint8 * 128)(*t.cpu().tolist())
+        h = C.c_void_p()
+        ctx._check(sp._lib.sp_comm_create(ctx.h, world, rank, uid, C.byref(h)))
+        return cls(h, ctx)
+
+    @classmethod
+    def from_process_group(cls, ctx, group=None) -> "SlabComm":
+        return cls.create(ctx, group)
+
+    @classmethod
+    def wrap(cls, ctx, nccl_comm: int) -> "SlabComm":
+        """Use an existing ncclComm_t (an integer handle; not owned)."""
+        import ctypes as C
+        import paper_2409_10743_b200 as sp
+        h = C.c_void_p()
+        ctx._check(sp._lib.sp_comm_wrap(ctx.h, C.c_void_p(nccl_comm), C.byref(h)))
+        return cls(h, ctx)
+
+    @property
+    def size(self) -> int:
+        import paper_2409_10743_b200 as sp
+        return int(sp._lib.sp_comm_size(self.h))
+
+    @property
+    def rank(self) -> int:
+        import paper_2409_10743_b200 as sp
+        return int(sp._lib.sp_comm_rank(self.h))
+
+    def close(self):
+        import paper_2409_10743_b200 as sp
+        if self.h:
+            sp._lib.sp_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_comms: dict = {}
+
+
+def _native_out(points, n, out, dev):
+    import paper_2409_10743_b200 as sp
+    if out is not None:
+        lab, lp = sp._given_out(out[0], (n,), 4, dev)
+        core, cp = sp._given_out(out[1], (n,), 1, dev)
+        return lab, core, lp, cp
+    kw = dict(device=points.device) if dev else dict(pin_memory=False)
+    lab = torch.empty(n, dtype=torch.int32, **kw)
+    core = torch.empty(n, dtype=torch.uint8, **kw)
+    return lab, core, sp._ptr(lab), sp._ptr(core)
+
+
+def fof_slabs(points, eps: float, first_index: int = 0, ctx=None, comm: Optional[SlabComm] = None, out=None,
+              local_fof: Optional[Callable] = None, samples: int = 4096):
+    """Friends-of-friends over all ranks' points; see the module docstring.
+
+    With a SlabComm, or CUDA points under an NCCL default group, this is the
+    native sp_fof_slabs (points: (n_local, 3) float32, device tensor or host
+    array/pinned tensor; `out` = (labels int32, core uint8) in the same memory
+    space).  With a custom `local_fof` or gloo/CPU tensors it is
+    fof_slabs_torch.  Returns (labels int32, core uint8) for this rank's rows."""
+    import ctypes as C
+    import paper_2409_10743_b200 as sp
+    native = comm is not None or (local_fof is None and sp._is_cuda(points) and dist.is_initialized() and
+                                  dist.get_backend() == "nccl")
+    if not native:
+        return fof_slabs_torch(points, eps, first_index=first_index, ctx=ctx, local_fof=local_fof, samples=samples)
+    if ctx is None:
+        ctx = sp.default_context(sp._device_of(points))
+    if comm is None:
+        key = (ctx.device, id(dist.group.WORLD))
+        if key not in _comms:
+            _comms[key] = SlabComm.create(ctx)
+        comm = _comms[key]
+    if len(points.shape) != 2 or int(points.shape[1]) != 3:
+        raise sp.InvalidArgument("points must have shape (n, 3)")
+    n = int(points.shape[0])
+    p, mem, keep = sp._in(points, np.float32)
+    dev = mem == sp.SP_MEM_DEVICE
+    lab, core, lp, cp = _native_out(points, n, out, dev)
+    ctx._check(sp._lib.sp_fof_slabs(ctx.h, comm.h, p, n, C.c_float(eps), int(first_index), lp, cp, mem))
+    return lab, core
+
+
+def fof_slabs_multi(points: list, eps: float, ctxs: Optional[list] = None, out: Optional[list] = None):
+    """All ranks in this process (sp_fof_slabs_multi): points[r] holds rank
+    r's rows (rank r's rows follow rank r-1's), on ctxs[r]'s device (or all on
+    the host).  Several contexts may share one device.  Returns
+    [(labels, core)] per rank."""
+    import ctypes as C
+    import paper_2409_10743_b200 as sp
+    G = len(points)
+    if ctxs is None:
+        ctxs = [sp.Context(sp._device_of(p)[0]) for p in points]
+    if len(ctxs) != G:
+        raise ValueError("one context per rank")
+    arrs, keeps, mems, res = [], [], set(), []
+    for r, pr in enumerate(points):
+        if len(pr.shape) != 2 or int(pr.shape[1]) != 3:
+            raise sp.InvalidArgument("points must have shape (n, 3)")
+        p, mem, keep = sp._in(pr, np.float32)
+        arrs.append(p)
+        keeps.append(keep)
+        mems.add(mem)
+        res.append(_native_out(pr, int(pr.shape[0]), out[r] if out is not None else None, mem == sp.SP_MEM_DEVICE))
+    if len(mems) != 1:
+        raise ValueError("all ranks' points must live in the same memory space")
+    mem = mems.pop()
+    P = (C.c_void_p * G)(*[a.value for a in arrs])
+    N = (C.c_int64 * G)(*[int(pr.shape[0]) for pr in points])
+    LP = (C.c_void_p * G)(*[r_[2].value for r_ in res])
+    CP = (C.c_void_p * G)(*[r_[3].value for r_ in res])
+    H = (C.c_void_p * G)(*[c.h.value for c in ctxs])
+    ctxs[0]._check(sp._lib.sp_fof_slabs_multi(H, G, P, N, C.c_float(eps), LP, CP, mem))
+    return [(r_[0], r_[1]) for r_ in res]
