@@ -388,20 +388,27 @@ def run_ours(args, rank, world, local_rank):
     else:
         # each rank uploads its pinned host slice, runs the slab FoF over NCCL
         # and downloads its labels + core flags, copies inside the timed region
+        # (SP_FLAG_ASYNC as in the single-GPU leg: step i+1's upload overlaps
+        # step i's compute after its one host read of the exchange sizes)
         host_labels = torch.empty(n, dtype=torch.int32, pin_memory=True)
         host_core = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        cstream = torch.cuda.Stream(dev)
+        ectx = sp.Context(local_rank, stream=cstream.cuda_stream)
 
         def e2e_step():
-            spd.fof_slabs(host_pts, eps, first_index=rank * n, ctx=ctx, comm=comm, out=(host_labels, host_core))
+            spd.fof_slabs(host_pts, eps, first_index=rank * n, ctx=ectx, comm=comm, out=(host_labels, host_core))
 
         e2e_step()
+        ectx.set_async(True)
         barrier()
         e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e_start.record(stream)
+        e_start.record(cstream)
         for _ in range(args.steps):
             e2e_step()
-        e_end.record(stream)
+        ectx.synchronize()
+        e_end.record(cstream)
         barrier()
+        ectx.set_async(False)
         t = torch.tensor([e_start.elapsed_time(e_end)], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_value = n_total * args.steps / (float(t.item()) / 1e3)
@@ -434,8 +441,7 @@ def run_ours(args, rank, world, local_rank):
     # free this run's device memory before the extra configs (C5 at 2^30 needs
     # ~146 GB) run in their own processes
     del pts, labels, core
-    if not slabs:
-        del ectx
+    ectx.close()
     ctx.close()
     torch.cuda.synchronize(dev)
     torch.cuda.empty_cache()

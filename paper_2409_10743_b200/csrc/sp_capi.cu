@@ -643,7 +643,7 @@ int sp_fof_slabs(sp_ctx *ctx, sp_comm *comm, const float *points, int64_t n_loca
     spb::fof_slabs(in, *comm->x, eps);
     ol.flush(c);
     oc.flush(c);
-    sync_all(c);
+    finish(c);
   });
 }
 

@@ -717,25 +717,24 @@ __device__ __forceinline__ void fof_cell_walk(const float4 *__restrict__ nodes, 
                                               const int64_t *__restrict__ cell_start, int64_t n,
                                               const float4 *__restrict__ cpts, const Radius &R, int32_t *parent,
                                               int64_t a, unsigned long long *stats = nullptr) {
-  const int64_t first_leaf = m - 1;
+  const int32_t first_leaf = (int32_t)(m - 1);
   const float4 qlo = ld_node(nodes, 2 * (first_leaf + a)), qhi = ld_node(nodes, 2 * (first_leaf + a) + 1);
   const int64_t sa = cell_start[a], ea = a + 1 < m ? cell_start[a + 1] : n;
   int32_t root = (int32_t)a;
   int32_t cur = node_rope(qhi);
   int64_t visits = 0, tests = 0;
+  // One exit (the loop test) and the leaf work as the only conditional
+  // block: an early exit inside the body lets the compiler drop the warp's
+  // per-iteration reconvergence (no BSSY/BSYNC around the body in the SASS),
+  // and the walk then runs about 5x slower.
   while (cur != kSentinel) {
     if (STATS) ++visits;
     const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
-    if (cells_far(R, qlo, qhi, lo, hi)) {
-      cur = node_rope(hi);
-      continue;
-    }
-    if (cur < first_leaf) {
-      cur = node_link(lo);
-      continue;
-    }
-    root = cells_leaf<STATS>(cell_start, m, n, cpts, R, parent, sa, ea, root, (int32_t)(cur - first_leaf), &tests);
-    cur = node_rope(hi);
+    const bool far = cells_far(R, qlo, qhi, lo, hi);
+    const bool descend = !far && cur < first_leaf;
+    if (!far && !descend)
+      root = cells_leaf<STATS>(cell_start, m, n, cpts, R, parent, sa, ea, root, (int32_t)(cur - first_leaf), &tests);
+    cur = descend ? node_link(lo) : node_rope(hi);
   }
   if (STATS) {
     atomicAdd(stats, (unsigned long long)visits);

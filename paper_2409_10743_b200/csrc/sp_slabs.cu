@@ -123,7 +123,22 @@ void nccl_unique_id(uint8_t out[128]) {
 // drives (one under NCCL, all of them in the single-process form).
 // ---------------------------------------------------------------------------
 struct SlabExchange {
-  virtual ~SlabExchange() = default;
+  // host-mapped pinned scratch for the count matrix: written by a kernel, so
+  // the read never queues on a copy engine behind a bulk transfer
+  unsigned long long *host_mat = nullptr, *dev_mat = nullptr;
+  unsigned long long *mapped(size_t count) {
+    if (!host_mat) {
+      SPB_CUDA(cudaHostAlloc(reinterpret_cast<void **>(&host_mat),
+                             (size_t)3 * kMaxSlabRanks * kMaxSlabRanks * sizeof(unsigned long long),
+                             cudaHostAllocMapped | cudaHostAllocPortable));
+      SPB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dev_mat), host_mat, 0));
+    }
+    (void)count;
+    return dev_mat;
+  }
+  virtual ~SlabExchange() {
+    if (host_mat) cudaFreeHost(host_mat);
+  }
   virtual int size() const = 0;
   virtual int rank_of(int local) const = 0;
   // recv[l] (G * bytes) <- every rank's send (bytes); in place allowed when
@@ -362,24 +377,43 @@ __global__ void __launch_bounds__(1024) k_slab_splitters(const uint32_t *__restr
   }
 }
 
+// Warp-aggregated atomic add of 1 per active lane on cnt[key] (lanes with the
+// same key share one atomic); returns the lane's slot among them.
+template <class T>
+__device__ __forceinline__ T agg_add(T *cnt, int key, bool active) {
+  const int lane = threadIdx.x & 31;
+  const unsigned act = __ballot_sync(0xffffffffu, active);
+  const unsigned peers = __match_any_sync(0xffffffffu, active ? key : -1) & act;
+  const int leader = peers ? __ffs(peers) - 1 : lane;
+  T base = 0;
+  if (active && lane == leader) base = atomicAdd(cnt + key, (T)__popc(peers));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return base + (T)__popc(peers & ((1u << lane) - 1u));
+}
+
 // per-destination counts: [0, G) owned, [G, 2G) ghost, [2G, 3G) near owned
 __global__ void __launch_bounds__(256) k_slab_count(const float *__restrict__ pts, int64_t n, Splitters SP,
                                                     unsigned long long *counts) {
   __shared__ unsigned int sc[3 * kMaxSlabRanks];
   __shared__ Route S;
+  for (int i = threadIdx.x; i < 3 * kMaxSlabRanks; i += blockDim.x) sc[i] = 0;
   S.load(SP);
   const int G = SP.G;
-  for (int i = threadIdx.x; i < 3 * G; i += blockDim.x) sc[i] = 0;
-  __syncthreads();
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) {
-    int d, lo, hi;
-    S.route(pts[3 * i], d, lo, hi);
-    atomicAdd(&sc[d], 1u);
-    if (lo != d || hi != d) {
-      atomicAdd(&sc[2 * G + d], 1u);
-      for (int t = lo; t <= hi; ++t)
-        if (t != d) atomicAdd(&sc[G + t], 1u);
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t wb = t0 - (threadIdx.x & 31); wb < n; wb += st) {
+    const int64_t i = wb + (threadIdx.x & 31);
+    const bool valid = i < n;
+    int d = 0, lo = 0, hi = 0;
+    if (valid) S.route(pts[3 * i], d, lo, hi);
+    agg_add(sc, d, valid);
+    const bool near = valid && (lo != d || hi != d);
+    agg_add(sc, 2 * G + d, near);
+    for (int t = lo;; ++t) {
+      if (near && t == d) ++t;
+      const bool more = near && t <= hi;
+      if (!__any_sync(0xffffffffu, more)) break;
+      agg_add(sc, G + t, more);
     }
   }
   __syncthreads();
@@ -391,66 +425,101 @@ struct PackLayout {
   int64_t owned_base[kMaxSlabRanks];  // send position of the owned block for peer d
   int64_t ghost_base[kMaxSlabRanks];  // send position of the ghost block for peer d
   int64_t ret_base[kMaxSlabRanks];    // where peer d's returned labels land
+  // the self block -- rows this rank owns itself, then ghost copies of rows
+  // it holds for slabs it owns -- skips the send buffer and the exchange: it
+  // is written straight into the receive buffer at self_base (owned rows
+  // never return)
+  int me;
+  int64_t self_base, self_owned;
+  float *rxyz;
+  int32_t *rid;
 };
 
-// warp-aggregated slot: lanes with the same key share one atomic
+// warp-aggregated global slot (one atomic per key per warp)
 __device__ __forceinline__ unsigned long long agg_slot(unsigned long long *ctr, int key, bool active) {
-  const unsigned act = __ballot_sync(0xffffffffu, active);
-  const unsigned peers = __match_any_sync(0xffffffffu, active ? key : -1) & act;
-  const int lane = threadIdx.x & 31;
-  unsigned long long base = 0;
-  const int leader = peers ? __ffs(peers) - 1 : lane;
-  if (active && lane == leader) base = atomicAdd(ctr + key, (unsigned long long)__popc(peers));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  return base + __popc(peers & ((1u << lane) - 1u));
+  return agg_add(ctr, key, active);
 }
 
+// Pack a tile of PK_ITEMS x 256 rows per block: slots are reserved per block
+// (one global atomic per destination per block, not per warp) and handed out
+// inside the block by warp-aggregated shared atomics, so the entries of one
+// destination stay in runs of about a tile in input order.
+constexpr int PK_ITEMS = 4;
 __global__ void __launch_bounds__(256) k_slab_pack(const float *__restrict__ pts, int64_t n, int64_t first,
                                                    Splitters SP, PackLayout L, unsigned long long *cursor,
                                                    float *__restrict__ sxyz, int32_t *__restrict__ sid,
                                                    int32_t *__restrict__ slot_of_row) {
   __shared__ Route S;
-  S.load(SP);
+  __shared__ unsigned int cnt[2 * kMaxSlabRanks], gcnt[kMaxSlabRanks];
+  __shared__ unsigned long long base[2 * kMaxSlabRanks];
   const int G = SP.G;
-  const int64_t st = (int64_t)gridDim.x * blockDim.x;
-  // warp-uniform trip count: the base index of the lane's warp drives the loop
-  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (int64_t wb = t0 - (threadIdx.x & 31); wb < n; wb += st) {
-    const int64_t i = wb + (threadIdx.x & 31);
-    const bool valid = i < n;
-    float x = 0.f, y = 0.f, z = 0.f;
-    int d = 0, lo = 0, hi = 0;
-    if (valid) {
-      x = pts[3 * i];
-      y = pts[3 * i + 1];
-      z = pts[3 * i + 2];
-      S.route(x, d, lo, hi);
-    }
-    const unsigned long long off = agg_slot(cursor, d, valid);
-    if (valid) {
-      const int64_t pos = L.owned_base[d] + (int64_t)off;
-      sxyz[3 * pos] = x;
-      sxyz[3 * pos + 1] = y;
-      sxyz[3 * pos + 2] = z;
-      sid[pos] = (int32_t)(first + i);
-      slot_of_row[i] = (int32_t)(L.ret_base[d] + (int64_t)off);
-    }
-    // ghost copies: target t runs over [lo, hi] \ {d}, one round per target
-    int t = lo;
-    while (true) {
-      if (valid && t == d) ++t;
-      const bool more = valid && t <= hi;
-      if (!__any_sync(0xffffffffu, more)) break;
-      const unsigned long long g = agg_slot(cursor + G, t, more);
-      if (more) {
-        const int64_t pos = L.ghost_base[t] + (int64_t)g;
-        sxyz[3 * pos] = x;
-        sxyz[3 * pos + 1] = y;
-        sxyz[3 * pos + 2] = z;
-        sid[pos] = (int32_t)(first + i);
-        ++t;
+  const int64_t tile = (int64_t)blockDim.x * PK_ITEMS;
+  S.load(SP);
+  for (int64_t t0 = (int64_t)blockIdx.x * tile; t0 < n; t0 += (int64_t)gridDim.x * tile) {
+    if (threadIdx.x < 2 * kMaxSlabRanks) cnt[threadIdx.x] = 0;
+    if (threadIdx.x < kMaxSlabRanks) gcnt[threadIdx.x] = 0;
+    __syncthreads();
+    float x[PK_ITEMS], y[PK_ITEMS], z[PK_ITEMS];
+    int d[PK_ITEMS], lo[PK_ITEMS], hi[PK_ITEMS];
+    unsigned off[PK_ITEMS];
+#pragma unroll
+    for (int j = 0; j < PK_ITEMS; ++j) {
+      const int64_t i = t0 + (int64_t)j * blockDim.x + threadIdx.x;
+      const bool valid = i < n;
+      d[j] = lo[j] = 0;
+      hi[j] = -1;  // no ghosts for an invalid row
+      x[j] = y[j] = z[j] = 0.f;
+      if (valid) {
+        x[j] = pts[3 * i];
+        y[j] = pts[3 * i + 1];
+        z[j] = pts[3 * i + 2];
+        S.route(x[j], d[j], lo[j], hi[j]);
+      }
+      off[j] = agg_add(cnt, d[j], valid);
+      for (int t = lo[j];; ++t) {
+        if (valid && t == d[j]) ++t;
+        const bool more = valid && t <= hi[j];
+        if (!__any_sync(0xffffffffu, more)) break;
+        agg_add(cnt, G + t, more);
       }
     }
+    __syncthreads();
+    if (threadIdx.x < 2 * G) base[threadIdx.x] = cnt[threadIdx.x] ? atomicAdd(cursor + threadIdx.x,
+                                                                              (unsigned long long)cnt[threadIdx.x])
+                                                                  : 0ull;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < PK_ITEMS; ++j) {
+      const int64_t i = t0 + (int64_t)j * blockDim.x + threadIdx.x;
+      const bool valid = i < n;
+      if (valid) {
+        const int64_t k = (int64_t)base[d[j]] + off[j];
+        const bool self = d[j] == L.me;
+        const int64_t pos = self ? L.self_base + k : L.owned_base[d[j]] + k;
+        float *xyz = self ? L.rxyz : sxyz;
+        xyz[3 * pos] = x[j];
+        xyz[3 * pos + 1] = y[j];
+        xyz[3 * pos + 2] = z[j];
+        (self ? L.rid : sid)[pos] = (int32_t)(first + i);
+        slot_of_row[i] = self ? -1 : (int32_t)(L.ret_base[d[j]] + k);
+      }
+      for (int t = lo[j];; ++t) {  // ghost copies: one round per target slab
+        if (valid && t == d[j]) ++t;
+        const bool more = valid && t <= hi[j];
+        if (!__any_sync(0xffffffffu, more)) break;
+        const unsigned g = agg_add(gcnt, t, more);
+        if (more) {
+          const bool self = t == L.me;
+          const int64_t pos = (self ? L.self_base + L.self_owned : L.ghost_base[t]) + (int64_t)base[G + t] + g;
+          float *xyz = self ? L.rxyz : sxyz;
+          xyz[3 * pos] = x[j];
+          xyz[3 * pos + 1] = y[j];
+          xyz[3 * pos + 2] = z[j];
+          (self ? L.rid : sid)[pos] = (int32_t)(first + i);
+        }
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -543,9 +612,10 @@ __global__ void k_slab_comp(const uint64_t *__restrict__ slab, int64_t m, const 
 
 // Owned entries: final label (component minimum when the local label is
 // linked, else the local label), written to the return block of its source.
-__global__ void k_slab_relabel(const int32_t *__restrict__ rlab, int64_t nrecv, RecvLayout R,
-                               const uint64_t *__restrict__ slab, const int32_t *__restrict__ comp, int64_t m,
-                               int32_t *__restrict__ ret) {
+__global__ void k_slab_relabel(const int32_t *__restrict__ rlab, const int32_t *__restrict__ rid, int64_t nrecv,
+                               RecvLayout R, const uint64_t *__restrict__ slab, const int32_t *__restrict__ comp,
+                               int64_t m, int32_t *__restrict__ ret, int me, int64_t first,
+                               int32_t *__restrict__ labels, uint8_t *__restrict__ core) {
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nrecv; j += st) {
     const int p = R.seg(j);
@@ -556,7 +626,13 @@ __global__ void k_slab_relabel(const int32_t *__restrict__ rlab, int64_t nrecv, 
       const int64_t pos = lower_bound_u64(slab, m, (uint64_t)a);
       if (pos < m && slab[pos] == (uint64_t)a) a = comp[pos];
     }
-    ret[R.ret_off[p] + k] = a;
+    if (p == me) {  // this rank's own rows: final labels in input order
+      const int64_t row = (int64_t)rid[j] - first;
+      labels[row] = a;
+      core[row] = a >= 0;
+    } else {
+      ret[R.ret_off[p] + k] = a;
+    }
   }
 }
 
@@ -564,10 +640,16 @@ __global__ void k_slab_unpack(const int32_t *__restrict__ slot_of_row, const int
                               int32_t *__restrict__ labels, uint8_t *__restrict__ core) {
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) {
-    const int32_t l = ret[slot_of_row[i]];
+    const int32_t s = slot_of_row[i];
+    if (s < 0) continue;  // a row this rank owns itself (k_slab_relabel wrote it)
+    const int32_t l = ret[s];
     labels[i] = l;
     core[i] = l >= 0;
   }
+}
+
+__global__ void k_copy_u64(const unsigned long long *__restrict__ src, unsigned long long *dst, int count) {
+  for (int i = threadIdx.x; i < count; i += blockDim.x) dst[i] = src[i];
 }
 
 __global__ void k_iota_i32(int32_t *a, int64_t n) {
@@ -675,9 +757,10 @@ void fof_slabs(std::vector<SlabInput> &inputs, SlabExchange &ex, float eps) {
   std::vector<unsigned long long> mat((size_t)3 * G * G);
   {
     ScopedDevice sd(ctx[0]->device);
-    SPB_CUDA(cudaMemcpyAsync(mat.data(), R[0]->cmat.get(), mat.size() * sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, ctx[0]->stream));
+    k_copy_u64<<<1, 256, 0, ctx[0]->stream>>>(R[0]->cmat.get(), ex.mapped(mat.size()), (int)mat.size());
+    SPB_LAUNCHED();
     SPB_CUDA(cudaStreamSynchronize(ctx[0]->stream));
+    std::memcpy(mat.data(), ex.host_mat, mat.size() * sizeof(unsigned long long));
   }
   auto owned = [&](int src, int dst) { return (int64_t)mat[(size_t)src * 3 * G + dst]; };
   auto ghost = [&](int src, int dst) { return (int64_t)mat[(size_t)src * 3 * G + G + dst]; };
@@ -700,27 +783,34 @@ void fof_slabs(std::vector<SlabInput> &inputs, SlabExchange &ex, float eps) {
     r.sbytes.assign(G, 0);
     r.roff.assign(G, 0);
     r.rbytes.assign(G, 0);
+    // send blocks per peer; the self block is written straight into the
+    // receive buffer
     for (int d = 0; d < G; ++d) {
+      const bool self = d == me;
       PL[l].owned_base[d] = pos;
-      PL[l].ghost_base[d] = pos + owned(me, d);
+      PL[l].ghost_base[d] = pos + (self ? 0 : owned(me, d));
       PL[l].ret_base[d] = ret;
       r.soff[d] = (size_t)pos;
-      r.sbytes[d] = (size_t)(owned(me, d) + ghost(me, d));
-      pos += owned(me, d) + ghost(me, d);
-      ret += owned(me, d);
+      r.sbytes[d] = self ? 0 : (size_t)(owned(me, d) + ghost(me, d));
+      pos += (int64_t)r.sbytes[d];
+      ret += self ? 0 : owned(me, d);
     }
     int64_t rpos = 0, rret = 0;
     RL[l].G = G;
     for (int p = 0; p < G; ++p) {
+      const bool self = p == me;
       RL[l].seg_start[p] = rpos;
       RL[l].owned[p] = owned(p, me);
       RL[l].ret_off[p] = rret;
       r.roff[p] = (size_t)rpos;
-      r.rbytes[p] = (size_t)(owned(p, me) + ghost(p, me));
+      r.rbytes[p] = self ? 0 : (size_t)(owned(p, me) + ghost(p, me));
+      if (self) PL[l].self_base = rpos;
       rpos += owned(p, me) + ghost(p, me);
-      rret += owned(p, me);
+      rret += self ? 0 : owned(p, me);
     }
     RL[l].seg_start[G] = rpos;
+    PL[l].me = me;
+    PL[l].self_owned = owned(me, me);
     r.nrecv = rpos;
   }
   each([&](int l, SlabRank &r, Ctx &c) {
@@ -733,8 +823,10 @@ void fof_slabs(std::vector<SlabInput> &inputs, SlabExchange &ex, float eps) {
     r.rid = DevBuf<int32_t>((size_t)std::max<int64_t>(r.nrecv, 1), c.stream);
     r.cursor = DevBuf<unsigned long long>(2 * G, c.stream);
     SPB_CUDA(cudaMemsetAsync(r.cursor.get(), 0, 2 * G * sizeof(unsigned long long), c.stream));
+    PL[l].rxyz = r.rxyz.get();
+    PL[l].rid = r.rid.get();
     if (r.in.n > 0) {
-      k_slab_pack<<<grid_for(r.in.n, 256, 148 * 8), 256, 0, c.stream>>>(r.in.pts, r.in.n, r.in.first, r.S, PL[l],
+      k_slab_pack<<<grid_for((r.in.n + PK_ITEMS - 1) / PK_ITEMS, 256, 148 * 8), 256, 0, c.stream>>>(r.in.pts, r.in.n, r.in.first, r.S, PL[l],
                                                                          r.cursor.get(), r.sxyz.get(), r.sid.get(),
                                                                          r.slot_of_row.get());
       SPB_LAUNCHED();
@@ -835,11 +927,12 @@ void fof_slabs(std::vector<SlabInput> &inputs, SlabExchange &ex, float eps) {
       SPB_LAUNCHED();
     }
     int64_t nret_send = 0;
-    for (int p = 0; p < G; ++p) nret_send += RL[l].owned[p];
+    for (int p = 0; p < G; ++p) nret_send += p == r.rank ? 0 : RL[l].owned[p];
     r.ret_send = DevBuf<int32_t>((size_t)std::max<int64_t>(nret_send, 1), c.stream);
     if (r.nrecv > 0) {
-      k_slab_relabel<<<grid_for(r.nrecv, 256, 148 * 8), 256, 0, c.stream>>>(r.rlab.get(), r.nrecv, RL[l], slabels,
-                                                                             comp.get(), M, r.ret_send.get());
+      k_slab_relabel<<<grid_for(r.nrecv, 256, 148 * 8), 256, 0, c.stream>>>(
+          r.rlab.get(), r.rid.get(), r.nrecv, RL[l], slabels, comp.get(), M, r.ret_send.get(), r.rank, r.in.first,
+          r.in.labels, r.in.core);
       SPB_LAUNCHED();
     }
     r.ret_recv = DevBuf<int32_t>((size_t)std::max<int64_t>(r.in.n, 1), c.stream);
@@ -861,15 +954,17 @@ void fof_slabs(std::vector<SlabInput> &inputs, SlabExchange &ex, float eps) {
       rcv.push_back(r.ret_recv.get());
       for (int p = 0; p < G; ++p) {
         so[l].push_back((size_t)RL[l].ret_off[p] * 4);
-        sb[l].push_back((size_t)owned(p, me) * 4);
+        sb[l].push_back(p == me ? 0 : (size_t)owned(p, me) * 4);
         ro[l].push_back((size_t)PL[l].ret_base[p] * 4);
-        rb[l].push_back((size_t)owned(me, p) * 4);
+        rb[l].push_back(p == me ? 0 : (size_t)owned(me, p) * 4);
       }
     }
     ex.alltoallv(ctx, snd, so, sb, rcv, ro, rb);
   }
   each([&](int l, SlabRank &r, Ctx &c) {
-    if (r.in.n > 0) {
+    int64_t from_peers = 0;  // rows of this rank owned elsewhere
+    for (int p = 0; p < G; ++p) from_peers += p == r.rank ? 0 : owned(r.rank, p);
+    if (from_peers > 0) {
       k_slab_unpack<<<grid_for(r.in.n, 256, 148 * 8), 256, 0, c.stream>>>(r.slot_of_row.get(), r.ret_recv.get(),
                                                                            r.in.n, r.in.labels, r.in.core);
       SPB_LAUNCHED();

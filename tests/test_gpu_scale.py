@@ -100,3 +100,37 @@ def test_fof_cells_equal_point_pipeline(sp, shape, mult):
     b = sp.friends_of_friends(p, eps, algorithm="points")
     assert torch.equal(a.labels, b.labels), (shape, mult)
     assert torch.equal(a.core_flags, b.core_flags), (shape, mult)
+
+
+@pytest.mark.parametrize("key", ["H_2^27", "H_2^30"])
+def test_field_fof_against_reference_pin(sp, key):
+    # the SURVEY field H(n) at the bench size (2^27) and at C5's full size
+    # (2^30, 1.07 B points, one GPU): labels, core flags and counts equal the
+    # unmodified reference's friends_of_friends on the same input
+    # (scripts/ref_pin*.py, run on the GPU host); then the same rows through
+    # the slab pipeline at one rank (sp_fof_slabs_multi, the device path of
+    # sp_fof_slabs) give the same labels.
+    import torch
+    from paper_2409_10743_b200.distributed import fof_slabs_multi
+    g = golden_hashes()[key]
+    n = g["n"]
+    eps = eps_for(n)
+    torch.cuda.empty_cache()
+    pts = torch.from_numpy(sp.generate_reference_field(n)).cuda()
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    core = torch.empty(n, dtype=torch.uint8, device="cuda")
+    ctx = sp.Context(0)
+    sp.friends_of_friends(pts, eps, ctx=ctx, out=(lab, core))
+    ctx.close()
+    hl, hc = lab.cpu().numpy(), core.cpu().numpy()
+    assert summarize(hl, hc) == (g["clusters"], g["noise"], g["core"])
+    assert fnv1a64(hc) == g["core_hash"]
+    assert fnv1a64(hl) == g["labels_hash"]
+    del hl, hc
+    lab.fill_(-2)
+    core.fill_(2)
+    ctx = sp.Context(0)
+    fof_slabs_multi([pts], eps, ctxs=[ctx], out=[(lab, core)])
+    ctx.close()
+    assert fnv1a64(core.cpu().numpy()) == g["core_hash"]
+    assert fnv1a64(lab.cpu().numpy()) == g["labels_hash"]
