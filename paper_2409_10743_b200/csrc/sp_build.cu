@@ -767,7 +767,7 @@ void build_sorted_hierarchy(Ctx &c, const uint64_t *keys, int64_t m, int dim, co
   t.stream = c.stream;
   if (m == 0) return;
   t.nodes = static_cast<decltype(t.nodes)>(cache_alloc((size_t)(2 * m - 1) * 2 * sizeof(float4), c.stream));
-  t.perm = static_cast<decltype(t.perm)>(cache_alloc((size_t)m * sizeof(int32_t), c.stream));
+  // leaves are the objects in order: no permutation array (t.perm stays null)
   DevBuf<int32_t> own_delta, flags(m > 1 ? m - 1 : 1, c.stream);
   DevBuf<int32_t> &delta = delta_in ? *delta_in : own_delta;
   if (!delta_in) own_delta = DevBuf<int32_t>(m > 1 ? m - 1 : 1, c.stream);
@@ -780,7 +780,7 @@ void build_sorted_hierarchy(Ctx &c, const uint64_t *keys, int64_t m, int dim, co
   }
   ClimbQueue q(c, m, 6);
   k_hierarchy<false><<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(m, delta.get(), nullptr, boxes, dim, t.nodes,
-                                                                        flags.get(), t.perm, nullptr, q.levels,
+                                                                        flags.get(), nullptr, nullptr, q.levels,
                                                                         q.buf.get(), q.count.get());
   SPB_LAUNCHED();
   q.finish(c, m, delta.get(), t.nodes, flags.get());

@@ -56,9 +56,9 @@ __global__ void __launch_bounds__(128, 1) k_core_flags(const float4 *__restrict_
         if (cur >= first_leaf) {
           const int64_t q = cur - first_leaf;
           const float4 L = ld_node(leafpt, q);
-          cur = __float_as_int(L.w);
-          if (q >= w_lo && q <= w_hi) continue;
-          if (hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z) && ++c == min_pts) break;
+          const bool counted = q >= w_lo && q <= w_hi;  // in the Morton window above
+          if (!counted && hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z) && ++c == min_pts) cur = kSentinel;
+          else cur = __float_as_int(L.w);
         } else {
           const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
           cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);

@@ -1313,7 +1313,7 @@ __global__ void __launch_bounds__(128) k_cells_core(const float4 *__restrict__ n
           const float4 q = cpts[j];
           cnt += hit_point(R, me.x, me.y, me.z, q.x, q.y, q.z);
         }
-        if (cnt >= min_pts) break;
+        if (cnt >= min_pts) cur = kSentinel;  // through the loop test, not a break
       }
     }
     corep[k] = cnt >= min_pts;

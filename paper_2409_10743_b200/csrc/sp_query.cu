@@ -76,8 +76,7 @@ __device__ __forceinline__ void range_count_one(const float4 *__restrict__ nodes
       const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
       const bool hit = box_touch(lo, hi, b);
       if (cur >= n - 1) {
-        if (hit && ++c == cap) break;
-        cur = node_rope(hi);
+        cur = (hit && ++c == cap) ? kSentinel : node_rope(hi);
       } else {
         cur = hit ? node_link(lo) : node_rope(hi);
       }

@@ -108,8 +108,9 @@ __device__ __forceinline__ int32_t count_sphere(const float4 *__restrict__ nodes
         hit = hit_box(R, cx, cy, cz, lo, hi);
         next = node_rope(hi);
       }
-      if (hit && ++c == cap) break;
-      cur = next;
+      // cap reached: end the walk through the loop test (a break here costs
+      // the warp its per-iteration reconvergence)
+      cur = (hit && ++c == cap) ? kSentinel : next;
     } else {
       const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
       cur = maybe_box(R, cx, cy, cz, lo, hi) ? node_link(lo) : node_rope(hi);
