@@ -589,32 +589,79 @@ struct HierView {
 // second knows the parent's full range [l, r] and split, recovers its Karras
 // index (r for a left child, l for a right child, 0 for the root), joins the
 // two child boxes left-first and writes {box, left, rope}.
-// Climbs at most max_levels merges; returns true when this thread still owns
-// a node whose parent is not built yet (the state in l, r, lo, hi).
+// Climbs at most max_levels merges through the global flags; returns true
+// when this thread still owns a node whose parent is not built yet (the state
+// in l, r, lo, hi).
+//
+// Block-local hand-off (k_hierarchy): a CTA owns the leaves [B, B + BLK).
+// When a parent lies inside, its two children meet in shared memory (box
+// slots and a flag exchanged with CTA-scope acquire/release: no L2 round trip,
+// no L1 invalidation); otherwise both use the global flag.  Both children must
+// choose alike, so the choice is a property of the split: the parent at split
+// a (the lowest common ancestor of leaves a and a + 1, prefix length D(a))
+// spans [l'', r''] with l'' - 1 = max{j < a : D(j) < D(a)} and r'' = min{j > a
+// : D(j) < D(a)} (D(-1) = D(n-1) = -1; equal lengths are always separated by a
+// smaller one).  It lies inside the CTA iff the CTA holds a smaller split
+// length on each side of a: prefix and suffix minima of the CTA's staged
+// D(B-1 .. B+BLK-1), computed once per CTA.
+constexpr int CLIMB_BLK = 256;
+struct LocalClimb {
+  int64_t B;
+  const uint8_t *in;  // [CLIMB_BLK] shared: the parent at split B + i lies inside
+  int32_t *flag;      // [CLIMB_BLK] shared flags, -1 = empty
+  float *box;         // [2][CLIMB_BLK][6] shared child boxes (0 = left, 1 = right)
+  __device__ __forceinline__ bool inside(int64_t a) const { return a >= B && a < B + CLIMB_BLK && in[a - B]; }
+};
+
+__device__ __forceinline__ int32_t exch_acq_rel_gpu(int32_t *p, int32_t v) {
+  int32_t old;
+  asm volatile("atom.acq_rel.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ int32_t exch_acq_rel_cta_shared(int32_t *p, int32_t v) {
+  int32_t old;
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  asm volatile("atom.acq_rel.cta.shared::cta.exch.b32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+  return old;
+}
+
+template <bool LOCAL>
 __device__ __forceinline__ bool climb(const HierView &H, int64_t &l, int64_t &r, float lo[3], float hi[3],
-                                      float4 *nodes, int32_t *flags, int max_levels) {
+                                      float4 *nodes, int32_t *flags, int max_levels, const LocalClimb &lc) {
   const int64_t n = H.n;
-  for (int level = 0; level < max_levels; ++level) {
+  for (int level = 0; level < max_levels;) {
     const bool L = H.is_left(l, r);
     const int64_t a = L ? r : l - 1;  // the parent's split position
-    // Acquire-release exchange: the release half orders this node's box
+    const int32_t bound = (int32_t)(L ? l : r);
+    // Acquire-release exchanges: the release half orders this node's box
     // stores before the flag changes hands; the acquire half orders the second
     // arrival's reads of the sibling box after the first arrival's stores (the
     // PTX memory model gives no ordering through the address dependency
-    // alone).  The sibling box is read with L2-coherent loads.
-    int32_t other;
-    asm volatile("atom.acq_rel.gpu.global.exch.b32 %0, [%1], %2;"
-                 : "=r"(other)
-                 : "l"(flags + a), "r"((int32_t)(L ? l : r))
-                 : "memory");
-    if (other < 0) return false;  // first arrival
-    if (L) r = other;
-    else l = other;
+    // alone).  The global sibling box is read with L2-coherent loads.
+    const bool local = LOCAL && lc.inside(a);
+    float4 slo, shi;
+    if (local) {
+      float *mine = lc.box + ((L ? 0 : CLIMB_BLK) + (a - lc.B)) * 6;
+      mine[0] = lo[0]; mine[1] = lo[1]; mine[2] = lo[2];
+      mine[3] = hi[0]; mine[4] = hi[1]; mine[5] = hi[2];
+      const int32_t other = exch_acq_rel_cta_shared(lc.flag + (a - lc.B), bound);
+      if (other < 0) return false;  // first arrival: the sibling is inside and will come
+      if (L) r = other;
+      else l = other;
+      const float *sb = lc.box + ((L ? CLIMB_BLK : 0) + (a - lc.B)) * 6;
+      slo = make_float4(sb[0], sb[1], sb[2], 0.f);
+      shi = make_float4(sb[3], sb[4], sb[5], 0.f);
+    } else {
+      const int32_t other = exch_acq_rel_gpu(flags + a, bound);
+      if (other < 0) return false;  // first arrival
+      if (L) r = other;
+      else l = other;
+      const int64_t sib = L ? ((a + 1 == r) ? n - 1 + r : a + 1) : ((a == l) ? n - 1 + l : a);
+      slo = __ldcg(nodes + 2 * sib);
+      shi = __ldcg(nodes + 2 * sib + 1);
+      ++level;
+    }
     const int64_t left = (a == l) ? n - 1 + l : a;
-    const int64_t right = (a + 1 == r) ? n - 1 + r : a + 1;
-    const int64_t sib = L ? right : left;
-    const float4 slo = __ldcg(nodes + 2 * sib);
-    const float4 shi = __ldcg(nodes + 2 * sib + 1);
     if (L) {  // this node is the left child
       lo[0] = keep_min(lo[0], slo.x); lo[1] = keep_min(lo[1], slo.y); lo[2] = keep_min(lo[2], slo.z);
       hi[0] = keep_max(hi[0], shi.x); hi[1] = keep_max(hi[1], shi.y); hi[2] = keep_max(hi[2], shi.z);
@@ -645,19 +692,51 @@ __global__ void __launch_bounds__(256) k_climb_rest(int64_t n, const int32_t *__
   const float4 s0 = queue[2 * i], s1 = queue[2 * i + 1];
   int64_t l = __float_as_int(s0.x), r = __float_as_int(s0.y);
   float lo[3] = {s0.z, s0.w, s1.x}, hi[3] = {s1.y, s1.z, s1.w};
-  climb(H, l, r, lo, hi, nodes, flags, 1 << 30);
+  climb<false>(H, l, r, lo, hi, nodes, flags, 1 << 30, LocalClimb{0, nullptr, nullptr, nullptr});
 }
 
 template <bool POINTS>
-__global__ void __launch_bounds__(256) k_hierarchy(int64_t n, const int32_t *__restrict__ delta,
+__global__ void __launch_bounds__(CLIMB_BLK) k_hierarchy(int64_t n, const int32_t *__restrict__ delta,
                                                    const uint32_t *__restrict__ perm, const float *__restrict__ obj,
                                                    int dim, float4 *nodes, int32_t *flags,
                                                    int32_t *__restrict__ perm_out, float4 *__restrict__ leafpt,
                                                    int max_levels, float4 *__restrict__ queue,
                                                    uint32_t *__restrict__ qcount) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ int32_t s_flag[CLIMB_BLK];
+  __shared__ int32_t s_D[CLIMB_BLK + 1], s_pre[CLIMB_BLK], s_suf[CLIMB_BLK + 1], s_wmin[2][CLIMB_BLK / 32];
+  __shared__ uint8_t s_in[CLIMB_BLK];
+  __shared__ float s_box[2 * CLIMB_BLK * 6];
+  const HierView H{n, delta};
+  const int64_t B = (int64_t)blockIdx.x * CLIMB_BLK;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  s_flag[t] = -1;
+  const int32_t dv = H.D(B - 1 + t);  // element t of D(B-1 .. B+BLK-1)
+  s_D[t] = dv;
+  if (t == 0) s_D[CLIMB_BLK] = H.D(B + CLIMB_BLK - 1);
+  // inclusive prefix / suffix minima over the 256 elements (warp scans, then
+  // the warp totals), suffix also over the last element s_D[BLK]
+  int32_t pm = dv, sm = dv;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, pm, o), z = __shfl_down_sync(0xffffffffu, sm, o);
+    if (lane >= o) pm = min(pm, y);
+    if (lane + o < 32) sm = min(sm, z);
+  }
+  if (lane == 31) s_wmin[0][w] = pm;
+  if (lane == 0) s_wmin[1][w] = sm;
+  __syncthreads();
+  for (int k = 0; k < w; ++k) pm = min(pm, s_wmin[0][k]);
+  for (int k = w + 1; k < CLIMB_BLK / 32; ++k) sm = min(sm, s_wmin[1][k]);
+  s_pre[t] = pm;
+  s_suf[t] = min(sm, s_D[CLIMB_BLK]);
+  if (t == 0) s_suf[CLIMB_BLK] = s_D[CLIMB_BLK];
+  __syncthreads();
+  // split a = B + t: D(a) = s_D[t + 1]; left minimum over D(B-1 .. a-1) =
+  // s_pre[t], right minimum over D(a+1 .. B+BLK-1) = s_suf[t + 2]
+  s_in[t] = t + 1 < CLIMB_BLK && s_pre[t] < s_D[t + 1] && s_suf[t + 2] < s_D[t + 1];
+  __syncthreads();
+  const int64_t p = B + threadIdx.x;
   if (p >= n) return;
-  HierView H{n, delta};
   const uint32_t oi = perm ? perm[p] : (uint32_t)p;
   if (perm_out) perm_out[p] = (int32_t)oi;
   const int sz = POINTS ? dim : 2 * dim;
@@ -674,18 +753,26 @@ __global__ void __launch_bounds__(256) k_hierarchy(int64_t n, const int32_t *__r
   if (POINTS) leafpt[p] = make_float4(lo[0], lo[1], lo[2], __int_as_float(leaf_rope));
   if (n == 1) return;
   int64_t l = p, r = p;
-  if (climb(H, l, r, lo, hi, nodes, flags, max_levels)) {
+  const LocalClimb lc{B, s_in, s_flag, s_box};
+  if (climb<true>(H, l, r, lo, hi, nodes, flags, max_levels, lc)) {
     const uint32_t slot = atomicAdd(qcount, 1u);
     queue[2 * (int64_t)slot] = make_float4(__int_as_float((int)l), __int_as_float((int)r), lo[0], lo[1]);
     queue[2 * (int64_t)slot + 1] = make_float4(lo[2], hi[0], hi[1], hi[2]);
   }
 }
 
-// The two-kernel climb: k_hierarchy climbs `levels` merges per leaf, the
-// survivors (<= n / (levels + 1): their nodes are disjoint subtrees of
-// >= levels + 1 leaves) are queued and finished by k_climb_rest.
-// Measured best at 2^27: 8 levels for point trees (hierarchy 11.3 -> 10.7 ms),
-// 6 for the cell tree of the FoF grid (9.9 -> 9.3 ms).
+// The two-kernel climb: k_hierarchy climbs every block-local merge and at most
+// `levels` merges through the global flags per leaf; the survivors (<= n /
+// (levels + 1): their nodes are disjoint subtrees of >= levels + 1 leaves) are
+// queued and finished by k_climb_rest.  With the block-local hand-off, one
+// global level is best at 2^27 (hierarchy phase 13.1 -> 11.1 ms for point
+// trees, 9.5 -> 9.1 ms for the FoF cell tree; 2, 4 and 8 levels are slower).
+#ifndef SPB_CLIMB_LEVELS_POINTS
+#define SPB_CLIMB_LEVELS_POINTS 1
+#endif
+#ifndef SPB_CLIMB_LEVELS_CELLS
+#define SPB_CLIMB_LEVELS_CELLS 1
+#endif
 struct ClimbQueue {
   int levels = 8;
   int64_t cap = 0;
@@ -746,7 +833,7 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
     SPB_CUDA(cudaMemsetAsync(flags.get(), 0xff, (size_t)(n - 1) * sizeof(int32_t), c.stream));
   }
   unsigned g = (unsigned)((n + 255) / 256);
-  ClimbQueue q(c, n, 8);
+  ClimbQueue q(c, n, SPB_CLIMB_LEVELS_POINTS);
   if (points)
     k_hierarchy<true><<<g, 256, 0, c.stream>>>(n, delta.get(), va, objects, dim, t.nodes, flags.get(), t.perm,
                                                t.leafpt, q.levels, q.buf.get(), q.count.get());
@@ -778,7 +865,7 @@ void build_sorted_hierarchy(Ctx &c, const uint64_t *keys, int64_t m, int dim, co
     }
     SPB_CUDA(cudaMemsetAsync(flags.get(), 0xff, (size_t)(m - 1) * sizeof(int32_t), c.stream));
   }
-  ClimbQueue q(c, m, 6);
+  ClimbQueue q(c, m, SPB_CLIMB_LEVELS_CELLS);
   k_hierarchy<false><<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(m, delta.get(), nullptr, boxes, dim, t.nodes,
                                                                         flags.get(), nullptr, nullptr, q.levels,
                                                                         q.buf.get(), q.count.get());
