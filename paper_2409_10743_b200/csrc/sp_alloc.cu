@@ -100,6 +100,12 @@ void *cache_alloc(size_t bytes, cudaStream_t s) {
   return p;
 }
 
+void cache_drain() {
+  Cache &c = cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  drain_all(c);
+}
+
 void cache_free(void *p, cudaStream_t s) {
   if (!p) return;
   Cache &c = cache();

@@ -57,7 +57,13 @@ spb::Ctx::Staging &stage(spb::Ctx &c, bool input, size_t bytes) {
     if (s.p) SPB_CUDA(cudaFree(s.p));
     s.p = nullptr;
     s.cap = 0;
-    SPB_CUDA(cudaMalloc(&s.p, bytes));
+    if (cudaMalloc(&s.p, bytes) != cudaSuccess) {
+      // out of memory: other streams' cached scratch blocks may hold it
+      cudaGetLastError();
+      spb::cache_drain();
+      SPB_CUDA(cudaDeviceSynchronize());
+      SPB_CUDA(cudaMalloc(&s.p, bytes));
+    }
     s.cap = bytes;
   }
   return s;

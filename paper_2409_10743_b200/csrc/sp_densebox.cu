@@ -722,7 +722,7 @@ __device__ __forceinline__ void fof_cell_walk(const float4 *__restrict__ nodes, 
   const int64_t sa = cell_start[a], ea = a + 1 < m ? cell_start[a + 1] : n;
   int32_t root = (int32_t)a;
   int32_t cur = node_rope(qhi);
-  int64_t visits = 0, tests = 0;
+  int64_t visits = 0, tests = 0, nfar = 0, nleaf = 0, tail = 0;
   // One exit (the loop test) and the leaf work as the only conditional
   // block: an early exit inside the body lets the compiler drop the warp's
   // per-iteration reconvergence (no BSSY/BSYNC around the body in the SASS),
@@ -732,6 +732,11 @@ __device__ __forceinline__ void fof_cell_walk(const float4 *__restrict__ nodes, 
     const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
     const bool far = cells_far(R, qlo, qhi, lo, hi);
     const bool descend = !far && cur < first_leaf;
+    if (STATS) {
+      nfar += far;
+      nleaf += !far && !descend;
+      tail = far ? tail + 1 : 0;
+    }
     if (!far && !descend)
       root = cells_leaf<STATS>(cell_start, m, n, cpts, R, parent, sa, ea, root, (int32_t)(cur - first_leaf), &tests);
     cur = descend ? node_link(lo) : node_rope(hi);
@@ -739,6 +744,9 @@ __device__ __forceinline__ void fof_cell_walk(const float4 *__restrict__ nodes, 
   if (STATS) {
     atomicAdd(stats, (unsigned long long)visits);
     atomicAdd(stats + 1, (unsigned long long)tests);
+    atomicAdd(stats + 2, (unsigned long long)nfar);
+    atomicAdd(stats + 3, (unsigned long long)nleaf);
+    atomicAdd(stats + 4, (unsigned long long)tail);
   }
 }
 
@@ -1166,16 +1174,19 @@ bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t 
   {
     const Radius R = make_radius(eps);
     if (c.stats()) {
-      DevBuf<unsigned long long> st(2, c.stream);
-      SPB_CUDA(cudaMemsetAsync(st.get(), 0, 2 * sizeof(unsigned long long), c.stream));
+      DevBuf<unsigned long long> st(5, c.stream);
+      SPB_CUDA(cudaMemsetAsync(st.get(), 0, 5 * sizeof(unsigned long long), c.stream));
       auto kern = R.fast ? k_fof_cells_merge_stats<true> : k_fof_cells_merge_stats<false>;
       kern<<<(unsigned)((m + 127) / 128), 128, 0, c.stream>>>(g.t.nodes, m, g.cell_start.get(), n, g.cpts.get(), R,
                                                               parent.get(), st.get());
       SPB_LAUNCHED();
-      unsigned long long hs[2] = {0, 0};
+      unsigned long long hs[5] = {0, 0, 0, 0, 0};
       peek(c, {{st.get(), hs, sizeof(hs)}});
       c.count("merge_node_visits", (int64_t)hs[0]);
       c.count("merge_pair_tests", (int64_t)hs[1]);
+      c.count("merge_far_visits", (int64_t)hs[2]);
+      c.count("merge_leaf_visits", (int64_t)hs[3]);
+      c.count("merge_tail_visits", (int64_t)hs[4]);
     } else if (SPB_MERGE_SM && m >= SPB_SM_MIN_ITEMS) {
       SmSlices sl(c);
       if (R.fast)

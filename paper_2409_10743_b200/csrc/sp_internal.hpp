@@ -80,6 +80,7 @@ void cache_register_stream(cudaStream_t s);
 void cache_unregister_stream(cudaStream_t s);
 void *cache_alloc(size_t bytes, cudaStream_t s);  // throws CudaError
 void cache_free(void *p, cudaStream_t s);
+void cache_drain();  // return every cached block of every stream to the driver
 
 template <class T>
 struct DevBuf {
