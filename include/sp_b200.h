@@ -55,6 +55,16 @@ enum { SP_FLAG_ASYNC = 1, SP_FLAG_STATS = 2 };
  * DENSEBOX_MIXED is fdbscan_densebox over the reference's mixed tree of dense
  * cells and sparse points (dbscan.hpp:298-449), equivalent results. */
 enum { SP_ALGO_FDBSCAN = 0, SP_ALGO_FOF = 1, SP_ALGO_DENSEBOX = 2, SP_ALGO_FOF_POINTS = 3, SP_ALGO_DENSEBOX_MIXED = 4 };
+/* OR'ed into the selector: ExecMode::kSequential (exec.hpp:12).  FDBSCAN with
+ * min_pts > 2 then assigns every border point to the cluster of its core
+ * neighbour of smallest leaf position, which is the claim the reference's
+ * sequential pair traversal makes (dbscan.hpp:123-137, traversal.hpp:162-184):
+ * labels equal the reference's sequential labels bit for bit.  DENSEBOX and
+ * DENSEBOX_MIXED with min_pts > 2 run over the reference's mixed tree and give
+ * a border point to the core neighbour the reference's sequential merge
+ * (dbscan.hpp:406-442) reports first: bit-identical labels too.  Friends-of-
+ * friends is deterministic in both modes. */
+enum { SP_ALGO_SEQUENTIAL = 0x100 };
 
 /* Range predicate kinds (traversal.hpp:25-28: variant<Sphere, Aabb>). */
 enum { SP_PRED_SPHERE = 0, SP_PRED_BOX = 1 };

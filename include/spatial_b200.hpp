@@ -78,7 +78,10 @@ inline Aabb<Dim> point_box(const Point<Dim> &p) {
 }
 
 enum class CodeWidth : int { k32 = 32, k64 = 64 };
-enum class ExecMode { kSequential, kParallel };  // accepted for signature parity; the GPU is always parallel
+// The GPU always runs in parallel; kSequential selects the deterministic
+// border assignment of the reference's sequential run where results differ
+// (fdbscan with min_pts > 2; friends_of_friends is deterministic anyway).
+enum class ExecMode { kSequential, kParallel };
 enum class CallbackControl { kContinue, kTerminateQuery };
 
 struct NodeRef {
@@ -509,10 +512,13 @@ DbscanOutput run_dbscan(std::span<const Point<Dim>> pts, float eps, std::int32_t
 }
 }  // namespace detail
 
+// ExecMode::kSequential: the reference's deterministic sequential labels
+// (sp_b200.h SP_ALGO_SEQUENTIAL); kParallel: any valid border assignment.
 template <int Dim>
 DbscanOutput fdbscan(std::span<const Point<Dim>> points, const DbscanParams &params,
-                     ExecMode = ExecMode::kParallel, CodeWidth width = CodeWidth::k64) {
-  return detail::run_dbscan<Dim>(points, params.eps, params.min_pts, SP_ALGO_FDBSCAN, width);
+                     ExecMode mode = ExecMode::kParallel, CodeWidth width = CodeWidth::k64) {
+  const int seq = mode == ExecMode::kSequential ? SP_ALGO_SEQUENTIAL : 0;
+  return detail::run_dbscan<Dim>(points, params.eps, params.min_pts, SP_ALGO_FDBSCAN | seq, width);
 }
 
 template <int Dim>
@@ -523,8 +529,9 @@ DbscanOutput friends_of_friends(std::span<const Point<Dim>> points, float eps, E
 
 template <int Dim>
 DbscanOutput fdbscan_densebox(std::span<const Point<Dim>> points, const DbscanParams &params,
-                              ExecMode = ExecMode::kParallel, CodeWidth width = CodeWidth::k64) {
-  return detail::run_dbscan<Dim>(points, params.eps, params.min_pts, SP_ALGO_DENSEBOX, width);
+                              ExecMode mode = ExecMode::kParallel, CodeWidth width = CodeWidth::k64) {
+  const int seq = mode == ExecMode::kSequential ? SP_ALGO_SEQUENTIAL : 0;
+  return detail::run_dbscan<Dim>(points, params.eps, params.min_pts, SP_ALGO_DENSEBOX | seq, width);
 }
 
 }  // namespace spatial_b200

@@ -83,6 +83,8 @@ int dbscan_t(const float *v, int64_t n, float eps, int32_t min_pts, int algo, in
   try {
     std::span<const Point<Dim>> s(pts);
     if (algo == 0) out = fdbscan(s, DbscanParams{eps, min_pts});
+    else if (algo == 5) out = fdbscan(s, DbscanParams{eps, min_pts}, ExecMode::kSequential);
+    else if (algo == 6) out = fdbscan_densebox(s, DbscanParams{eps, min_pts}, ExecMode::kSequential);
     else if (algo == 1) out = friends_of_friends(s, eps);
     else if (algo == 2) out = fdbscan_densebox(s, DbscanParams{eps, min_pts});
     else if (algo == 3) out = dbscan_reference(s, DbscanParams{eps, min_pts});
@@ -131,7 +133,8 @@ int ref_bvh_build(const float *v, int64_t n, int dim, int is_points, int width, 
 }
 
 // algo: 0 fdbscan, 1 friends_of_friends, 2 fdbscan_densebox, 3 dbscan_reference,
-// 4 adjacency_graph_dbscan (dbscan.hpp:188-504)
+// 4 adjacency_graph_dbscan (dbscan.hpp:188-504); 5 fdbscan and 6
+// fdbscan_densebox in ExecMode::kSequential (exec.hpp:12)
 int ref_dbscan(const float *v, int64_t n, int dim, float eps, int32_t min_pts, int algo, int32_t *labels,
                uint8_t *core, int64_t *stats, double *phase_ms) {
   return dim == 2 ? dbscan_t<2>(v, n, eps, min_pts, algo, labels, core, stats, phase_ms)

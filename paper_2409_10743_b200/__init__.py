@@ -46,6 +46,7 @@ __all__ = [
 SP_OK, SP_EINVAL, SP_ECAPACITY, SP_ECUDA, SP_ENOMEM, SP_ENCCL = range(6)
 SP_MEM_HOST, SP_MEM_DEVICE = 0, 1
 SP_ALGO_FDBSCAN, SP_ALGO_FOF, SP_ALGO_DENSEBOX, SP_ALGO_FOF_POINTS, SP_ALGO_DENSEBOX_MIXED = 0, 1, 2, 3, 4
+SP_ALGO_SEQUENTIAL = 0x100  # ExecMode::kSequential (exec.hpp:12)
 SP_PRED_SPHERE, SP_PRED_BOX = 0, 1
 kNoiseLabel = -1
 
@@ -605,9 +606,16 @@ def _dbscan(points, eps, min_pts, algo, width, ctx, out=None):
                         DbscanStats(s.distance_checks, s.num_dense_cells, s.num_dense_points))
 
 
-def fdbscan(points, params: DbscanParams, width: int = 64, ctx: Optional[Context] = None, out=None) -> DbscanOutput:
-    """fdbscan (dbscan.hpp:277-282)."""
-    return _dbscan(points, params.eps, params.min_pts, SP_ALGO_FDBSCAN, width, ctx, out)
+def fdbscan(points, params: DbscanParams, width: int = 64, ctx: Optional[Context] = None, out=None,
+            mode: str = "parallel") -> DbscanOutput:
+    """fdbscan (dbscan.hpp:277-282).  mode="sequential" (ExecMode::kSequential,
+    exec.hpp:12) gives the reference's deterministic sequential labels: each
+    border point joins the cluster of its core neighbour of smallest leaf
+    position; "parallel" admits any valid border assignment."""
+    if mode not in ("parallel", "sequential"):
+        raise InvalidArgument("mode must be 'parallel' or 'sequential'")
+    seq = SP_ALGO_SEQUENTIAL if mode == "sequential" else 0
+    return _dbscan(points, params.eps, params.min_pts, SP_ALGO_FDBSCAN | seq, width, ctx, out)
 
 
 def friends_of_friends(points, eps: float, width: int = 64, ctx: Optional[Context] = None, out=None,
@@ -646,11 +654,16 @@ def friends_of_friends_ids(points, eps: float, ids, ctx: Optional[Context] = Non
 
 
 def fdbscan_densebox(points, params: DbscanParams, width: int = 64, ctx: Optional[Context] = None,
-                     out=None, algorithm: str = "cells") -> DbscanOutput:
+                     out=None, algorithm: str = "cells", mode: str = "parallel") -> DbscanOutput:
     """fdbscan_densebox (dbscan.hpp:298-449).  algorithm="cells" (default)
     runs the all-cells pipeline; "mixed" the reference's
-    mixed tree of dense cells and sparse points.  Equivalent clusterings."""
+    mixed tree of dense cells and sparse points.  Equivalent clusterings.
+    mode="sequential" (ExecMode::kSequential) gives the reference's
+    sequential labels bit for bit (over the mixed tree)."""
+    if mode not in ("parallel", "sequential"):
+        raise InvalidArgument("mode must be 'parallel' or 'sequential'")
     algo = {"cells": SP_ALGO_DENSEBOX, "mixed": SP_ALGO_DENSEBOX_MIXED}[algorithm]
+    algo |= SP_ALGO_SEQUENTIAL if mode == "sequential" else 0
     return _dbscan(points, params.eps, params.min_pts, algo, width, ctx, out)
 
 

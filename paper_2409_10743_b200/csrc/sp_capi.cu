@@ -553,7 +553,7 @@ int sp_dbscan(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, i
               int code_width, int32_t *labels, uint8_t *core, sp_timings *timings, sp_stats *stats, int mem) {
   return guarded(ctx, [&](spb::Ctx &c) {
     check_dim(dim);
-    if (algo < 0 || algo > 4) throw spb::InvalidArgument("unknown algorithm");
+    if ((algo & ~0x100) < 0 || (algo & ~0x100) > 4) throw spb::InvalidArgument("unknown algorithm");
     if (code_width != 32 && code_width != 64) throw spb::InvalidArgument("code width must be 32 or 64");
     if (n < 0 || n > (1LL << 30)) throw spb::InvalidArgument("point count out of range");
     In<float> p(c, points, (size_t)n * dim, mem);

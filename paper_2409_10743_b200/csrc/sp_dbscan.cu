@@ -77,7 +77,9 @@ __global__ void __launch_bounds__(128, 1) k_core_flags(const float4 *__restrict_
 // root_p is a hint for p's root: if q already points at it the pair is in one
 // set (true even for a stale hint, which is still a member of p's set), else a
 // union costs one find on q.
-template <bool FOF>
+// SEQ (ExecMode::kSequential): core-core pairs only; border points are
+// assigned afterwards by k_border_seq.
+template <bool FOF, bool SEQ = false>
 __device__ __forceinline__ void merge_pair(int32_t p, int32_t q, bool core_p, int32_t &root_p, int32_t *parent,
                                            const uint8_t *corep, uint32_t *claims) {
   if (FOF) {
@@ -89,7 +91,7 @@ __device__ __forceinline__ void merge_pair(int32_t p, int32_t q, bool core_p, in
   if (core_p && core_q) {
     if (parent[q] == root_p) return;
     root_p = uf_union(parent, root_p, q);
-  } else if (core_p || core_q) {
+  } else if (!SEQ && (core_p || core_q)) {
     const int32_t b = core_p ? q : p;  // the non-core side
     const uint32_t bit = 1u << (b & 31);
     if (!(atomicOr(&claims[b >> 5], bit) & bit)) root_p = uf_union(parent, root_p, q);
@@ -101,7 +103,7 @@ __device__ __forceinline__ void merge_pair(int32_t p, int32_t q, bool core_p, in
 // leaves are examined and each close pair is seen exactly once.  Leaves are
 // read as one 16-byte {x,y,z,rope}; internal nodes take the conservative
 // fp32 test, leaves the exact one.
-template <bool FOF, bool FAST>
+template <bool FOF, bool FAST, bool SEQ = false>
 __global__ void __launch_bounds__(128, 1) k_merge_pairs(const float4 *__restrict__ nodes,
                                                      const float4 *__restrict__ leafpt, int64_t n, Radius R,
                                                      int32_t *parent, const uint8_t *__restrict__ corep,
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(128, 1) k_merge_pairs(const float4 *__restrict
         const int32_t q = (int32_t)(cur - first_leaf);
         const float4 L = ld_node(leafpt, q);
         if (hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z))
-          merge_pair<FOF>((int32_t)p, q, core_p, root_p, parent, corep, claims);
+          merge_pair<FOF, SEQ>((int32_t)p, q, core_p, root_p, parent, corep, claims);
         cur = __float_as_int(L.w);
       } else {
         const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
@@ -128,6 +130,47 @@ __global__ void __launch_bounds__(128, 1) k_merge_pairs(const float4 *__restrict
         cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
       }
     }
+  }
+}
+
+// Border points of the sequential mode (ExecMode::kSequential, exec.hpp:12).
+// The reference's sequential pair traversal (traversal.hpp:162-184 with
+// parallel_for run in order) reports the pairs of leaf p before those of leaf
+// p + 1, and each leaf's later partners in leaf order, so the first
+// (core, border) pair of a border point y -- the one whose claim latch wins
+// (dbscan.hpp:123-137) -- is the one with its core neighbour of SMALLEST leaf
+// position: a partner x before y is reported in x's turn, before y's own,
+// and among partners after y the rope walk meets the smallest first.  Here
+// every non-core point walks the tree from the root in depth-first order,
+// which meets the leaves in increasing position, stops at the first core
+// leaf within eps and joins that point's set.  The labels are therefore the
+// reference's sequential labels bit for bit.
+template <bool FAST>
+__global__ void __launch_bounds__(128) k_border_seq(const float4 *__restrict__ nodes,
+                                                    const float4 *__restrict__ leafpt, int64_t n, Radius R,
+                                                    int32_t *parent, const uint8_t *__restrict__ corep,
+                                                    uint32_t *claims) {
+  R.fast = FAST ? 1 : 0;
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n || corep[p]) return;
+  const float4 me = ld_node(leafpt, p);
+  const int64_t first_leaf = n - 1;
+  int32_t cur = 0, found = -1;
+  while (cur != kSentinel) {
+    if (cur >= first_leaf) {
+      const int32_t q = (int32_t)(cur - first_leaf);
+      const float4 L = ld_node(leafpt, q);
+      const bool take = q != p && corep[q] && hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z);
+      found = take ? q : found;
+      cur = take ? kSentinel : __float_as_int(L.w);
+    } else {
+      const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+      cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
+    }
+  }
+  if (found >= 0) {
+    atomicOr(&claims[p >> 5], 1u << (p & 31));
+    uf_union(parent, (int32_t)p, found);
   }
 }
 
@@ -191,6 +234,11 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
   // SP_ALGO_*); 3 friends_of_friends by pair traversal over the point
   // hierarchy (the reference's own algorithm, no grid); 4 fdbscan_densebox
   // over the reference's mixed tree of dense cells and sparse points.
+  // SP_ALGO_SEQUENTIAL (0x100): ExecMode::kSequential; deterministic border
+  // assignment equal to the reference's sequential run.  Friends-of-friends
+  // is deterministic in both modes.
+  const bool seq = (algo & 0x100) != 0;
+  algo &= 0xff;
   if (algo == 1 || algo == 3) min_pts = 2;
   if (min_pts < 2) throw InvalidArgument("dbscan: min_pts must be at least 2");
   if (n == 0) return;
@@ -202,8 +250,8 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
   }
   if (algo == 2 || algo == 4) {
     extern void densebox(Ctx &, const float *, int64_t, int, float, int32_t, int, int32_t *, uint8_t *,
-                         DbscanResult *, bool);
-    densebox(c, points, n, dim, eps, min_pts, width, labels, core, res, algo == 2);
+                         DbscanResult *, bool, bool);
+    densebox(c, points, n, dim, eps, min_pts, width, labels, core, res, algo == 2, seq);
     return;
   }
   cudaEvent_t ev[5];
@@ -245,12 +293,19 @@ void dbscan(Ctx &c, const float *points, int64_t n, int dim, float eps, int32_t 
   {
     SmSlices sl(c);
     if (count_phase) SPB_CUDA(cudaMemsetAsync(claims.get(), 0, claims.n * sizeof(uint32_t), c.stream));
-    auto kern = count_phase ? (R.fast ? k_merge_pairs<false, true> : k_merge_pairs<false, false>)
+    auto kern = count_phase ? (seq ? (R.fast ? k_merge_pairs<false, true, true> : k_merge_pairs<false, false, true>)
+                                   : (R.fast ? k_merge_pairs<false, true> : k_merge_pairs<false, false>))
                             : (R.fast ? k_merge_pairs<true, true> : k_merge_pairs<true, false>);
     kern<<<sl.grid(kern, 128), 128, 0, c.stream>>>(t.nodes, t.leafpt, n, R, parent.get(), corep.get(),
                                                    count_phase ? claims.get() : nullptr, sl.ctr.get(), sl.nsm);
   }
   SPB_LAUNCHED();
+  if (count_phase && seq) {
+    auto kern = R.fast ? k_border_seq<true> : k_border_seq<false>;
+    kern<<<(unsigned)((n + 127) / 128), 128, 0, c.stream>>>(t.nodes, t.leafpt, n, R, parent.get(), corep.get(),
+                                                            claims.get());
+    SPB_LAUNCHED();
+  }
   SPB_CUDA(cudaEventRecord(ev[3], c.stream));
   mark(c, "merge");
   if (!count_phase) {

@@ -559,6 +559,78 @@ __global__ void __launch_bounds__(128) k_db_core_pairs(DenseView v, const int32_
 }
 
 // Border points: the first core point within eps claims the point.
+// Border points of the sequential mode (ExecMode::kSequential) over the mixed
+// tree.  The reference's sequential merge (dbscan.hpp:406-442) runs the points'
+// range queries in sort_queries order (the point Morton order, position spos)
+// and reports, in query i's turn, the pairs (i, j) with i < j in object leaf
+// order, members of a dense cell in index order.  The claim of a border point
+// y therefore goes to the core neighbour x minimising
+//   (spos[x], 0, 0)                    for x < y  (reported in x's turn),
+//   (spos[y], leaf position of x's object, x)  for x > y  (in y's own turn);
+// every core neighbour within eps is examined (a full walk), and y joins the
+// set of the minimiser.
+__global__ void __launch_bounds__(128) k_db_border_seq(DenseView v, const int32_t *__restrict__ border_leaf,
+                                                       const int64_t *__restrict__ ncore_p, int32_t *parent,
+                                                       const uint8_t *__restrict__ core,
+                                                       const int32_t *__restrict__ spos, uint32_t *__restrict__ claims,
+                                                       unsigned long long *__restrict__ checks_total) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nborder = v.nobj - *ncore_p;
+  uint64_t checks = 0;
+  if (k < nborder) {
+    const int64_t first_leaf = v.nobj - 1;
+    const float4 me = ld_node(v.nodes, 2 * (first_leaf + border_leaf[k]));
+    const int32_t i = v.sparse_pts[node_link(me) - v.nd];
+    const uint64_t own = (uint64_t)(uint32_t)spos[i] << 32;
+    const float x = me.x, y = me.y, z = me.z;
+    uint64_t best = ~0ull;
+    int32_t best_x = 0x7fffffff, found = -1;
+    auto offer = [&](int32_t j, int64_t leafpos) {
+      const uint64_t key = j < i ? (uint64_t)(uint32_t)spos[j] << 32 : own | (uint64_t)leafpos;
+      const int32_t tie = j < i ? 0 : j;
+      if (key < best || (key == best && tie < best_x)) {
+        best = key;
+        best_x = tie;
+        found = j;
+      }
+    };
+    int32_t cur = 0;
+    while (cur != kSentinel) {
+      const float4 lo = ld_node(v.nodes, 2 * (int64_t)cur), hi = ld_node(v.nodes, 2 * (int64_t)cur + 1);
+      if (cur < first_leaf) {
+        cur = maybe_box(v.R, x, y, z, lo, hi) ? node_link(lo) : node_rope(hi);
+        continue;
+      }
+      const int64_t leafpos = cur - first_leaf;
+      cur = node_rope(hi);
+      if (!hit_box(v.R, x, y, z, lo, hi)) continue;
+      const int32_t o = node_link(lo);
+      if (o < v.nd) {
+        const int64_t b = v.dbeg[o];
+        const int32_t len = v.dlen[o];
+        for (int32_t t = 0; t < len; ++t) {
+          const float4 q = v.cpts[b + t];
+          ++checks;
+          if (hit_point(v.R, x, y, z, q.x, q.y, q.z)) offer(__float_as_int(q.w), leafpos);
+        }
+      } else {
+        const int32_t j = v.sparse_pts[o - v.nd];
+        if (core[j]) offer(j, leafpos);  // the point box hit is the exact point test
+      }
+    }
+    if (found >= 0) {
+      atomicOr(&claims[i >> 5], 1u << (i & 31));
+      uf_union(parent, found, i);
+    }
+  }
+  add_checks(checks, checks_total);
+}
+
+__global__ void k_invert(const int32_t *__restrict__ order, int64_t n, int32_t *__restrict__ pos) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) pos[order[k]] = (int32_t)k;
+}
+
 __global__ void __launch_bounds__(128) k_db_border(DenseView v, const int32_t *__restrict__ border_leaf,
                                                    const int64_t *__restrict__ ncore_p, int32_t *parent, const uint8_t *__restrict__ core,
                                                    uint32_t *__restrict__ claims,
@@ -857,8 +929,9 @@ bool dbscan_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32
 // applies; otherwise the reference's mixed tree of dense cells and sparse
 // points below.
 void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t min_pts, int width, int32_t *labels,
-              uint8_t *core_out, DbscanResult *res, bool cells) {
-  if (cells && dbscan_cells(c, pts, n, dim, eps, min_pts, labels, core_out, res)) return;
+              uint8_t *core_out, DbscanResult *res, bool cells, bool seq) {
+  seq = seq && min_pts > 2;  // min_pts = 2 has no border points
+  if (cells && !seq && dbscan_cells(c, pts, n, dim, eps, min_pts, labels, core_out, res)) return;
   cudaEvent_t ev[5];
   for (auto &e : ev) SPB_CUDA(cudaEventCreate(&e));
   SPB_CUDA(cudaEventRecord(ev[0], c.stream));
@@ -1033,7 +1106,16 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
                                                       core.get(), checks.get());
     SPB_LAUNCHED();
     mark(c, "merge_core");
-    if (count_phase) {
+    if (count_phase && seq) {
+      // sort_queries order of the points (traversal.hpp:188-218): spos
+      DevBuf<int32_t> porder((size_t)n, c.stream), spos((size_t)n, c.stream);
+      sort_points(c, pts, n, dim, porder.get());
+      k_invert<<<G, 256, 0, c.stream>>>(porder.get(), n, spos.get());
+      SPB_LAUNCHED();
+      k_db_border_seq<<<Gl, 128, 0, c.stream>>>(v, border_leaf.get(), kscan.get() + nobj, parent.get(), core.get(),
+                                                spos.get(), claims.get(), checks.get());
+      SPB_LAUNCHED();
+    } else if (count_phase) {
       k_db_border<<<Gl, 128, 0, c.stream>>>(v, border_leaf.get(), kscan.get() + nobj, parent.get(), core.get(),
                                             claims.get(), checks.get());
       SPB_LAUNCHED();

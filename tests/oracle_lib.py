@@ -235,7 +235,8 @@ class Reference:
         return out
 
     def dbscan(self, pts, dim, eps, min_pts, algo="fdbscan", with_stats=False):
-        code = {"fdbscan": 0, "fof": 1, "densebox": 2, "reference": 3, "adjacency": 4}[algo]
+        code = {"fdbscan": 0, "fof": 1, "densebox": 2, "reference": 3, "adjacency": 4, "fdbscan_seq": 5,
+                "densebox_seq": 6}[algo]
         pts = _f32(pts)
         n = pts.shape[0]
         labels = np.empty(max(n, 1), np.int32)

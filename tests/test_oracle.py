@@ -5,7 +5,7 @@ the unmodified reference itself on random instances."""
 import numpy as np
 import pytest
 
-from fixtures import BVH_KEYS, bvh_cases, dbscan_cases, generator_hashes, golden_hashes, query_cases, same_bits, \
+from fixtures import _cases, BVH_KEYS, bvh_cases, dbscan_cases, generator_hashes, golden_hashes, query_cases, same_bits, \
     summarize
 from oracle_lib import Reference, eps_for, fnv1a64
 
@@ -119,3 +119,18 @@ def test_oracle_equals_reference_on_random_instances(oracle):
         rl, rc = R.dbscan(pts, dim, eps, mp, "reference")
         assert np.array_equal(core, rc)
         assert oracle.check_equivalence(pts, dim, eps, (lab, core), (rl, rc)) is None
+
+
+@pytest.mark.parametrize("name", list(_cases("seq_cases.npz").keys()))
+def test_sequential_fixtures_pinned_by_oracle(oracle, name):
+    # the sequential-mode fixtures (ExecMode::kSequential) against the
+    # independent restatement: identical core flags, and clusters equivalent
+    # to the oracle's under verify.hpp's contract
+    c = _cases("seq_cases.npz")[name]
+    dim, min_pts = (int(v) for v in c["meta"])
+    eps = float(c["eps"])
+    lab, core = oracle.dbscan(c["points"], dim, eps, min_pts)
+    for key in ("fd", "db"):
+        assert np.array_equal(c[key + "_core"], core), key
+        assert oracle.check_equivalence(c["points"], dim, eps, (c[key + "_labels"], c[key + "_core"]),
+                                        (lab, core)) is None, key
