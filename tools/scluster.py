@@ -3,8 +3,9 @@
 
 Same flags, stdout lines, report keys and exit codes (0 ok, 1 usage, 2 I/O or
 capacity, 3 verification mismatch); the clustering runs on the B200 through
-libspb200.so.  --sequential is accepted for compatibility (results here do not
-depend on it).  --verify compares against the device brute-force
+libspb200.so.  --sequential selects the sequential modes (ExecMode::kSequential):
+fdbscan and densebox labels then equal the reference's sequential run bit for
+bit (deterministic border assignment).  --verify compares against the device brute-force
 dbscan_reference with check_equivalence (both on the GPU).
 """
 from __future__ import annotations
@@ -92,10 +93,11 @@ def run(opt) -> int:
     if opt.verify and n > opt.oracle_ceiling:
         raise UsageError("--verify is limited to %d points (got %d)" % (opt.oracle_ceiling, n))
     params = sp.DbscanParams(float(np.float32(eps)), opt.minpts)
+    mode = "sequential" if opt.sequential else "parallel"
     if opt.algo == "fdbscan":
-        out = sp.fdbscan(pts, params, width=opt.code_width)
+        out = sp.fdbscan(pts, params, width=opt.code_width, mode=mode)
     elif opt.algo == "densebox":
-        out = sp.fdbscan_densebox(pts, params, width=opt.code_width)
+        out = sp.fdbscan_densebox(pts, params, width=opt.code_width, mode=mode)
     elif opt.algo == "fof":
         out = sp.friends_of_friends(pts, params.eps, width=opt.code_width)
     elif opt.algo == "legacy":
