@@ -608,8 +608,9 @@ constexpr int CLIMB_BLK = 256;
 struct LocalClimb {
   int64_t B;
   const uint8_t *in;  // [CLIMB_BLK] shared: the parent at split B + i lies inside
-  int32_t *flag;      // [CLIMB_BLK] shared flags, -1 = empty
-  float *box;         // [2][CLIMB_BLK][6] shared child boxes (0 = left, 1 = right)
+  int32_t *flag;      // [CLIMB_BLK] shared flags, -1 = empty (modes 0, 1)
+  unsigned long long *flag128;  // [CLIMB_BLK][2] shared flag words, bound -1 = empty (mode 2)
+  unsigned long long *box;  // [2][CLIMB_BLK][3] shared child boxes (0 = left, 1 = right), float pairs
   __device__ __forceinline__ bool inside(int64_t a) const { return a >= B && a < B + CLIMB_BLK && in[a - B]; }
 };
 
@@ -623,6 +624,79 @@ __device__ __forceinline__ int32_t exch_acq_rel_cta_shared(int32_t *p, int32_t v
   const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
   asm volatile("atom.acq_rel.cta.shared::cta.exch.b32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
   return old;
+}
+
+#ifndef SPB_CLIMB_SMEM_MODE
+#define SPB_CLIMB_SMEM_MODE 2
+#endif
+__device__ __forceinline__ unsigned long long pack2(float a, float b) {
+  return (unsigned long long)__float_as_uint(a) | ((unsigned long long)__float_as_uint(b) << 32);
+}
+__device__ __forceinline__ float lo32f(unsigned long long w) { return __uint_as_float((uint32_t)w); }
+__device__ __forceinline__ float hi32f(unsigned long long w) { return __uint_as_float((uint32_t)(w >> 32)); }
+__device__ __forceinline__ void exch128(unsigned long long *p, unsigned long long &x, unsigned long long &y,
+                                        bool acq_rel) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  if (acq_rel)
+    asm volatile("{ .reg .b128 d, v; mov.b128 v, {%0, %1}; atom.acq_rel.cta.shared::cta.exch.b128 d, [%2], v;"
+                 " mov.b128 {%0, %1}, d; }" : "+l"(x), "+l"(y) : "r"(a) : "memory");
+  else
+    asm volatile("{ .reg .b128 d, v; mov.b128 v, {%0, %1}; atom.relaxed.cta.shared::cta.exch.b128 d, [%2], v;"
+                 " mov.b128 {%0, %1}, d; }" : "+l"(x), "+l"(y) : "r"(a) : "memory");
+}
+
+// One block-local hand-off at split a: publish this child's box, exchange
+// the flag; returns the first arrival's bound (second arrival, sibling box in
+// slo/shi) or -1 (first arrival).  Every shared access of the slots is an
+// atomic (racecheck tracks barriers, not acquire/release), either 64-bit
+// words (mode 1) or 128-bit exchanges (mode 2): the flag word carries
+// {bound, lo.xyz} of the first arrival, a second word its hi.xyz.
+__device__ __forceinline__ int32_t local_handoff(const LocalClimb &lc, int64_t a, bool L, int32_t bound,
+                                                 const float lo[3], const float hi[3], float4 &slo, float4 &shi) {
+  const int64_t k = a - lc.B;
+  if (SPB_CLIMB_SMEM_MODE == 2) {
+    // box: [2][CLIMB_BLK][2] words of 64 bit per side: hi.xyz of that side;
+    // flag words: [CLIMB_BLK][2] {bound | lo.x, lo.y | lo.z}
+    unsigned long long *hslot = lc.box + ((L ? 0 : CLIMB_BLK) + k) * 2;
+    unsigned long long h0 = pack2(hi[0], hi[1]), h1 = pack2(hi[2], 0.f);
+    exch128(hslot, h0, h1, false);
+    unsigned long long w0 = (unsigned long long)(uint32_t)bound | ((unsigned long long)__float_as_uint(lo[0]) << 32);
+    unsigned long long w1 = pack2(lo[1], lo[2]);
+    exch128(lc.flag128 + 2 * k, w0, w1, true);
+    const int32_t other = (int32_t)(uint32_t)w0;
+    if (other < 0) return other;
+    unsigned long long g0 = 0, g1 = 0;
+    exch128(lc.box + ((L ? CLIMB_BLK : 0) + k) * 2, g0, g1, false);
+    slo = make_float4(hi32f(w0), lo32f(w1), hi32f(w1), 0.f);
+    shi = make_float4(lo32f(g0), hi32f(g0), lo32f(g1), 0.f);
+    return other;
+  }
+  unsigned long long *mine = lc.box + ((L ? 0 : CLIMB_BLK) + k) * 3;
+  if (SPB_CLIMB_SMEM_MODE == 1) {
+    atomicExch(mine, pack2(lo[0], lo[1]));
+    atomicExch(mine + 1, pack2(lo[2], hi[0]));
+    atomicExch(mine + 2, pack2(hi[1], hi[2]));
+  } else {
+    mine[0] = pack2(lo[0], lo[1]);
+    mine[1] = pack2(lo[2], hi[0]);
+    mine[2] = pack2(hi[1], hi[2]);
+  }
+  const int32_t other = exch_acq_rel_cta_shared(lc.flag + k, bound);
+  if (other < 0) return other;
+  unsigned long long *sb = lc.box + ((L ? CLIMB_BLK : 0) + k) * 3;
+  unsigned long long w0, w1, w2;
+  if (SPB_CLIMB_SMEM_MODE == 1) {
+    w0 = atomicOr(sb, 0ull);
+    w1 = atomicOr(sb + 1, 0ull);
+    w2 = atomicOr(sb + 2, 0ull);
+  } else {
+    w0 = sb[0];
+    w1 = sb[1];
+    w2 = sb[2];
+  }
+  slo = make_float4(lo32f(w0), hi32f(w0), lo32f(w1), 0.f);
+  shi = make_float4(hi32f(w1), lo32f(w2), hi32f(w2), 0.f);
+  return other;
 }
 
 template <bool LOCAL>
@@ -641,16 +715,10 @@ __device__ __forceinline__ bool climb(const HierView &H, int64_t &l, int64_t &r,
     const bool local = LOCAL && lc.inside(a);
     float4 slo, shi;
     if (local) {
-      float *mine = lc.box + ((L ? 0 : CLIMB_BLK) + (a - lc.B)) * 6;
-      mine[0] = lo[0]; mine[1] = lo[1]; mine[2] = lo[2];
-      mine[3] = hi[0]; mine[4] = hi[1]; mine[5] = hi[2];
-      const int32_t other = exch_acq_rel_cta_shared(lc.flag + (a - lc.B), bound);
+      const int32_t other = local_handoff(lc, a, L, bound, lo, hi, slo, shi);
       if (other < 0) return false;  // first arrival: the sibling is inside and will come
       if (L) r = other;
       else l = other;
-      const float *sb = lc.box + ((L ? CLIMB_BLK : 0) + (a - lc.B)) * 6;
-      slo = make_float4(sb[0], sb[1], sb[2], 0.f);
-      shi = make_float4(sb[3], sb[4], sb[5], 0.f);
     } else {
       const int32_t other = exch_acq_rel_gpu(flags + a, bound);
       if (other < 0) return false;  // first arrival
@@ -692,7 +760,7 @@ __global__ void __launch_bounds__(256) k_climb_rest(int64_t n, const int32_t *__
   const float4 s0 = queue[2 * i], s1 = queue[2 * i + 1];
   int64_t l = __float_as_int(s0.x), r = __float_as_int(s0.y);
   float lo[3] = {s0.z, s0.w, s1.x}, hi[3] = {s1.y, s1.z, s1.w};
-  climb<false>(H, l, r, lo, hi, nodes, flags, 1 << 30, LocalClimb{0, nullptr, nullptr, nullptr});
+  climb<false>(H, l, r, lo, hi, nodes, flags, 1 << 30, LocalClimb{0, nullptr, nullptr, nullptr, nullptr});
 }
 
 template <bool POINTS>
@@ -705,11 +773,14 @@ __global__ void __launch_bounds__(CLIMB_BLK) k_hierarchy(int64_t n, const int32_
   __shared__ int32_t s_flag[CLIMB_BLK];
   __shared__ int32_t s_D[CLIMB_BLK + 1], s_pre[CLIMB_BLK], s_suf[CLIMB_BLK + 1], s_wmin[2][CLIMB_BLK / 32];
   __shared__ uint8_t s_in[CLIMB_BLK];
-  __shared__ float s_box[2 * CLIMB_BLK * 6];
+  __shared__ __align__(16) unsigned long long s_box[2 * CLIMB_BLK * 3];
+  __shared__ __align__(16) unsigned long long s_flag128[2 * CLIMB_BLK];
   const HierView H{n, delta};
   const int64_t B = (int64_t)blockIdx.x * CLIMB_BLK;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   s_flag[t] = -1;
+  s_flag128[2 * t] = 0xffffffffull;  // bound -1
+  s_flag128[2 * t + 1] = 0;
   const int32_t dv = H.D(B - 1 + t);  // element t of D(B-1 .. B+BLK-1)
   s_D[t] = dv;
   if (t == 0) s_D[CLIMB_BLK] = H.D(B + CLIMB_BLK - 1);
@@ -753,7 +824,7 @@ __global__ void __launch_bounds__(CLIMB_BLK) k_hierarchy(int64_t n, const int32_
   if (POINTS) leafpt[p] = make_float4(lo[0], lo[1], lo[2], __int_as_float(leaf_rope));
   if (n == 1) return;
   int64_t l = p, r = p;
-  const LocalClimb lc{B, s_in, s_flag, s_box};
+  const LocalClimb lc{B, s_in, s_flag, s_flag128, s_box};
   if (climb<true>(H, l, r, lo, hi, nodes, flags, max_levels, lc)) {
     const uint32_t slot = atomicAdd(qcount, 1u);
     queue[2 * (int64_t)slot] = make_float4(__int_as_float((int)l), __int_as_float((int)r), lo[0], lo[1]);
