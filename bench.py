@@ -498,11 +498,13 @@ def run_extra(w: str, steps: int) -> dict:
     reduced to the keys the headline line carries."""
     cmd = [sys.executable, os.path.abspath(__file__), "--workload", w, "--steps", str(steps), "--warmup", "1",
            "--no-cpu-baseline"]
+    err = ""
     try:
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        err = r.stderr.strip()[-300:]
         d = json.loads(r.stdout.strip().splitlines()[-1])
     except Exception as e:  # reported, not fatal: the headline stands on its own
-        return {"error": "%s: %s" % (type(e).__name__, str(e)[:200])}
+        return {"error": "%s: %s" % (type(e).__name__, str(e)[:200]), "stderr": err}
     keep = ("metric", "value", "unit", "ms_per_step", "steps", "parts_ms", "parity", "e2e", "gpu_launches", "clocks")
     out = {k: d.get(k) for k in keep}
     out["workload"] = d.get("config", {}).get("workload")

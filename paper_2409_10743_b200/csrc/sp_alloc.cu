@@ -100,10 +100,20 @@ void *cache_alloc(size_t bytes, cudaStream_t s) {
   return p;
 }
 
+// Return every cached block of every stream and the default pool's reserved
+// but unused memory (sp_ctx_create keeps freed pool memory reserved) to the
+// driver, so that cudaMalloc and other processes can have it.
 void cache_drain() {
   Cache &c = cache();
-  std::lock_guard<std::mutex> g(c.mu);
-  drain_all(c);
+  {
+    std::lock_guard<std::mutex> g(c.mu);
+    drain_all(c);
+  }
+  cudaDeviceSynchronize();
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+    cudaMemPoolTrimTo(pool, 0);
 }
 
 void cache_free(void *p, cudaStream_t s) {

@@ -61,7 +61,6 @@ spb::Ctx::Staging &stage(spb::Ctx &c, bool input, size_t bytes) {
       // out of memory: other streams' cached scratch blocks may hold it
       cudaGetLastError();
       spb::cache_drain();
-      SPB_CUDA(cudaDeviceSynchronize());
       SPB_CUDA(cudaMalloc(&s.p, bytes));
     }
     s.cap = bytes;
@@ -255,6 +254,10 @@ int sp_ctx_destroy(sp_ctx *ctx) {
     spb::cache_unregister_stream(ctx->c.stream);
     cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.owns_stream) cudaStreamDestroy(ctx->c.stream);
+    // the pool keeps freed memory reserved while contexts run (release
+    // threshold above); a destroyed context hands its share back
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, ctx->c.device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
   }
   delete ctx;
   return SP_OK;
