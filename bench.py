@@ -160,12 +160,12 @@ PROFILED = {"merge": "merge_cells_2p27", "sort": "sort_cells_2p27", "hierarchy":
 
 def profiled_traffic(phase: str, n: int):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the phase's
-    kernel from the committed ncu --set full capture (profiles/r01), for the
+    kernel from the committed ncu --set full capture (profiles/r02), for the
     headline size only; None otherwise."""
     if n != (1 << 27) or phase not in PROFILED:
         return None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01", PROFILED[phase] + ".summary.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02", PROFILED[phase] + ".summary.json")) as f:
             d = json.load(f)
         scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         tot = 0.0
