@@ -307,19 +307,20 @@ void morton_codes(Ctx &c, const float *objects, int64_t n, int dim, bool points,
 constexpr int RS_BINS = 256;
 constexpr int RS_WH = RS_BINS + 1;  // + one slot for out-of-range items
 
-template <int ITEMS, int THREADS>
+template <int ITEMS, int THREADS, class K>
 constexpr size_t rs_smem_bytes() {
-  return (size_t)THREADS * ITEMS * 12 + (size_t)(THREADS / 32) * RS_WH * 4;
+  return (size_t)THREADS * ITEMS * (sizeof(K) + 4) + (size_t)(THREADS / 32) * RS_WH * 4;
 }
 
-__global__ void __launch_bounds__(256) k_rs_hist(const uint64_t *__restrict__ keys, int64_t n, int npass,
+template <class K>
+__global__ void __launch_bounds__(256) k_rs_hist(const K *__restrict__ keys, int64_t n, int npass,
                                                  uint32_t *__restrict__ ghist) {
   __shared__ uint32_t h[8 * RS_BINS];
   for (int i = threadIdx.x; i < npass * RS_BINS; i += blockDim.x) h[i] = 0;
   __syncthreads();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    uint64_t k = keys[i];
+    const uint64_t k = keys[i];
     for (int p = 0; p < npass; ++p) atomicAdd(&h[p * RS_BINS + ((k >> (8 * p)) & 0xff)], 1u);
   }
   __syncthreads();
@@ -347,15 +348,19 @@ __global__ void k_rs_scan(uint32_t *ghist) {
 
 // THREADS threads, ITEMS keys each; threads [0, 256) own one digit each for
 // the cross-warp prefix, the look-back and the tile-local digit scan.
-template <int ITEMS, int THREADS>
-__global__ void __launch_bounds__(THREADS, (THREADS * ITEMS <= 2048) ? 4 : SPB_RS_MINBLOCKS) k_rs_onesweep(
-    const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
+#ifndef SPB_RS_MINBLOCKS32
+#define SPB_RS_MINBLOCKS32 3
+#endif
+template <int ITEMS, int THREADS, class K>
+__global__ void __launch_bounds__(THREADS, (THREADS * ITEMS <= 2048) ? 4
+                                           : (sizeof(K) == 4 ? SPB_RS_MINBLOCKS32 : SPB_RS_MINBLOCKS)) k_rs_onesweep(
+    const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
     uint32_t *__restrict__ vout, int64_t n, int shift, const uint32_t *__restrict__ binbase,
     unsigned long long *lookback, uint32_t *tile_ctr, uint32_t tag) {
   constexpr int TILE = THREADS * ITEMS;
   constexpr int WARPS = THREADS / 32;
   extern __shared__ __align__(16) unsigned char rs_smem[];
-  uint64_t *skeys = reinterpret_cast<uint64_t *>(rs_smem);
+  K *skeys = reinterpret_cast<K *>(rs_smem);
   uint32_t *svals = reinterpret_cast<uint32_t *>(skeys + TILE);
   uint32_t *whist = svals + TILE;
   __shared__ uint32_t s_dstart[RS_BINS];
@@ -370,7 +375,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS * ITEMS <= 2048) ? 4 : SPB_R
   const uint32_t tile = s_tile;
   const int64_t base = (int64_t)tile * TILE;
 
-  uint64_t key[ITEMS];
+  K key[ITEMS];
   uint32_t val[ITEMS];
   uint16_t rk[ITEMS];
   const int64_t wbase = base + (int64_t)warp * (ITEMS * 32);
@@ -388,7 +393,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS * ITEMS <= 2048) ? 4 : SPB_R
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const int64_t idx = wbase + i * 32 + lane;
-      key[i] = idx < n ? kin[idx] : ~0ull;
+      key[i] = idx < n ? kin[idx] : (K)~(K)0;
       val[i] = idx < n ? (vin ? vin[idx] : (uint32_t)idx) : 0u;
     }
   }
@@ -487,7 +492,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS * ITEMS <= 2048) ? 4 : SPB_R
   __syncthreads();
   const int valid = (int)((n - base) < (int64_t)TILE ? (n - base) : (int64_t)TILE);
   for (int pos = tid; pos < valid; pos += THREADS) {
-    const uint64_t k = skeys[pos];
+    const K k = skeys[pos];
     const uint32_t d = (uint32_t)(k >> shift) & 0xffu;
     const uint32_t o = s_gbase[d] + (uint32_t)pos - s_dstart[d];
     kout[o] = k;
@@ -502,18 +507,18 @@ __global__ void __launch_bounds__(THREADS, (THREADS * ITEMS <= 2048) ? 4 : SPB_R
 #define SPB_RS_ITEMS 16
 #endif
 
-template <int ITEMS, int THREADS>
-void onesweep_passes(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_alt, uint32_t **vals_alt, int64_t n,
+template <int ITEMS, int THREADS, class K>
+void onesweep_passes(Ctx &c, K **keys, uint32_t **vals, K **keys_alt, uint32_t **vals_alt, int64_t n,
                      int npass, bool vals_iota) {
   constexpr int TILE = THREADS * ITEMS;
-  constexpr size_t SMEM = rs_smem_bytes<ITEMS, THREADS>();
+  constexpr size_t SMEM = rs_smem_bytes<ITEMS, THREADS, K>();
   // the dynamic shared-memory opt-in is per device (and per kernel)
   static std::mutex mu;
   static uint64_t opted = 0;  // bit d: set on device d
   {
     std::lock_guard<std::mutex> g(mu);
     if (c.device >= 64 || !((opted >> c.device) & 1)) {
-      SPB_CUDA(cudaFuncSetAttribute(k_rs_onesweep<ITEMS, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      SPB_CUDA(cudaFuncSetAttribute(k_rs_onesweep<ITEMS, THREADS, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)SMEM));
       if (c.device < 64) opted |= 1ull << c.device;
     }
@@ -523,13 +528,13 @@ void onesweep_passes(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_a
   DevBuf<unsigned long long> lookback((size_t)ntiles * RS_BINS, c.stream);
   SPB_CUDA(cudaMemsetAsync(hist.get(), 0, hist.n * sizeof(uint32_t), c.stream));
   SPB_CUDA(cudaMemsetAsync(lookback.get(), 0, lookback.n * sizeof(unsigned long long), c.stream));
-  k_rs_hist<<<grid_for(n, 256, 148 * 4), 256, 0, c.stream>>>(*keys, n, npass, hist.get());
+  k_rs_hist<K><<<grid_for(n, 256, 148 * 4), 256, 0, c.stream>>>(*keys, n, npass, hist.get());
   SPB_LAUNCHED();
   k_rs_scan<<<npass, RS_BINS, 0, c.stream>>>(hist.get());
   SPB_LAUNCHED();
   uint32_t *ctr = hist.get() + (size_t)npass * RS_BINS;
   for (int p = 0; p < npass; ++p) {
-    k_rs_onesweep<ITEMS, THREADS><<<(unsigned)ntiles, THREADS, SMEM, c.stream>>>(
+    k_rs_onesweep<ITEMS, THREADS, K><<<(unsigned)ntiles, THREADS, SMEM, c.stream>>>(
         *keys, (p == 0 && vals_iota) ? nullptr : *vals, *keys_alt, *vals_alt, n, 8 * p,
         hist.get() + (size_t)p * RS_BINS, lookback.get(), ctr + p, (uint32_t)(2 * p + 1));
     SPB_LAUNCHED();
@@ -545,7 +550,17 @@ void radix_sort_pairs(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_
     return;
   }
   const int npass = std::max(1, (key_bits + 7) / 8);
-  onesweep_passes<SPB_RS_ITEMS, SPB_RS_THREADS>(c, keys, vals, keys_alt, vals_alt, n, npass, vals_iota);
+  onesweep_passes<SPB_RS_ITEMS, SPB_RS_THREADS, uint64_t>(c, keys, vals, keys_alt, vals_alt, n, npass, vals_iota);
+}
+
+void radix_sort_pairs(Ctx &c, uint32_t **keys, uint32_t **vals, uint32_t **keys_alt, uint32_t **vals_alt, int64_t n,
+                      int key_bits, bool vals_iota) {
+  if (n <= 1) {
+    if (n == 1 && vals_iota) SPB_CUDA(cudaMemsetAsync(*vals, 0, sizeof(uint32_t), c.stream));
+    return;
+  }
+  const int npass = std::max(1, std::min(4, (key_bits + 7) / 8));
+  onesweep_passes<SPB_RS_ITEMS, SPB_RS_THREADS, uint32_t>(c, keys, vals, keys_alt, vals_alt, n, npass, vals_iota);
 }
 
 // ---------------------------------------------------------------------------
@@ -769,7 +784,7 @@ __global__ void __launch_bounds__(CLIMB_BLK) k_hierarchy(int64_t n, const int32_
                                                    int dim, float4 *nodes, int32_t *flags,
                                                    int32_t *__restrict__ perm_out, float4 *__restrict__ leafpt,
                                                    int max_levels, float4 *__restrict__ queue,
-                                                   uint32_t *__restrict__ qcount) {
+                                                   uint32_t *__restrict__ qcount, const float4 *spts) {
   __shared__ int32_t s_flag[CLIMB_BLK];
   __shared__ int32_t s_D[CLIMB_BLK + 1], s_pre[CLIMB_BLK], s_suf[CLIMB_BLK + 1], s_wmin[2][CLIMB_BLK / 32];
   __shared__ uint8_t s_in[CLIMB_BLK];
@@ -808,15 +823,24 @@ __global__ void __launch_bounds__(CLIMB_BLK) k_hierarchy(int64_t n, const int32_
   __syncthreads();
   const int64_t p = B + threadIdx.x;
   if (p >= n) return;
-  const uint32_t oi = perm ? perm[p] : (uint32_t)p;
-  if (perm_out) perm_out[p] = (int32_t)oi;
-  const int sz = POINTS ? dim : 2 * dim;
-  const float *o = obj + (int64_t)oi * sz;
+  uint32_t oi;
   float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f};
-  for (int k = 0; k < dim; ++k) {
-    lo[k] = o[k];
-    hi[k] = POINTS ? lo[k] : o[dim + k];
+  if (POINTS && spts) {  // sorted points from the top-32 sort (3-D): no gather
+    const float4 q = spts[p];
+    oi = __float_as_uint(q.w);
+    lo[0] = hi[0] = q.x;
+    lo[1] = hi[1] = q.y;
+    lo[2] = hi[2] = q.z;
+  } else {
+    oi = perm ? perm[p] : (uint32_t)p;
+    const int sz = POINTS ? dim : 2 * dim;
+    const float *o = obj + (int64_t)oi * sz;
+    for (int k = 0; k < dim; ++k) {
+      lo[k] = o[k];
+      hi[k] = POINTS ? lo[k] : o[dim + k];
+    }
   }
+  if (perm_out) perm_out[p] = (int32_t)oi;
   const int64_t leaf = n - 1 + p;
   nodes[2 * leaf] = make_float4(lo[0], lo[1], lo[2], __int_as_float((int)oi));
   const int32_t leaf_rope = H.rope(p);
@@ -862,6 +886,128 @@ struct ClimbQueue {
   }
 };
 
+// ---------------------------------------------------------------------------
+// Point trees with 63-bit codes: sort by the top 32 code bits, then order the
+// runs of equal top bits (morton.hpp:113-121 stable order = full code, then
+// index).  Four 8-bit passes over (u32 key, u32 index) instead of eight over
+// (u64, u32); the run fix-up gathers each point once (the gather the
+// hierarchy needed anyway), recomputes its full code, and writes the sorted
+// points for the hierarchy.  Runs longer than FIX_MAX_RUN (dense clumps,
+// duplicates) make the host fall back to the full 63-bit sort.
+// ---------------------------------------------------------------------------
+constexpr int FIX_MAX_RUN = 512;
+#ifndef SPB_FIX_ILP
+#define SPB_FIX_ILP 4
+#endif
+constexpr int FIX_ILP = SPB_FIX_ILP;
+
+__global__ void __launch_bounds__(256) k_morton_top32(const float *__restrict__ pts, int64_t n, int width,
+                                                      const float *__restrict__ scene, uint32_t *__restrict__ key32) {
+  const int bits = width / 3;
+  const uint32_t top = bits >= 32 ? 0xffffffffu : ((1u << bits) - 1u);
+  const double scale = (double)(1ull << bits);
+  const int shift = 3 * bits - 32;
+  const float lo0 = scene[0], lo1 = scene[1], lo2 = scene[2], hi0 = scene[3], hi1 = scene[4], hi2 = scene[5];
+  auto code = [&](float x, float y, float z) -> uint32_t {
+    return (uint32_t)(encode_bins(axis_bin(x, lo0, hi0, scale, top), axis_bin(y, lo1, hi1, scale, top),
+                                  axis_bin(z, lo2, hi2, scale, top), 3) >> shift);
+  };
+  const int64_t chunks = n / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t ch = t0; ch < chunks; ch += stride) {
+    float x[4], y[4], z[4];
+    load4pts(pts, ch, x, y, z);
+    uint4 k;
+    k.x = code(x[0], y[0], z[0]);
+    k.y = code(x[1], y[1], z[1]);
+    k.z = code(x[2], y[2], z[2]);
+    k.w = code(x[3], y[3], z[3]);
+    reinterpret_cast<uint4 *>(key32)[ch] = k;
+  }
+  for (int64_t i = chunks * 4 + t0; i < n; i += stride) key32[i] = code(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+}
+
+// Sorted position p: gather the point, recompute its full code.
+__global__ void __launch_bounds__(256) k_fix_gather(const float *__restrict__ pts, int64_t n, int width,
+                                                    const float *__restrict__ scene,
+                                                    const uint32_t *__restrict__ idx, uint64_t *__restrict__ tcode,
+                                                    float4 *__restrict__ tpt) {
+  const int bits = width / 3;
+  const uint32_t top = bits >= 32 ? 0xffffffffu : ((1u << bits) - 1u);
+  const double scale = (double)(1ull << bits);
+  const float lo0 = scene[0], lo1 = scene[1], lo2 = scene[2], hi0 = scene[3], hi1 = scene[4], hi2 = scene[5];
+  // FIX_ILP sorted positions per thread, their random gathers all in flight
+  // together (a gather is one DRAM round trip; one thread per position would
+  // need the whole grid resident)
+  const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x) * FIX_ILP + threadIdx.x;
+  uint32_t i[FIX_ILP];
+  float x[FIX_ILP], y[FIX_ILP], z[FIX_ILP];
+#pragma unroll
+  for (int u = 0; u < FIX_ILP; ++u) {
+    const int64_t p = p0 + (int64_t)u * blockDim.x;
+    i[u] = p < n ? idx[p] : 0u;
+  }
+  // three 4-byte loads: measured faster here than gather_pt3's 16-byte
+  // blocks (3.41 vs 3.66 ms at 2^27; a uniformly random gather costs ~128 B of
+  // DRAM per point either way)
+#pragma unroll
+  for (int u = 0; u < FIX_ILP; ++u) {
+    const float *q = pts + 3 * (int64_t)i[u];
+    x[u] = __ldg(q);
+    y[u] = __ldg(q + 1);
+    z[u] = __ldg(q + 2);
+  }
+#pragma unroll
+  for (int u = 0; u < FIX_ILP; ++u) {
+    const int64_t p = p0 + (int64_t)u * blockDim.x;
+    if (p >= n) break;
+    tcode[p] = encode_bins(axis_bin(x[u], lo0, hi0, scale, top), axis_bin(y[u], lo1, hi1, scale, top),
+                           axis_bin(z[u], lo2, hi2, scale, top), 3);
+    tpt[p] = make_float4(x[u], y[u], z[u], __uint_as_float(i[u]));
+  }
+}
+
+// Each element of a run of equal top bits [s, e) takes rank #{q in run :
+// (code, index)(q) < (code, index)(p)} and moves to s + rank; singletons copy.
+__global__ void __launch_bounds__(256) k_fix_runs(const uint32_t *__restrict__ key32, int64_t n,
+                                                  const uint64_t *__restrict__ tcode, const float4 *__restrict__ tpt,
+                                                  uint64_t *__restrict__ code, uint32_t *__restrict__ perm,
+                                                  float4 *__restrict__ spts, int *overflow) {
+  {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const uint32_t k = key32[p];
+    int64_t s = p, e = p + 1;
+    while (s > 0 && p - s < FIX_MAX_RUN && key32[s - 1] == k) --s;
+    while (e < n && e - p <= FIX_MAX_RUN && key32[e] == k) ++e;
+    const uint64_t c = tcode[p];
+    const float4 q = tpt[p];
+    int64_t dst = p;
+    if (e - s > 1) {
+      if (e - s > FIX_MAX_RUN) {
+        *overflow = 1;
+        return;
+      }
+      const uint32_t i = __float_as_uint(q.w);
+      int64_t r = 0;
+      for (int64_t j = s; j < e; ++j) {
+        const uint64_t cj = tcode[j];
+        const uint32_t ij = __float_as_uint(tpt[j].w);
+        r += (cj < c) | ((cj == c) & (ij < i));
+      }
+      dst = s + r;
+    }
+    code[dst] = c;
+    perm[dst] = __float_as_uint(q.w);
+    spts[dst] = q;
+  }
+}
+
+#ifndef SPB_SORT_TOP32
+#define SPB_SORT_TOP32 1
+#endif
+
 void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, int width, Tree &t) {
   t.n = n;
   t.dim = dim;
@@ -891,11 +1037,43 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
 
   DevBuf<uint64_t> k0(n, c.stream), k1(n, c.stream);
   DevBuf<uint32_t> v0(n, c.stream), v1(n, c.stream);
-  morton_codes(c, objects, n, dim, points, width, t.scene, k0.get(), nullptr);
-  mark(c, "morton");
   uint64_t *ka = k0.get(), *kb = k1.get();
   uint32_t *va = v0.get(), *vb = v1.get();
-  radix_sort_pairs(c, &ka, &va, &kb, &vb, n, (width / dim) * dim, /*vals_iota=*/true);
+  const float4 *spts = nullptr;  // points in sorted order (the top-32 path writes them)
+  if (SPB_SORT_TOP32 && points && dim == 3 && width == 64 && n >= 2 && !c.async() && aligned16(objects)) {
+    uint32_t *k32a = reinterpret_cast<uint32_t *>(k0.get()), *k32b = k32a + n;
+    k_morton_top32<<<grid_for((n + 3) / 4, 256, 148 * 16), 256, 0, c.stream>>>(objects, n, width, t.scene, k32a);
+    SPB_LAUNCHED();
+    mark(c, "morton");
+    radix_sort_pairs(c, &k32a, &va, &k32b, &vb, n, 32, /*vals_iota=*/true);
+    // scratch in the node array (written by the hierarchy afterwards)
+    float4 *tpt = reinterpret_cast<float4 *>(t.nodes);
+    uint64_t *tcode = reinterpret_cast<uint64_t *>(tpt + n);
+    DevBuf<int> ovf(1, c.stream);
+    SPB_CUDA(cudaMemsetAsync(ovf.get(), 0, sizeof(int), c.stream));
+    k_fix_gather<<<(unsigned)((n + 256 * FIX_ILP - 1) / (256 * FIX_ILP)), 256, 0, c.stream>>>(
+        objects, n, width, t.scene, va, tcode, tpt);
+    SPB_LAUNCHED();
+    k_fix_runs<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(k32a, n, tcode, tpt, k1.get(), vb, t.leafpt,
+                                                                  ovf.get());
+    SPB_LAUNCHED();
+    int h_ovf = 0;
+    peek(c, {{ovf.get(), &h_ovf, sizeof(int)}});
+    if (!h_ovf) {
+      ka = k1.get();
+      kb = k0.get();
+      std::swap(va, vb);
+      spts = t.leafpt;
+    } else {
+      va = v0.get();  // a run longer than FIX_MAX_RUN: the full 63-bit sort below
+      vb = v1.get();
+    }
+  }
+  if (!spts) {
+    morton_codes(c, objects, n, dim, points, width, t.scene, k0.get(), nullptr);
+    mark(c, "morton");
+    radix_sort_pairs(c, &ka, &va, &kb, &vb, n, (width / dim) * dim, /*vals_iota=*/true);
+  }
   mark(c, "sort");
   DevBuf<int32_t> delta(n > 1 ? n - 1 : 1, c.stream), flags(n > 1 ? n - 1 : 1, c.stream);
   if (n > 1) {
@@ -907,10 +1085,10 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
   ClimbQueue q(c, n, SPB_CLIMB_LEVELS_POINTS);
   if (points)
     k_hierarchy<true><<<g, 256, 0, c.stream>>>(n, delta.get(), va, objects, dim, t.nodes, flags.get(), t.perm,
-                                               t.leafpt, q.levels, q.buf.get(), q.count.get());
+                                               t.leafpt, q.levels, q.buf.get(), q.count.get(), spts);
   else
     k_hierarchy<false><<<g, 256, 0, c.stream>>>(n, delta.get(), va, objects, dim, t.nodes, flags.get(), t.perm,
-                                                nullptr, q.levels, q.buf.get(), q.count.get());
+                                                nullptr, q.levels, q.buf.get(), q.count.get(), nullptr);
   SPB_LAUNCHED();
   q.finish(c, n, delta.get(), t.nodes, flags.get());
   mark(c, "hierarchy");
@@ -939,7 +1117,7 @@ void build_sorted_hierarchy(Ctx &c, const uint64_t *keys, int64_t m, int dim, co
   ClimbQueue q(c, m, SPB_CLIMB_LEVELS_CELLS);
   k_hierarchy<false><<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(m, delta.get(), nullptr, boxes, dim, t.nodes,
                                                                         flags.get(), nullptr, nullptr, q.levels,
-                                                                        q.buf.get(), q.count.get());
+                                                                        q.buf.get(), q.count.get(), nullptr);
   SPB_LAUNCHED();
   q.finish(c, m, delta.get(), t.nodes, flags.get());
 }

@@ -190,6 +190,28 @@ __host__ __device__ __forceinline__ bool aligned16(const void *p) {
   return (reinterpret_cast<uintptr_t>(p) & 15) == 0;
 }
 
+// Point i of a 16-byte aligned float[3n] array by one or two 16-byte loads of
+// the aligned blocks holding its 12 bytes (three 4-byte loads would each go to
+// L2 on their own: a random gather then costs ~4 sectors of DRAM traffic per
+// point instead of ~2).  The tail stays inside the array.
+__device__ __forceinline__ void gather_pt3(const float *__restrict__ pts, int64_t n, int64_t i, float &x, float &y,
+                                           float &z) {
+  const int64_t f = 3 * i, blk = f >> 2;
+  const int off = (int)(f & 3);
+  const float4 *v = reinterpret_cast<const float4 *>(pts);
+  if (off >= 2 && blk + 1 > (3 * n - 1) >> 2) {
+    x = __ldg(pts + f);
+    y = __ldg(pts + f + 1);
+    z = __ldg(pts + f + 2);
+    return;
+  }
+  const float4 a = __ldg(v + blk);
+  const float4 b = off >= 2 ? __ldg(v + blk + 1) : a;
+  x = off == 0 ? a.x : (off == 1 ? a.y : (off == 2 ? a.z : a.w));
+  y = off == 0 ? a.y : (off == 1 ? a.z : (off == 2 ? a.w : b.x));
+  z = off == 0 ? a.z : (off == 1 ? a.w : (off == 2 ? b.x : b.y));
+}
+
 // Decoupled look-back status words (bypass L1: other CTAs publish them).
 __device__ __forceinline__ void st_volatile_u64(unsigned long long *p, unsigned long long v) {
   asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");

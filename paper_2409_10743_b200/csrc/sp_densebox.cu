@@ -349,6 +349,39 @@ __global__ void k_cell_points(const uint32_t *__restrict__ order, const float *_
   }
 }
 
+// 3-D, 16-byte aligned points: four sorted positions per thread with their
+// random gathers in flight together, each point by one or two 16-byte loads
+// (gather_pt3).
+constexpr int CP_ILP = 4;
+__global__ void __launch_bounds__(256) k_cell_points3v(const uint32_t *__restrict__ order,
+                                                       const float *__restrict__ pts, int64_t n,
+                                                       float4 *__restrict__ cpts) {
+  const int64_t k0 = ((int64_t)blockIdx.x * blockDim.x) * CP_ILP + threadIdx.x;
+  uint32_t o[CP_ILP];
+  float x[CP_ILP], y[CP_ILP], z[CP_ILP];
+#pragma unroll
+  for (int u = 0; u < CP_ILP; ++u) {
+    const int64_t k = k0 + (int64_t)u * blockDim.x;
+    o[u] = k < n ? order[k] : 0u;
+  }
+#pragma unroll
+  for (int u = 0; u < CP_ILP; ++u) gather_pt3(pts, n, o[u], x[u], y[u], z[u]);
+#pragma unroll
+  for (int u = 0; u < CP_ILP; ++u) {
+    const int64_t k = k0 + (int64_t)u * blockDim.x;
+    if (k < n) cpts[k] = make_float4(x[u], y[u], z[u], __int_as_float((int)o[u]));
+  }
+}
+
+void cell_points(Ctx &c, const uint32_t *order, const float *pts, int64_t n, int dim, float4 *cpts) {
+  if (n <= 0) return;
+  if (dim == 3 && aligned16(pts))
+    k_cell_points3v<<<(unsigned)((n + 256 * CP_ILP - 1) / (256 * CP_ILP)), 256, 0, c.stream>>>(order, pts, n, cpts);
+  else
+    k_cell_points<<<grid_for(n, 256, 148 * 16), 256, 0, c.stream>>>(order, pts, n, dim, cpts);
+  SPB_LAUNCHED();
+}
+
 __device__ __forceinline__ void load_pt(const float *pts, int dim, int64_t i, float &x, float &y, float &z) {
   x = pts[i * dim];
   y = pts[i * dim + 1];
@@ -1053,8 +1086,7 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
   mark(c, "objects");
   const int64_t nobj = nd + ns;
   DevBuf<float4> cpts((size_t)n, c.stream);
-  k_cell_points<<<G, 256, 0, c.stream>>>(order, pts, n, dim, cpts.get());
-  SPB_LAUNCHED();
+  cell_points(c, order, pts, n, dim, cpts.get());
   Tree t;
   build_tree(c, objects.get(), nobj, dim, false, width, t);
   SPB_CUDA(cudaEventRecord(ev[1], c.stream));
@@ -1200,8 +1232,7 @@ bool build_cell_grid(Ctx &c, const float *pts, int64_t n, int dim, float eps, Ce
   g.order = va;
   mark(c, "sort");
   g.cpts = DevBuf<float4>((size_t)n, c.stream);
-  k_cell_points<<<G, 256, 0, c.stream>>>(va, pts, n, dim, g.cpts.get());
-  SPB_LAUNCHED();
+  cell_points(c, va, pts, n, dim, g.cpts.get());
   int64_t m = 0;
   g.cell_of = DevBuf<int32_t>((size_t)n, c.stream);
   g.cell_start = DevBuf<int64_t>((size_t)n, c.stream);  // capacity: m <= n
