@@ -351,12 +351,14 @@ __global__ void k_rs_scan(uint32_t *ghist) {
 #ifndef SPB_RS_MINBLOCKS32
 #define SPB_RS_MINBLOCKS32 3
 #endif
-template <int ITEMS, int THREADS, class K>
+// KO / oshift: the keys are written out as (KO)(key >> oshift) (a pass that
+// narrows 64-bit keys to their remaining 32 bits for the following passes).
+template <int ITEMS, int THREADS, class K, class KO = K>
 __global__ void __launch_bounds__(THREADS, (THREADS * ITEMS <= 2048) ? 4
                                            : (sizeof(K) == 4 ? SPB_RS_MINBLOCKS32 : SPB_RS_MINBLOCKS)) k_rs_onesweep(
-    const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
+    const K *__restrict__ kin, const uint32_t *__restrict__ vin, KO *__restrict__ kout,
     uint32_t *__restrict__ vout, int64_t n, int shift, const uint32_t *__restrict__ binbase,
-    unsigned long long *lookback, uint32_t *tile_ctr, uint32_t tag) {
+    unsigned long long *lookback, uint32_t *tile_ctr, uint32_t tag, int oshift = 0) {
   constexpr int TILE = THREADS * ITEMS;
   constexpr int WARPS = THREADS / 32;
   extern __shared__ __align__(16) unsigned char rs_smem[];
@@ -495,7 +497,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS * ITEMS <= 2048) ? 4
     const K k = skeys[pos];
     const uint32_t d = (uint32_t)(k >> shift) & 0xffu;
     const uint32_t o = s_gbase[d] + (uint32_t)pos - s_dstart[d];
-    kout[o] = k;
+    kout[o] = (KO)(k >> oshift);
     vout[o] = svals[pos];
   }
 }
@@ -551,6 +553,58 @@ void radix_sort_pairs(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_
   }
   const int npass = std::max(1, (key_bits + 7) / 8);
   onesweep_passes<SPB_RS_ITEMS, SPB_RS_THREADS, uint64_t>(c, keys, vals, keys_alt, vals_alt, n, npass, vals_iota);
+}
+
+// Stable sort of (u64 key < 2^40, u32 value) in five 8-bit passes: the first
+// moves the 64-bit keys and writes key >> 8 as 32-bit keys, the other four
+// move (u32, u32) pairs (16 instead of 24 bytes per element and pass).  Only
+// the sorted values come back (*vals); the keys are consumed.  k32 and k32_alt
+// hold n u32 each.
+void radix_sort_pairs_40(Ctx &c, const uint64_t *keys, uint32_t **vals, uint32_t **vals_alt, uint32_t *k32,
+                         uint32_t *k32_alt, int64_t n, bool vals_iota) {
+  if (n <= 1) {
+    if (n == 1 && vals_iota) SPB_CUDA(cudaMemsetAsync(*vals, 0, sizeof(uint32_t), c.stream));
+    return;
+  }
+  constexpr int ITEMS = SPB_RS_ITEMS, THREADS = SPB_RS_THREADS, TILE = ITEMS * THREADS;
+  constexpr size_t SMEM64 = rs_smem_bytes<ITEMS, THREADS, uint64_t>();
+  constexpr size_t SMEM32 = rs_smem_bytes<ITEMS, THREADS, uint32_t>();
+  {
+    static std::mutex mu;
+    static uint64_t opted = 0;
+    std::lock_guard<std::mutex> g(mu);
+    if (c.device >= 64 || !((opted >> c.device) & 1)) {
+      SPB_CUDA(cudaFuncSetAttribute(k_rs_onesweep<ITEMS, THREADS, uint64_t, uint32_t>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM64));
+      SPB_CUDA(cudaFuncSetAttribute(k_rs_onesweep<ITEMS, THREADS, uint32_t>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM32));
+      if (c.device < 64) opted |= 1ull << c.device;
+    }
+  }
+  constexpr int npass = 5;
+  const int64_t ntiles = (n + TILE - 1) / TILE;
+  DevBuf<uint32_t> hist((size_t)npass * RS_BINS + npass, c.stream);
+  DevBuf<unsigned long long> lookback((size_t)ntiles * RS_BINS, c.stream);
+  SPB_CUDA(cudaMemsetAsync(hist.get(), 0, hist.n * sizeof(uint32_t), c.stream));
+  SPB_CUDA(cudaMemsetAsync(lookback.get(), 0, lookback.n * sizeof(unsigned long long), c.stream));
+  k_rs_hist<uint64_t><<<grid_for(n, 256, 148 * 4), 256, 0, c.stream>>>(keys, n, npass, hist.get());
+  SPB_LAUNCHED();
+  k_rs_scan<<<npass, RS_BINS, 0, c.stream>>>(hist.get());
+  SPB_LAUNCHED();
+  uint32_t *ctr = hist.get() + (size_t)npass * RS_BINS;
+  k_rs_onesweep<ITEMS, THREADS, uint64_t, uint32_t><<<(unsigned)ntiles, THREADS, SMEM64, c.stream>>>(
+      keys, vals_iota ? nullptr : *vals, k32, *vals_alt, n, 0, hist.get(), lookback.get(), ctr, 1u, 8);
+  SPB_LAUNCHED();
+  std::swap(*vals, *vals_alt);
+  uint32_t *ka = k32, *kb = k32_alt;
+  for (int p = 1; p < npass; ++p) {
+    k_rs_onesweep<ITEMS, THREADS, uint32_t><<<(unsigned)ntiles, THREADS, SMEM32, c.stream>>>(
+        ka, *vals, kb, *vals_alt, n, 8 * (p - 1), hist.get() + (size_t)p * RS_BINS, lookback.get(), ctr + p,
+        (uint32_t)(2 * p + 1));
+    SPB_LAUNCHED();
+    std::swap(ka, kb);
+    std::swap(*vals, *vals_alt);
+  }
 }
 
 void radix_sort_pairs(Ctx &c, uint32_t **keys, uint32_t **vals, uint32_t **keys_alt, uint32_t **vals_alt, int64_t n,

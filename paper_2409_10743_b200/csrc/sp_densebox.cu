@@ -373,6 +373,33 @@ __global__ void __launch_bounds__(256) k_cell_points3v(const uint32_t *__restric
   }
 }
 
+// The same gather, also writing each sorted point's Morton cell key (the
+// 40-bit sort returns no keys: k_cell_keys_p3v's formula on the gathered point).
+__global__ void __launch_bounds__(256) k_cell_points3v_keys(const uint32_t *__restrict__ order,
+                                                            const float *__restrict__ pts, int64_t n,
+                                                            const float *__restrict__ scene, float cell,
+                                                            float4 *__restrict__ cpts, uint64_t *__restrict__ keys) {
+  const float a0 = scene[0], a1 = scene[1], a2 = scene[2];
+  const int64_t k0 = ((int64_t)blockIdx.x * blockDim.x) * CP_ILP + threadIdx.x;
+  uint32_t o[CP_ILP];
+  float x[CP_ILP], y[CP_ILP], z[CP_ILP];
+#pragma unroll
+  for (int u = 0; u < CP_ILP; ++u) {
+    const int64_t k = k0 + (int64_t)u * blockDim.x;
+    o[u] = k < n ? order[k] : 0u;
+  }
+#pragma unroll
+  for (int u = 0; u < CP_ILP; ++u) gather_pt3(pts, n, o[u], x[u], y[u], z[u]);
+#pragma unroll
+  for (int u = 0; u < CP_ILP; ++u) {
+    const int64_t k = k0 + (int64_t)u * blockDim.x;
+    if (k >= n) continue;
+    cpts[k] = make_float4(x[u], y[u], z[u], __int_as_float((int)o[u]));
+    keys[k] = spread3_21((uint64_t)cell_coord(x[u], a0, cell)) | (spread3_21((uint64_t)cell_coord(y[u], a1, cell)) << 1) |
+              (spread3_21((uint64_t)cell_coord(z[u], a2, cell)) << 2);
+  }
+}
+
 void cell_points(Ctx &c, const uint32_t *order, const float *pts, int64_t n, int dim, float4 *cpts) {
   if (n <= 0) return;
   if (dim == 3 && aligned16(pts))
@@ -1181,6 +1208,9 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
 // false (nothing computed) when the grid does not apply: coordinates that
 // could saturate (no dense cells in the reference either) or cell coordinates
 // too wide for a 63-bit Morton key.
+#ifndef SPB_SORT40
+#define SPB_SORT40 1
+#endif
 struct CellGrid {
   int64_t m = 0;
   DevBuf<uint64_t> k0, k1;
@@ -1227,12 +1257,25 @@ bool build_cell_grid(Ctx &c, const float *pts, int64_t n, int dim, float eps, Ce
   mark(c, "morton");
   uint64_t *ka = g.k0.get(), *kb = g.k1.get();
   uint32_t *va = g.v0.get(), *vb = g.v1.get();
-  radix_sort_pairs(c, &ka, &va, &kb, &vb, n, bits * dim, true);
-  g.keys = ka;
-  g.order = va;
-  mark(c, "sort");
   g.cpts = DevBuf<float4>((size_t)n, c.stream);
-  cell_points(c, va, pts, n, dim, g.cpts.get());
+  if (SPB_SORT40 && dim == 3 && bits * dim > 32 && bits * dim <= 40 && aligned16(pts)) {
+    // five passes, the last four over 32-bit keys; the keys are recomputed
+    // from the gathered points
+    uint32_t *k32 = reinterpret_cast<uint32_t *>(kb);
+    radix_sort_pairs_40(c, ka, &va, &vb, k32, k32 + n, n, true);
+    g.order = va;
+    mark(c, "sort");
+    k_cell_points3v_keys<<<(unsigned)((n + 256 * CP_ILP - 1) / (256 * CP_ILP)), 256, 0, c.stream>>>(
+        va, pts, n, scene.get(), cell, g.cpts.get(), ka);
+    SPB_LAUNCHED();
+    g.keys = ka;
+  } else {
+    radix_sort_pairs(c, &ka, &va, &kb, &vb, n, bits * dim, true);
+    g.keys = ka;
+    g.order = va;
+    mark(c, "sort");
+    cell_points(c, va, pts, n, dim, g.cpts.get());
+  }
   int64_t m = 0;
   g.cell_of = DevBuf<int32_t>((size_t)n, c.stream);
   g.cell_start = DevBuf<int64_t>((size_t)n, c.stream);  // capacity: m <= n

@@ -152,6 +152,8 @@ void radix_sort_pairs(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_
                       int key_bits, bool vals_iota);
 void radix_sort_pairs(Ctx &c, uint32_t **keys, uint32_t **vals, uint32_t **keys_alt, uint32_t **vals_alt, int64_t n,
                       int key_bits, bool vals_iota);
+void radix_sort_pairs_40(Ctx &c, const uint64_t *keys, uint32_t **vals, uint32_t **vals_alt, uint32_t *k32,
+                         uint32_t *k32_alt, int64_t n, bool vals_iota);
 // Full Bvh::build into `t` (allocates t.nodes/perm/scene). Throws
 // InvalidArgument on non-finite input.
 void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, int width, Tree &t);
