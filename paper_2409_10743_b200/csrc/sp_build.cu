@@ -982,6 +982,73 @@ __global__ void __launch_bounds__(256) k_morton_top32(const float *__restrict__ 
   for (int64_t i = chunks * 4 + t0; i < n; i += stride) key32[i] = code(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
 }
 
+// Query ordering (sort_points): top 32 bits and the full code, both in input
+// order; the run fix-up below reads full codes only for members of runs.
+__global__ void __launch_bounds__(256) k_morton_top32_full(const float *__restrict__ pts, int64_t n, int width,
+                                                           const float *__restrict__ scene,
+                                                           uint32_t *__restrict__ key32, uint64_t *__restrict__ code) {
+  const int bits = width / 3;
+  const uint32_t top = bits >= 32 ? 0xffffffffu : ((1u << bits) - 1u);
+  const double scale = (double)(1ull << bits);
+  const int shift = 3 * bits - 32;
+  const float lo0 = scene[0], lo1 = scene[1], lo2 = scene[2], hi0 = scene[3], hi1 = scene[4], hi2 = scene[5];
+  auto full = [&](float x, float y, float z) -> uint64_t {
+    return encode_bins(axis_bin(x, lo0, hi0, scale, top), axis_bin(y, lo1, hi1, scale, top),
+                       axis_bin(z, lo2, hi2, scale, top), 3);
+  };
+  const int64_t chunks = n / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t ch = t0; ch < chunks; ch += stride) {
+    float x[4], y[4], z[4];
+    load4pts(pts, ch, x, y, z);
+    uint64_t c[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c[j] = full(x[j], y[j], z[j]);
+    reinterpret_cast<uint4 *>(key32)[ch] =
+        make_uint4((uint32_t)(c[0] >> shift), (uint32_t)(c[1] >> shift), (uint32_t)(c[2] >> shift),
+                   (uint32_t)(c[3] >> shift));
+    reinterpret_cast<ulonglong2 *>(code)[2 * ch] = make_ulonglong2(c[0], c[1]);
+    reinterpret_cast<ulonglong2 *>(code)[2 * ch + 1] = make_ulonglong2(c[2], c[3]);
+  }
+  for (int64_t i = chunks * 4 + t0; i < n; i += stride) {
+    const uint64_t c = full(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+    key32[i] = (uint32_t)(c >> shift);
+    code[i] = c;
+  }
+}
+
+// Runs of equal top bits ordered by (full code, index); singletons keep
+// their place.  Writes the final order only.
+__global__ void __launch_bounds__(256) k_fix_runs_order(const uint32_t *__restrict__ key32, int64_t n,
+                                                        const uint32_t *__restrict__ idx,
+                                                        const uint64_t *__restrict__ code, int32_t *__restrict__ order,
+                                                        int *overflow) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t k = key32[p];
+  int64_t s = p, e = p + 1;
+  while (s > 0 && p - s < FIX_MAX_RUN && key32[s - 1] == k) --s;
+  while (e < n && e - p <= FIX_MAX_RUN && key32[e] == k) ++e;
+  const uint32_t i = idx[p];
+  int64_t dst = p;
+  if (e - s > 1) {
+    if (e - s > FIX_MAX_RUN) {
+      *overflow = 1;
+      return;
+    }
+    const uint64_t c = code[i];
+    int64_t r = 0;
+    for (int64_t j = s; j < e; ++j) {
+      const uint32_t ij = idx[j];
+      const uint64_t cj = code[ij];
+      r += (cj < c) | ((cj == c) & (ij < i));
+    }
+    dst = s + r;
+  }
+  order[dst] = (int32_t)i;
+}
+
 // Sorted position p: gather the point, recompute its full code.
 __global__ void __launch_bounds__(256) k_fix_gather(const float *__restrict__ pts, int64_t n, int width,
                                                     const float *__restrict__ scene,
@@ -1183,6 +1250,22 @@ void sort_points(Ctx &c, const float *pts, int64_t n, int dim, int32_t *order) {
   scene_bounds(c, pts, n, dim, true, scene.get(), bad.get());
   DevBuf<uint64_t> k0(n, c.stream), k1(n, c.stream);
   DevBuf<uint32_t> v0(n, c.stream), v1(n, c.stream);
+  if (SPB_SORT_TOP32 && dim == 3 && n >= 2 && !c.async() && aligned16(pts)) {
+    // top 32 bits in four passes, runs ordered by the full codes (k1)
+    uint32_t *k32a = reinterpret_cast<uint32_t *>(k0.get()), *k32b = k32a + n;
+    uint32_t *va = v0.get(), *vb = v1.get();
+    k_morton_top32_full<<<grid_for((n + 3) / 4, 256, 148 * 16), 256, 0, c.stream>>>(pts, n, 64, scene.get(), k32a,
+                                                                                   k1.get());
+    SPB_LAUNCHED();
+    radix_sort_pairs(c, &k32a, &va, &k32b, &vb, n, 32, /*vals_iota=*/true);
+    DevBuf<int> ovf(1, c.stream);
+    SPB_CUDA(cudaMemsetAsync(ovf.get(), 0, sizeof(int), c.stream));
+    k_fix_runs_order<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(k32a, n, va, k1.get(), order, ovf.get());
+    SPB_LAUNCHED();
+    int h_ovf = 0;
+    peek(c, {{ovf.get(), &h_ovf, sizeof(int)}});
+    if (!h_ovf) return;
+  }
   morton_codes(c, pts, n, dim, true, 64, scene.get(), k0.get(), nullptr);
   uint64_t *ka = k0.get(), *kb = k1.get();
   uint32_t *va = v0.get(), *vb = v1.get();
