@@ -213,12 +213,25 @@ __device__ __forceinline__ void gather_pt3(const float *__restrict__ pts, int64_
 }
 
 // Decoupled look-back status words (bypass L1: other CTAs publish them).
+#ifndef SPB_LOOKBACK_GPU
+#define SPB_LOOKBACK_GPU 1
+#endif
+// Look-back status words: relaxed GPU-scope loads and stores (L2-coherent;
+// the status value itself carries the data, so no ordering is needed).
 __device__ __forceinline__ void st_volatile_u64(unsigned long long *p, unsigned long long v) {
+#if SPB_LOOKBACK_GPU
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+#else
   asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+#endif
 }
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long *p) {
   unsigned long long v;
+#if SPB_LOOKBACK_GPU
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+#else
   asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+#endif
   return v;
 }
 
