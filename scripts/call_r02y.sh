@@ -1,0 +1,5 @@
+# A/B: look-back relaxed.gpu (sd1 = all new) vs volatile (lbv); climb D from shared memory (sd1) vs global (sd0)
+mkdir -p gpurun_out
+for v in sd0 lbv sd1 sd0 lbv sd1; do cp var/$v.so paper_2409_10743_b200/libspb200.so; echo "== $v"; timeout 200 python scripts/build_probe.py 2>&1 | tail -1 | cut -c1-200; timeout 120 python scripts/ab_labels.py 134217728 3 2>&1 | tail -1 | cut -c 60-300; done
+cp var/sd1.so paper_2409_10743_b200/libspb200.so
+timeout 1500 python -m pytest tests/test_gpu_bvh.py tests/test_gpu_scale.py tests/test_gpu_sanitizer.py -q -x 2>&1 | tail -2
