@@ -1,5 +1,5 @@
-# A/B: Morton-reach cut-off of the cell merge walks
+# A/B: warp-common Morton reach cut-off of the cell merge walks
 mkdir -p gpurun_out
-for v in noreach reach refine reach; do cp var/$v.so paper_2409_10743_b200/libspb200.so; echo "== $v"; timeout 120 python scripts/ab_labels.py 134217728 3 2>&1 | tail -1 | cut -c 1-300; done
-timeout 300 python scripts/merge_walks.py 134217728
+for v in norch rch norch rch; do cp var/$v.so paper_2409_10743_b200/libspb200.so; echo "== $v"; timeout 120 python scripts/ab_labels.py 134217728 3 2>&1 | tail -1 | cut -c 1-300; done
+cp var/rch.so paper_2409_10743_b200/libspb200.so
 timeout 1500 python -m pytest tests/test_gpu_scale.py tests/test_gpu_dbscan.py tests/test_gpu_slabs.py -x -q 2>&1 | tail -2
