@@ -936,10 +936,17 @@ __global__ void __launch_bounds__(256) k_fof_cells_core_min(int64_t m, int64_t n
       multi[r] = 1;
     }
     key = r;
-    const int64_t s = cell_start[a], e = a + 1 < m ? cell_start[a + 1] : n;
-    for (int64_t k = s; k < e; ++k) {
-      const int32_t o = ids ? ids[order[k]] : (int32_t)order[k];
-      v = o < v ? o : v;
+    const int64_t s = cell_start[a];
+    if (!ids) {
+      // the sort is stable over original indices: a cell's first point has
+      // its smallest index
+      v = (int32_t)order[s];
+    } else {
+      const int64_t e = a + 1 < m ? cell_start[a + 1] : n;
+      for (int64_t k = s; k < e; ++k) {
+        const int32_t o = ids[order[k]];
+        v = o < v ? o : v;
+      }
     }
   }
   const uint32_t peers = __match_any_sync(0xffffffffu, key);
