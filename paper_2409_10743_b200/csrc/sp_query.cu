@@ -355,7 +355,10 @@ int64_t pair_list(Ctx &c, const Tree &t, float eps, int32_t *pairs, int64_t capa
 // stack (near child popped first) and its strict `dist > worst` pruning, with
 // the candidate max-heap in local memory.
 // ---------------------------------------------------------------------------
-constexpr int KNN_STACK = 100;  // tree depth <= 96 prefix bits + 1
+constexpr int KNN_STACK = 100;
+#ifndef SPB_KNN_STACK2
+#define SPB_KNN_STACK2 1
+#endif  // tree depth <= 96 prefix bits + 1
 
 __device__ __forceinline__ float box_dist(float x, float y, float z, const float4 &lo, const float4 &hi) {
   return __double2float_rn(__dsqrt_rn(gap2(x, y, z, lo, hi)));
@@ -403,8 +406,14 @@ __global__ void __launch_bounds__(128) k_knn(const float4 *__restrict__ nodes, i
   // entry carries what its node's box load already gave: ref = the left child
   // of an internal node, or ~object for a leaf, so a pop never re-reads the
   // node itself (42.6 -> 41.3 ms at C4).
+#if SPB_KNN_STACK2
+  // one 8-byte entry {distance bits, ref} per level: a push or pop is one
+  // local access instead of two
+  uint2 stk[KNN_STACK];
+#else
   float sd[KNN_STACK];
   int32_t sr[KNN_STACK];
+#endif
   int top = 0;
   float d;
   int32_t ref = 0;
@@ -418,8 +427,14 @@ __global__ void __launch_bounds__(128) k_knn(const float4 *__restrict__ nodes, i
     if (!have) {
       if (top == 0) break;
       --top;
+#if SPB_KNN_STACK2
+      const uint2 e = stk[top];
+      d = __uint_as_float(e.x);
+      ref = (int32_t)e.y;
+#else
       d = sd[top];
       ref = sr[top];
+#endif
     }
     have = false;
     if (size == kk && d > worst()) continue;
@@ -486,7 +501,11 @@ __global__ void __launch_bounds__(128) k_knn(const float4 *__restrict__ nodes, i
     const float w = worst();
     const bool keep_f = !(full && df > w), keep_n = !(full && dn > w);
     if (keep_n) {
+#if SPB_KNN_STACK2
+      if (keep_f && top < KNN_STACK) { stk[top] = make_uint2(__float_as_uint(df), (uint32_t)rf); ++top; }
+#else
       if (keep_f && top < KNN_STACK) { sd[top] = df; sr[top] = rf; ++top; }
+#endif
       d = dn;
       ref = rn;
       have = true;
