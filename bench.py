@@ -469,7 +469,8 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": value / ARBORX_A100_PTS_S,
-        "vs_baseline_ref": "ArborX on 1x A100: ~37M HACC particles FoF in < 0.15 s (PAPER.md:489-493) = %.3g points/s"
+        "vs_baseline_ref": "ArborX on 1x A100: ~37M HACC particles FoF in < 0.15 s (PAPER.md:489-493) = %.3g "
+                           "points/s; a bound on a different (real HACC) dataset, not a like-for-like ratio"
                            % ARBORX_A100_PTS_S,
         "dtype": "f32 (exact f64 distance predicate)",
         "data": "synthetic: the SURVEY field H(n) from the reference generator (generate.cpp:17-66)",
