@@ -1093,43 +1093,110 @@ __global__ void __launch_bounds__(256) k_fix_gather(const float *__restrict__ pt
 
 // Each element of a run of equal top bits [s, e) takes rank #{q in run :
 // (code, index)(q) < (code, index)(p)} and moves to s + rank; singletons copy.
-__global__ void __launch_bounds__(256) k_fix_runs(const uint32_t *__restrict__ key32, int64_t n,
-                                                  const uint64_t *__restrict__ tcode, const float4 *__restrict__ tpt,
-                                                  uint64_t *__restrict__ code, uint32_t *__restrict__ perm,
-                                                  float4 *__restrict__ spts, int *overflow) {
-  {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    const uint32_t k = key32[p];
-    int64_t s = p, e = p + 1;
-    while (s > 0 && p - s < FIX_MAX_RUN && key32[s - 1] == k) --s;
-    while (e < n && e - p <= FIX_MAX_RUN && key32[e] == k) ++e;
-    const uint64_t c = tcode[p];
-    const float4 q = tpt[p];
+// The same in shared memory: a CTA stages the keys, codes and indices of its
+// FIX_CH positions and FIX_MAX_RUN more on each side (every run of at most
+// FIX_MAX_RUN through a position of the chunk lies inside), so the run scans
+// and the O(run) ranking read shared memory (clustered fields have runs of
+// hundreds: the global-memory version took 20 ms at 2^27 on H(2^27)).
+constexpr int FIX_CH = 2048;
+constexpr int FIX_WIN = FIX_CH + 2 * FIX_MAX_RUN;
+__global__ void __launch_bounds__(256) k_fix_runs_win(const uint32_t *__restrict__ key32, int64_t n,
+                                                      const uint64_t *__restrict__ tcode,
+                                                      const float4 *__restrict__ tpt, uint64_t *__restrict__ code,
+                                                      uint32_t *__restrict__ perm, float4 *__restrict__ spts,
+                                                      int *overflow) {
+  __shared__ uint32_t sk[FIX_WIN];
+  __shared__ uint64_t sc[FIX_WIN];
+  __shared__ uint32_t si[FIX_WIN];
+  const int64_t c0 = (int64_t)blockIdx.x * FIX_CH, w0 = c0 - FIX_MAX_RUN;
+  const int lo_lim = w0 < 0 ? (int)(-w0) : 0;
+  const int hi_lim = (int)((n - w0) < FIX_WIN ? (n - w0) : FIX_WIN);
+  for (int i = threadIdx.x; i < FIX_WIN; i += blockDim.x) {
+    if (i >= lo_lim && i < hi_lim) {
+      const int64_t q = w0 + i;
+      sk[i] = key32[q];
+      sc[i] = tcode[q];
+      si[i] = __float_as_uint(__ldg(&tpt[q].w));
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < FIX_CH; j += blockDim.x) {
+    const int64_t p = c0 + j;
+    if (p >= n) break;
+    const int li = j + FIX_MAX_RUN;
+    const uint32_t k = sk[li];
+    int s = li, e = li + 1;
+    while (s > lo_lim && li - s < FIX_MAX_RUN && sk[s - 1] == k) --s;
+    while (e < hi_lim && e - li <= FIX_MAX_RUN && sk[e] == k) ++e;
+    const uint64_t c = sc[li];
+    const uint32_t i = si[li];
     int64_t dst = p;
     if (e - s > 1) {
       if (e - s > FIX_MAX_RUN) {
         *overflow = 1;
-        return;
+        continue;
       }
-      const uint32_t i = __float_as_uint(q.w);
-      int64_t r = 0;
-      for (int64_t j = s; j < e; ++j) {
-        const uint64_t cj = tcode[j];
-        const uint32_t ij = __float_as_uint(tpt[j].w);
-        r += (cj < c) | ((cj == c) & (ij < i));
+      int r = 0;
+      for (int q = s; q < e; ++q) {
+        const uint64_t cq = sc[q];
+        r += (cq < c) | ((cq == c) & (si[q] < i));
       }
-      dst = s + r;
+      dst = w0 + s + r;
     }
     code[dst] = c;
-    perm[dst] = __float_as_uint(q.w);
-    spts[dst] = q;
+    perm[dst] = i;
+    spts[dst] = tpt[p];
   }
 }
+
 
 #ifndef SPB_SORT_TOP32
 #define SPB_SORT_TOP32 1
 #endif
+
+// Clustered inputs make long runs of equal top bits (halo cores: hundreds of
+// points per top-32 cell on H(2^27)), for which the top-32 sort would end in
+// the fallback after all its work.  A sample of every 128th point predicts
+// them: a run of 3/4 FIX_MAX_RUN points leaves about 3 copies of its key in
+// the sample, so three equal keys among the sorted sample keys choose the
+// 63-bit sort (on uniform points at 2^27 three equal sampled keys have
+// probability ~1%; a miss only costs the fallback).
+__global__ void __launch_bounds__(256) k_sample_top32(const float *__restrict__ pts, int64_t n, int64_t stride,
+                                                      int64_t ns, int width, const float *__restrict__ scene,
+                                                      uint32_t *__restrict__ key32) {
+  const int bits = width / 3;
+  const uint32_t top = bits >= 32 ? 0xffffffffu : ((1u << bits) - 1u);
+  const double scale = (double)(1ull << bits);
+  const int shift = 3 * bits - 32;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ns) return;
+  const float *q = pts + 3 * (i * stride);
+  key32[i] = (uint32_t)(encode_bins(axis_bin(q[0], scene[0], scene[3], scale, top),
+                                    axis_bin(q[1], scene[1], scene[4], scale, top),
+                                    axis_bin(q[2], scene[2], scene[5], scale, top), 3) >> shift);
+}
+__global__ void __launch_bounds__(256) k_sample_triples(const uint32_t *__restrict__ key32, int64_t ns,
+                                                        int *found) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i + 2 < ns && key32[i] == key32[i + 2]) *found = 1;
+}
+bool top32_runs_short(Ctx &c, const float *pts, int64_t n, const float *scene) {
+  if (n < (1 << 18)) return true;  // small: a fallback costs little
+  const int64_t stride = 128, ns = n / stride;
+  DevBuf<uint32_t> k0((size_t)ns, c.stream), k1((size_t)ns, c.stream), v0((size_t)ns, c.stream),
+      v1((size_t)ns, c.stream);
+  DevBuf<int> found(1, c.stream);
+  SPB_CUDA(cudaMemsetAsync(found.get(), 0, sizeof(int), c.stream));
+  k_sample_top32<<<(unsigned)((ns + 255) / 256), 256, 0, c.stream>>>(pts, n, stride, ns, 64, scene, k0.get());
+  SPB_LAUNCHED();
+  uint32_t *ka = k0.get(), *kb = k1.get(), *va = v0.get(), *vb = v1.get();
+  radix_sort_pairs(c, &ka, &va, &kb, &vb, ns, 32, true);
+  k_sample_triples<<<(unsigned)((ns + 255) / 256), 256, 0, c.stream>>>(ka, ns, found.get());
+  SPB_LAUNCHED();
+  int h = 0;
+  peek(c, {{found.get(), &h, sizeof(int)}});
+  return h == 0;
+}
 
 void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, int width, Tree &t) {
   t.n = n;
@@ -1163,7 +1230,8 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
   uint64_t *ka = k0.get(), *kb = k1.get();
   uint32_t *va = v0.get(), *vb = v1.get();
   const float4 *spts = nullptr;  // points in sorted order (the top-32 path writes them)
-  if (SPB_SORT_TOP32 && points && dim == 3 && width == 64 && n >= 2 && !c.async() && aligned16(objects)) {
+  if (SPB_SORT_TOP32 && points && dim == 3 && width == 64 && n >= 2 && !c.async() && aligned16(objects) &&
+      top32_runs_short(c, objects, n, t.scene)) {
     uint32_t *k32a = reinterpret_cast<uint32_t *>(k0.get()), *k32b = k32a + n;
     k_morton_top32<<<grid_for((n + 3) / 4, 256, 148 * 16), 256, 0, c.stream>>>(objects, n, width, t.scene, k32a);
     SPB_LAUNCHED();
@@ -1177,7 +1245,7 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
     k_fix_gather<<<(unsigned)((n + 256 * FIX_ILP - 1) / (256 * FIX_ILP)), 256, 0, c.stream>>>(
         objects, n, width, t.scene, va, tcode, tpt);
     SPB_LAUNCHED();
-    k_fix_runs<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(k32a, n, tcode, tpt, k1.get(), vb, t.leafpt,
+    k_fix_runs_win<<<(unsigned)((n + FIX_CH - 1) / FIX_CH), 256, 0, c.stream>>>(k32a, n, tcode, tpt, k1.get(), vb, t.leafpt,
                                                                   ovf.get());
     SPB_LAUNCHED();
     int h_ovf = 0;
@@ -1252,7 +1320,7 @@ void sort_points(Ctx &c, const float *pts, int64_t n, int dim, int32_t *order) {
   scene_bounds(c, pts, n, dim, true, scene.get(), bad.get());
   DevBuf<uint64_t> k0(n, c.stream), k1(n, c.stream);
   DevBuf<uint32_t> v0(n, c.stream), v1(n, c.stream);
-  if (SPB_SORT_TOP32 && dim == 3 && n >= 2 && !c.async() && aligned16(pts)) {
+  if (SPB_SORT_TOP32 && dim == 3 && n >= 2 && !c.async() && aligned16(pts) && top32_runs_short(c, pts, n, scene.get())) {
     // top 32 bits in four passes, runs ordered by the full codes (k1)
     uint32_t *k32a = reinterpret_cast<uint32_t *>(k0.get()), *k32b = k32a + n;
     uint32_t *va = v0.get(), *vb = v1.get();

@@ -16,3 +16,13 @@ for n in (1 << 24, 1 << 27):
                   flush=True)
         del b
     del p
+# the clustered field (the bench's bvh_build input)
+n = 1 << 27
+p = sp.generate_field(n, seed=2409, ctx=ctx)
+for it in range(3):
+    b = sp.Bvh.build(p, ctx=ctx)
+    ph = ctx.phases()
+    tot = sum(v for _, v in ph)
+    if it == 2:
+        print("field n=2^27 build %.3f ms" % tot, [(k, round(v, 3)) for k, v in ph], flush=True)
+    del b
