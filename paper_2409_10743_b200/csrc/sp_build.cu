@@ -1100,12 +1100,11 @@ __global__ void __launch_bounds__(256) k_fix_gather(const float *__restrict__ pt
 // hundreds: the global-memory version took 20 ms at 2^27 on H(2^27)).
 constexpr int FIX_CH = 2048;
 constexpr int FIX_WIN = FIX_CH + 2 * FIX_MAX_RUN;
-__global__ void __launch_bounds__(256) k_fix_runs_win(const uint32_t *__restrict__ key32, int64_t n,
-                                                      const uint64_t *__restrict__ tcode,
+template <int SHIFT>  // runs: equal code >> SHIFT (31: top 32 of 63 bits, 23: top 40)
+__global__ void __launch_bounds__(256) k_fix_runs_win(int64_t n, const uint64_t *__restrict__ tcode,
                                                       const float4 *__restrict__ tpt, uint64_t *__restrict__ code,
                                                       uint32_t *__restrict__ perm, float4 *__restrict__ spts,
                                                       int *overflow) {
-  __shared__ uint32_t sk[FIX_WIN];
   __shared__ uint64_t sc[FIX_WIN];
   __shared__ uint32_t si[FIX_WIN];
   const int64_t c0 = (int64_t)blockIdx.x * FIX_CH, w0 = c0 - FIX_MAX_RUN;
@@ -1114,7 +1113,6 @@ __global__ void __launch_bounds__(256) k_fix_runs_win(const uint32_t *__restrict
   for (int i = threadIdx.x; i < FIX_WIN; i += blockDim.x) {
     if (i >= lo_lim && i < hi_lim) {
       const int64_t q = w0 + i;
-      sk[i] = key32[q];
       sc[i] = tcode[q];
       si[i] = __float_as_uint(__ldg(&tpt[q].w));
     }
@@ -1124,11 +1122,10 @@ __global__ void __launch_bounds__(256) k_fix_runs_win(const uint32_t *__restrict
     const int64_t p = c0 + j;
     if (p >= n) break;
     const int li = j + FIX_MAX_RUN;
-    const uint32_t k = sk[li];
+    const uint64_t c = sc[li], k = c >> SHIFT;
     int s = li, e = li + 1;
-    while (s > lo_lim && li - s < FIX_MAX_RUN && sk[s - 1] == k) --s;
-    while (e < hi_lim && e - li <= FIX_MAX_RUN && sk[e] == k) ++e;
-    const uint64_t c = sc[li];
+    while (s > lo_lim && li - s < FIX_MAX_RUN && (sc[s - 1] >> SHIFT) == k) --s;
+    while (e < hi_lim && e - li <= FIX_MAX_RUN && (sc[e] >> SHIFT) == k) ++e;
     const uint32_t i = si[li];
     int64_t dst = p;
     if (e - s > 1) {
@@ -1149,53 +1146,78 @@ __global__ void __launch_bounds__(256) k_fix_runs_win(const uint32_t *__restrict
   }
 }
 
-
 #ifndef SPB_SORT_TOP32
 #define SPB_SORT_TOP32 1
 #endif
 
 // Clustered inputs make long runs of equal top bits (halo cores: hundreds of
-// points per top-32 cell on H(2^27)), for which the top-32 sort would end in
-// the fallback after all its work.  A sample of every 128th point predicts
-// them: a run of 3/4 FIX_MAX_RUN points leaves about 3 copies of its key in
-// the sample, so three equal keys among the sorted sample keys choose the
-// 63-bit sort (on uniform points at 2^27 three equal sampled keys have
-// probability ~1%; a miss only costs the fallback).
-__global__ void __launch_bounds__(256) k_sample_top32(const float *__restrict__ pts, int64_t n, int64_t stride,
-                                                      int64_t ns, int width, const float *__restrict__ scene,
-                                                      uint32_t *__restrict__ key32) {
-  const int bits = width / 3;
-  const uint32_t top = bits >= 32 ? 0xffffffffu : ((1u << bits) - 1u);
+// points per top-32 cell on H(2^27)), for which a top-bits sort would end in
+// the fallback after all its work.  A sample of n / 128 scattered points
+// predicts them: a run of 3/4 FIX_MAX_RUN points leaves about 3 copies of its
+// key in the sample.  The sample is sorted by its top 40 code bits once; no three
+// equal top-32 keys choose the 32-bit sort (4 passes), else no three equal
+// top-40 keys the 40-bit sort (5 passes), else the full 63-bit sort (on
+// uniform points at 2^27 three equal sampled top-32 keys have probability
+// ~1%; a miss only costs the fallback).
+__global__ void __launch_bounds__(256) k_sample_top40(const float *__restrict__ pts, int64_t stride, int64_t ns,
+                                                      const float *__restrict__ scene, uint64_t *__restrict__ key) {
+  const int bits = 21;
+  const uint32_t top = (1u << bits) - 1u;
   const double scale = (double)(1ull << bits);
-  const int shift = 3 * bits - 32;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ns) return;
-  const float *q = pts + 3 * (i * stride);
-  key32[i] = (uint32_t)(encode_bins(axis_bin(q[0], scene[0], scene[3], scale, top),
-                                    axis_bin(q[1], scene[1], scene[4], scale, top),
-                                    axis_bin(q[2], scene[2], scene[5], scale, top), 3) >> shift);
+  // scattered sample positions (a multiplicative hash): a fixed stride can
+  // alias with the input's own structure (H(n) deals its halo points round
+  // robin, and every 128th point falls into 96 of the 12288 halos at 2^27)
+  const int64_t at = (int64_t)(((unsigned __int128)((uint64_t)i * 0x9E3779B97F4A7C15ull)) % (uint64_t)(ns * stride));
+  const float *q = pts + 3 * at;
+  key[i] = encode_bins(axis_bin(q[0], scene[0], scene[3], scale, top), axis_bin(q[1], scene[1], scene[4], scale, top),
+                       axis_bin(q[2], scene[2], scene[5], scale, top), 3) >> 23;
 }
-__global__ void __launch_bounds__(256) k_sample_triples(const uint32_t *__restrict__ key32, int64_t ns,
-                                                        int *found) {
+__global__ void __launch_bounds__(256) k_sample_triples(const uint64_t *__restrict__ key, int64_t ns, int *found) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i + 2 < ns && key32[i] == key32[i + 2]) *found = 1;
+  if (i + 2 >= ns) return;
+  if ((key[i] >> 8) == (key[i + 2] >> 8)) found[0] = 1;  // three equal top-32 keys
+  if (key[i] == key[i + 2]) found[1] = 1;                // three equal top-40 keys
 }
-bool top32_runs_short(Ctx &c, const float *pts, int64_t n, const float *scene) {
-  if (n < (1 << 18)) return true;  // small: a fallback costs little
+int choose_top_bits(Ctx &c, const float *pts, int64_t n, const float *scene) {
+  if (n < (1 << 18)) return 32;  // small: a fallback costs little
   const int64_t stride = 128, ns = n / stride;
-  DevBuf<uint32_t> k0((size_t)ns, c.stream), k1((size_t)ns, c.stream), v0((size_t)ns, c.stream),
-      v1((size_t)ns, c.stream);
-  DevBuf<int> found(1, c.stream);
-  SPB_CUDA(cudaMemsetAsync(found.get(), 0, sizeof(int), c.stream));
-  k_sample_top32<<<(unsigned)((ns + 255) / 256), 256, 0, c.stream>>>(pts, n, stride, ns, 64, scene, k0.get());
+  DevBuf<uint64_t> k0((size_t)ns, c.stream), k1((size_t)ns, c.stream);
+  DevBuf<uint32_t> v0((size_t)ns, c.stream), v1((size_t)ns, c.stream);
+  DevBuf<int> found(2, c.stream);
+  SPB_CUDA(cudaMemsetAsync(found.get(), 0, 2 * sizeof(int), c.stream));
+  k_sample_top40<<<(unsigned)((ns + 255) / 256), 256, 0, c.stream>>>(pts, stride, ns, scene, k0.get());
   SPB_LAUNCHED();
-  uint32_t *ka = k0.get(), *kb = k1.get(), *va = v0.get(), *vb = v1.get();
-  radix_sort_pairs(c, &ka, &va, &kb, &vb, ns, 32, true);
+  uint64_t *ka = k0.get(), *kb = k1.get();
+  uint32_t *va = v0.get(), *vb = v1.get();
+  radix_sort_pairs(c, &ka, &va, &kb, &vb, ns, 40, true);
   k_sample_triples<<<(unsigned)((ns + 255) / 256), 256, 0, c.stream>>>(ka, ns, found.get());
   SPB_LAUNCHED();
-  int h = 0;
-  peek(c, {{found.get(), &h, sizeof(int)}});
-  return h == 0;
+  int h[2] = {0, 0};
+  peek(c, {{found.get(), h, sizeof(h)}});
+  return !h[0] ? 32 : (!h[1] ? 40 : 0);
+}
+__global__ void __launch_bounds__(256) k_morton_top40(const float *__restrict__ pts, int64_t n,
+                                                      const float *__restrict__ scene, uint64_t *__restrict__ key) {
+  const int bits = 21;
+  const uint32_t top = (1u << bits) - 1u;
+  const double scale = (double)(1ull << bits);
+  const float lo0 = scene[0], lo1 = scene[1], lo2 = scene[2], hi0 = scene[3], hi1 = scene[4], hi2 = scene[5];
+  auto code = [&](float x, float y, float z) -> uint64_t {
+    return encode_bins(axis_bin(x, lo0, hi0, scale, top), axis_bin(y, lo1, hi1, scale, top),
+                       axis_bin(z, lo2, hi2, scale, top), 3) >> 23;
+  };
+  const int64_t chunks = n / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t ch = t0; ch < chunks; ch += stride) {
+    float x[4], y[4], z[4];
+    load4pts(pts, ch, x, y, z);
+    reinterpret_cast<ulonglong2 *>(key)[2 * ch] = make_ulonglong2(code(x[0], y[0], z[0]), code(x[1], y[1], z[1]));
+    reinterpret_cast<ulonglong2 *>(key)[2 * ch + 1] = make_ulonglong2(code(x[2], y[2], z[2]), code(x[3], y[3], z[3]));
+  }
+  for (int64_t i = chunks * 4 + t0; i < n; i += stride) key[i] = code(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
 }
 
 void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, int width, Tree &t) {
@@ -1230,13 +1252,24 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
   uint64_t *ka = k0.get(), *kb = k1.get();
   uint32_t *va = v0.get(), *vb = v1.get();
   const float4 *spts = nullptr;  // points in sorted order (the top-32 path writes them)
-  if (SPB_SORT_TOP32 && points && dim == 3 && width == 64 && n >= 2 && !c.async() && aligned16(objects) &&
-      top32_runs_short(c, objects, n, t.scene)) {
-    uint32_t *k32a = reinterpret_cast<uint32_t *>(k0.get()), *k32b = k32a + n;
-    k_morton_top32<<<grid_for((n + 3) / 4, 256, 148 * 16), 256, 0, c.stream>>>(objects, n, width, t.scene, k32a);
-    SPB_LAUNCHED();
-    mark(c, "morton");
-    radix_sort_pairs(c, &k32a, &va, &k32b, &vb, n, 32, /*vals_iota=*/true);
+  const int topbits = (SPB_SORT_TOP32 && points && dim == 3 && width == 64 && n >= 2 && !c.async() &&
+                       aligned16(objects))
+                          ? choose_top_bits(c, objects, n, t.scene)
+                          : 0;
+  if (topbits) {
+    if (topbits == 32) {
+      uint32_t *k32a = reinterpret_cast<uint32_t *>(k0.get()), *k32b = k32a + n;
+      k_morton_top32<<<grid_for((n + 3) / 4, 256, 148 * 16), 256, 0, c.stream>>>(objects, n, width, t.scene, k32a);
+      SPB_LAUNCHED();
+      mark(c, "morton");
+      radix_sort_pairs(c, &k32a, &va, &k32b, &vb, n, 32, /*vals_iota=*/true);
+    } else {
+      k_morton_top40<<<grid_for((n + 3) / 4, 256, 148 * 16), 256, 0, c.stream>>>(objects, n, t.scene, k0.get());
+      SPB_LAUNCHED();
+      mark(c, "morton");
+      uint32_t *k32 = reinterpret_cast<uint32_t *>(k1.get());
+      radix_sort_pairs_40(c, k0.get(), &va, &vb, k32, k32 + n, n, /*vals_iota=*/true);
+    }
     // scratch in the node array (written by the hierarchy afterwards)
     float4 *tpt = reinterpret_cast<float4 *>(t.nodes);
     uint64_t *tcode = reinterpret_cast<uint64_t *>(tpt + n);
@@ -1245,11 +1278,16 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
     k_fix_gather<<<(unsigned)((n + 256 * FIX_ILP - 1) / (256 * FIX_ILP)), 256, 0, c.stream>>>(
         objects, n, width, t.scene, va, tcode, tpt);
     SPB_LAUNCHED();
-    k_fix_runs_win<<<(unsigned)((n + FIX_CH - 1) / FIX_CH), 256, 0, c.stream>>>(k32a, n, tcode, tpt, k1.get(), vb, t.leafpt,
-                                                                  ovf.get());
+    const unsigned gw = (unsigned)((n + FIX_CH - 1) / FIX_CH);
+    if (topbits == 32)
+      k_fix_runs_win<31><<<gw, 256, 0, c.stream>>>(n, tcode, tpt, k1.get(), vb, t.leafpt, ovf.get());
+    else
+      k_fix_runs_win<23><<<gw, 256, 0, c.stream>>>(n, tcode, tpt, k1.get(), vb, t.leafpt, ovf.get());
     SPB_LAUNCHED();
     int h_ovf = 0;
     peek(c, {{ovf.get(), &h_ovf, sizeof(int)}});
+    c.count("sort_top_bits", topbits);
+    c.count("sort_fallback", h_ovf);
     if (!h_ovf) {
       ka = k1.get();
       kb = k0.get();
@@ -1320,7 +1358,8 @@ void sort_points(Ctx &c, const float *pts, int64_t n, int dim, int32_t *order) {
   scene_bounds(c, pts, n, dim, true, scene.get(), bad.get());
   DevBuf<uint64_t> k0(n, c.stream), k1(n, c.stream);
   DevBuf<uint32_t> v0(n, c.stream), v1(n, c.stream);
-  if (SPB_SORT_TOP32 && dim == 3 && n >= 2 && !c.async() && aligned16(pts) && top32_runs_short(c, pts, n, scene.get())) {
+  if (SPB_SORT_TOP32 && dim == 3 && n >= 2 && !c.async() && aligned16(pts) &&
+      choose_top_bits(c, pts, n, scene.get()) == 32) {
     // top 32 bits in four passes, runs ordered by the full codes (k1)
     uint32_t *k32a = reinterpret_cast<uint32_t *>(k0.get()), *k32b = k32a + n;
     uint32_t *va = v0.get(), *vb = v1.get();

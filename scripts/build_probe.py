@@ -16,9 +16,11 @@ for n in (1 << 24, 1 << 27):
                   flush=True)
         del b
     del p
-# the clustered field (the bench's bvh_build input)
+# the clustered field H(2^27) (the bench's bvh_build input)
 n = 1 << 27
-p = sp.generate_field(n, seed=2409, ctx=ctx)
+h = torch.empty((n, 3), dtype=torch.float32, pin_memory=True)
+sp.generate_reference_field(n, 0, n, out=h)  # the bench's H(2^27) (reference generator)
+p = h.cuda()
 for it in range(3):
     b = sp.Bvh.build(p, ctx=ctx)
     ph = ctx.phases()

@@ -154,3 +154,28 @@ def test_unaligned_device_points_take_the_scalar_path(sp):
     fa = sp.friends_of_friends(view, eps)
     fb = sp.friends_of_friends(dense, eps)
     assert torch.equal(fa.labels, fb.labels) and torch.equal(fa.core_flags, fb.core_flags)
+
+
+@pytest.mark.parametrize("case", ["top40", "overflow", "top32_runs"])
+def test_top_bits_sort_paths_match_oracle(sp, oracle, case):
+    # Bvh::build sorts by the top 32 or 40 code bits and orders the runs of
+    # equal top bits afterwards; a sample routes clumps to the wider sort, and
+    # runs over 512 fall back to the full 63-bit sort.  Every path must give
+    # the reference's tree bit for bit.
+    rng = np.random.default_rng(4040)
+    if case == "top40":  # dense enough for long top-32 runs, sparse at 40 bits
+        pts = np.concatenate([rng.random((1 << 20, 3), dtype=np.float32),
+                              (0.3 + rng.random((1 << 16, 3)) * 0.006).astype(np.float32)])
+    elif case == "overflow":  # 1000 identical points below the sampling size: fix-up overflow
+        pts = np.concatenate([rng.random((5000, 3), dtype=np.float32), np.full((1000, 3), 0.25, np.float32)])
+    else:  # runs of tens of equal top-32 keys, handled in place
+        pts = np.concatenate([rng.random((20000, 3), dtype=np.float32),
+                              (0.6 + rng.random((3000, 3)) * 0.003).astype(np.float32)])
+    ctx = sp.Context(0)
+    tree = sp.Bvh.build(pts, ctx=ctx)
+    path = (ctx.counter("sort_top_bits"), ctx.counter("sort_fallback"))
+    got = tree.export()
+    assert path == {"top40": (40, 0), "overflow": (32, 1), "top32_runs": (32, 0)}[case], path
+    want = oracle.bvh(pts, 3)
+    for key in BVH_KEYS:
+        assert same_bits(got[key], want[key]), (case, key)
