@@ -2,7 +2,7 @@
 # (with its C3/C5 extras and CPU baseline), the reference arm, the other
 # SURVEY configs, the one-rank slab path, launch lists and ncu --set full
 # captures of the top kernels.  Outputs under gpurun_out/r02/.
-O=gpurun_out/r02b
+O=gpurun_out/r02c
 mkdir -p $O
 python paper_2409_10743_b200/build.py >/dev/null
 make -s -C oracle all
