@@ -723,13 +723,15 @@ __device__ __forceinline__ void exch128(unsigned long long *p, unsigned long lon
 // words (mode 1) or 128-bit exchanges (mode 2): the flag word carries
 // {bound, lo.xyz} of the first arrival, a second word its hi.xyz.
 __device__ __forceinline__ int32_t local_handoff(const LocalClimb &lc, int64_t a, bool L, int32_t bound,
-                                                 const float lo[3], const float hi[3], float4 &slo, float4 &shi) {
+                                                 const float lo[3], const float hi[3], float4 &slo, float4 &shi,
+                                                 uint32_t pass = 0, uint32_t *theirs = nullptr) {
   const int64_t k = a - lc.B;
   if (SPB_CLIMB_SMEM_MODE == 2) {
-    // box: [2][CLIMB_BLK][2] words of 64 bit per side: hi.xyz of that side;
-    // flag words: [CLIMB_BLK][2] {bound | lo.x, lo.y | lo.z}
+    // box: [2][CLIMB_BLK][2] words of 64 bit per side: hi.xyz of that side
+    // and 32 free bits (`pass`: split lengths for the sibling); flag words:
+    // [CLIMB_BLK][2] {bound | lo.x, lo.y | lo.z}
     unsigned long long *hslot = lc.box + ((L ? 0 : CLIMB_BLK) + k) * 2;
-    unsigned long long h0 = pack2(hi[0], hi[1]), h1 = pack2(hi[2], 0.f);
+    unsigned long long h0 = pack2(hi[0], hi[1]), h1 = pack2(hi[2], __uint_as_float(pass));
     exch128(hslot, h0, h1, false);
     unsigned long long w0 = (unsigned long long)(uint32_t)bound | ((unsigned long long)__float_as_uint(lo[0]) << 32);
     unsigned long long w1 = pack2(lo[1], lo[2]);
@@ -740,6 +742,7 @@ __device__ __forceinline__ int32_t local_handoff(const LocalClimb &lc, int64_t a
     exch128(lc.box + ((L ? CLIMB_BLK : 0) + k) * 2, g0, g1, false);
     slo = make_float4(hi32f(w0), lo32f(w1), hi32f(w1), 0.f);
     shi = make_float4(lo32f(g0), hi32f(g0), lo32f(g1), 0.f);
+    if (theirs) *theirs = (uint32_t)(g1 >> 32);
     return other;
   }
   unsigned long long *mine = lc.box + ((L ? 0 : CLIMB_BLK) + k) * 3;
@@ -774,8 +777,12 @@ template <bool LOCAL>
 __device__ __forceinline__ bool climb(const HierView &H, int64_t &l, int64_t &r, float lo[3], float hi[3],
                                       float4 *nodes, int32_t *flags, int max_levels, const LocalClimb &lc) {
   const int64_t n = H.n;
+  // the split lengths around the node [l, r], carried from level to level: a
+  // block-local hand-off passes the sibling's far-side lengths along with its
+  // box, so the local levels read no split lengths from memory
+  int32_t dl1 = H.D(l - 1), dr = H.D(r), dr1 = H.D(r + 1);
   for (int level = 0; level < max_levels;) {
-    const bool L = H.is_left(l, r);
+    const bool L = l == 0 || (r != n - 1 && dr > dl1);  // HierView::is_left
     const int64_t a = L ? r : l - 1;  // the parent's split position
     const int32_t bound = (int32_t)(L ? l : r);
     // Acquire-release exchanges: the release half orders this node's box
@@ -786,15 +793,31 @@ __device__ __forceinline__ bool climb(const HierView &H, int64_t &l, int64_t &r,
     const bool local = LOCAL && lc.inside(a);
     float4 slo, shi;
     if (local) {
-      const int32_t other = local_handoff(lc, a, L, bound, lo, hi, slo, shi);
+      // the parent keeps this child's far side: a left child hands over
+      // D(l-1), a right child D(r) and D(r+1) (16 bits each; -1 sentinel)
+      const uint32_t mine = L ? (uint32_t)(uint16_t)dl1 : ((uint32_t)(uint16_t)dr | ((uint32_t)(uint16_t)dr1 << 16));
+      uint32_t theirs = 0;
+      const int32_t other = local_handoff(lc, a, L, bound, lo, hi, slo, shi, mine, &theirs);
       if (other < 0) return false;  // first arrival: the sibling is inside and will come
-      if (L) r = other;
-      else l = other;
+      if (L) {
+        r = other;
+        dr = (int16_t)(theirs & 0xffffu);
+        dr1 = (int16_t)(theirs >> 16);
+      } else {
+        l = other;
+        dl1 = (int16_t)(theirs & 0xffffu);
+      }
     } else {
       const int32_t other = exch_acq_rel_gpu(flags + a, bound);
       if (other < 0) return false;  // first arrival
-      if (L) r = other;
-      else l = other;
+      if (L) {
+        r = other;
+        dr = H.D(r);
+        dr1 = H.D(r + 1);
+      } else {
+        l = other;
+        dl1 = H.D(l - 1);
+      }
       const int64_t sib = L ? ((a + 1 == r) ? n - 1 + r : a + 1) : ((a == l) ? n - 1 + l : a);
       slo = __ldcg(nodes + 2 * sib);
       shi = __ldcg(nodes + 2 * sib + 1);
@@ -809,9 +832,11 @@ __device__ __forceinline__ bool climb(const HierView &H, int64_t &l, int64_t &r,
       hi[0] = keep_max(shi.x, hi[0]); hi[1] = keep_max(shi.y, hi[1]); hi[2] = keep_max(shi.z, hi[2]);
     }
     const bool root = (l == 0 && r == n - 1);
-    const int64_t k = root ? 0 : (H.is_left(l, r) ? r : l);
+    const int64_t k = root ? 0 : ((l == 0 || (r != n - 1 && dr > dl1)) ? r : l);
+    const int32_t rope = r == n - 1 ? kSentinel
+                                    : ((r + 1 == n - 1 || dr1 < dr) ? (int32_t)(n - 1 + r + 1) : (int32_t)(r + 1));
     nodes[2 * k] = make_float4(lo[0], lo[1], lo[2], __int_as_float((int)left));
-    nodes[2 * k + 1] = make_float4(hi[0], hi[1], hi[2], __int_as_float(H.rope(r)));
+    nodes[2 * k + 1] = make_float4(hi[0], hi[1], hi[2], __int_as_float(rope));
     if (root) return false;
   }
   return true;
