@@ -912,6 +912,11 @@ __global__ void __launch_bounds__(CLIMB_BLK) k_hierarchy(int64_t n, const int32_
     lo[0] = hi[0] = q.x;
     lo[1] = hi[1] = q.y;
     lo[2] = hi[2] = q.z;
+  } else if (!POINTS && !obj) {  // leaf nodes written by the caller (k_cell_ranges): read the box back
+    oi = (uint32_t)p;
+    const float4 a = nodes[2 * (n - 1 + p)], b = nodes[2 * (n - 1 + p) + 1];
+    lo[0] = a.x; lo[1] = a.y; lo[2] = a.z;
+    hi[0] = b.x; hi[1] = b.y; hi[2] = b.z;
   } else {
     oi = perm ? perm[p] : (uint32_t)p;
     const int sz = POINTS ? dim : 2 * dim;
@@ -923,9 +928,11 @@ __global__ void __launch_bounds__(CLIMB_BLK) k_hierarchy(int64_t n, const int32_
   }
   if (perm_out) perm_out[p] = (int32_t)oi;
   const int64_t leaf = n - 1 + p;
-  nodes[2 * leaf] = make_float4(lo[0], lo[1], lo[2], __int_as_float((int)oi));
   const int32_t leaf_rope = H.rope(p);
-  nodes[2 * leaf + 1] = make_float4(hi[0], hi[1], hi[2], __int_as_float(leaf_rope));
+  if (POINTS || obj) {
+    nodes[2 * leaf] = make_float4(lo[0], lo[1], lo[2], __int_as_float((int)oi));
+    nodes[2 * leaf + 1] = make_float4(hi[0], hi[1], hi[2], __int_as_float(leaf_rope));
+  }
   if (POINTS) leafpt[p] = make_float4(lo[0], lo[1], lo[2], __int_as_float(leaf_rope));
   if (n == 1) return;
   int64_t l = p, r = p;
@@ -1356,7 +1363,8 @@ void build_sorted_hierarchy(Ctx &c, const uint64_t *keys, int64_t m, int dim, co
   t.points = false;
   t.stream = c.stream;
   if (m == 0) return;
-  t.nodes = static_cast<decltype(t.nodes)>(cache_alloc((size_t)(2 * m - 1) * 2 * sizeof(float4), c.stream));
+  // boxes == nullptr: the caller allocated t.nodes and wrote the leaf nodes
+  if (boxes) t.nodes = static_cast<decltype(t.nodes)>(cache_alloc((size_t)(2 * m - 1) * 2 * sizeof(float4), c.stream));
   // leaves are the objects in order: no permutation array (t.perm stays null)
   DevBuf<int32_t> own_delta, flags(m > 1 ? m - 1 : 1, c.stream);
   DevBuf<int32_t> &delta = delta_in ? *delta_in : own_delta;

@@ -775,10 +775,14 @@ __global__ void k_dense_core(const int32_t *__restrict__ point_cell, int64_t n, 
 // ckeys == nullptr: write the hierarchy's split array instead (delta[j] =
 // the common-prefix length of cell keys j and j + 1, k_delta's value for
 // distinct 64-bit keys), so the cell keys need not be stored and re-read.
+// leaves != nullptr: write the cell tree's leaf nodes {box, cell, rope}
+// directly (no box array for the hierarchy to re-read); rope(j) from the split
+// lengths D(j), D(j+1) as HierView::rope.
 __global__ void k_cell_ranges(const int64_t *__restrict__ cell_start, int64_t m, int64_t n,
                               const uint64_t *__restrict__ skeys, const float4 *__restrict__ cpts, int dim,
                               uint64_t *__restrict__ ckeys, float *__restrict__ boxes, int32_t *__restrict__ cell_of,
-                              uint8_t *__restrict__ multi, int32_t *__restrict__ delta) {
+                              uint8_t *__restrict__ multi, int32_t *__restrict__ delta,
+                              float4 *__restrict__ leaves = nullptr) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride) {
     const int64_t s = cell_start[j], e = j + 1 < m ? cell_start[j + 1] : n;
@@ -790,12 +794,23 @@ __global__ void k_cell_ranges(const int64_t *__restrict__ cell_start, int64_t m,
       hi[0] = fmaxf(hi[0], q.x); hi[1] = fmaxf(hi[1], q.y); hi[2] = fmaxf(hi[2], q.z);
       if (cell_of) cell_of[k] = (int32_t)j;
     }
-    for (int k = 0; k < dim; ++k) {
-      boxes[j * 2 * dim + k] = lo[k];
-      boxes[j * 2 * dim + dim + k] = hi[k];
+    if (boxes) {
+      for (int k = 0; k < dim; ++k) {
+        boxes[j * 2 * dim + k] = lo[k];
+        boxes[j * 2 * dim + dim + k] = hi[k];
+      }
     }
     if (ckeys) ckeys[j] = skeys[s];
-    if (delta && j + 1 < m) delta[j] = __clzll((long long)(skeys[s] ^ skeys[e]));
+    const int32_t dj = j + 1 < m ? __clzll((long long)(skeys[s] ^ skeys[e])) : -1;
+    if (delta && j + 1 < m) delta[j] = dj;
+    if (leaves) {
+      const int32_t dj1 = j + 2 < m ? __clzll((long long)(skeys[e] ^ skeys[cell_start[j + 2]])) : -1;
+      const int32_t rope = j == m - 1 ? kSentinel
+                                      : ((j + 1 == m - 1 || dj1 < dj) ? (int32_t)(m - 1 + j + 1) : (int32_t)(j + 1));
+      if (dim < 3) lo[2] = hi[2] = 0.f;
+      leaves[2 * j] = make_float4(lo[0], lo[1], lo[2], __int_as_float((int)j));
+      leaves[2 * j + 1] = make_float4(hi[0], hi[1], hi[2], __int_as_float(rope));
+    }
     multi[j] = (e - s) > 1;
   }
 }
@@ -1300,13 +1315,17 @@ bool build_cell_grid(Ctx &c, const float *pts, int64_t n, int dim, float eps, Ce
   }
   g.m = m;
   DevBuf<int32_t> delta(m > 1 ? m - 1 : 1, c.stream);
-  DevBuf<float> boxes((size_t)m * 2 * dim, c.stream);
   g.multi = DevBuf<uint8_t>((size_t)m, c.stream);
-  k_cell_ranges<<<grid_for(m, 256, 148 * 16), 256, 0, c.stream>>>(g.cell_start.get(), m, n, ka, g.cpts.get(), dim,
-                                                                   nullptr, boxes.get(), nullptr, g.multi.get(),
-                                                                   delta.get());
-  SPB_LAUNCHED();
-  build_sorted_hierarchy(c, nullptr, m, dim, boxes.get(), g.t, &delta);
+  // the cell tree's leaf nodes straight from the cell ranges
+  g.t.nodes = m > 0 ? static_cast<float4 *>(cache_alloc((size_t)(2 * m - 1) * 2 * sizeof(float4), c.stream))
+                    : nullptr;
+  if (m > 0) {
+    k_cell_ranges<<<grid_for(m, 256, 148 * 16), 256, 0, c.stream>>>(g.cell_start.get(), m, n, ka, g.cpts.get(), dim,
+                                                                     nullptr, nullptr, nullptr, g.multi.get(),
+                                                                     delta.get(), g.t.nodes + 2 * (m - 1));
+    SPB_LAUNCHED();
+  }
+  build_sorted_hierarchy(c, nullptr, m, dim, nullptr, g.t, &delta);
   mark(c, "hierarchy");
   return true;
 }
