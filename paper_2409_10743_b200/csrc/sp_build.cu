@@ -505,6 +505,9 @@ __global__ void __launch_bounds__(THREADS, (THREADS * ITEMS <= 2048) ? 4
 #ifndef SPB_RS_THREADS
 #define SPB_RS_THREADS 256
 #endif
+#ifndef SPB_RS_ITEMS32
+#define SPB_RS_ITEMS32 16  // keys per thread of the 32-bit-key passes
+#endif
 #ifndef SPB_RS_ITEMS
 #define SPB_RS_ITEMS 16
 #endif
@@ -566,9 +569,10 @@ void radix_sort_pairs_40(Ctx &c, const uint64_t *keys, uint32_t **vals, uint32_t
     if (n == 1 && vals_iota) SPB_CUDA(cudaMemsetAsync(*vals, 0, sizeof(uint32_t), c.stream));
     return;
   }
-  constexpr int ITEMS = SPB_RS_ITEMS, THREADS = SPB_RS_THREADS, TILE = ITEMS * THREADS;
+  constexpr int ITEMS = SPB_RS_ITEMS, ITEMS32 = SPB_RS_ITEMS32, THREADS = SPB_RS_THREADS, TILE = ITEMS * THREADS,
+                TILE32 = ITEMS32 * THREADS;
   constexpr size_t SMEM64 = rs_smem_bytes<ITEMS, THREADS, uint64_t>();
-  constexpr size_t SMEM32 = rs_smem_bytes<ITEMS, THREADS, uint32_t>();
+  constexpr size_t SMEM32 = rs_smem_bytes<ITEMS32, THREADS, uint32_t>();
   {
     static std::mutex mu;
     static uint64_t opted = 0;
@@ -576,15 +580,15 @@ void radix_sort_pairs_40(Ctx &c, const uint64_t *keys, uint32_t **vals, uint32_t
     if (c.device >= 64 || !((opted >> c.device) & 1)) {
       SPB_CUDA(cudaFuncSetAttribute(k_rs_onesweep<ITEMS, THREADS, uint64_t, uint32_t>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM64));
-      SPB_CUDA(cudaFuncSetAttribute(k_rs_onesweep<ITEMS, THREADS, uint32_t>,
+      SPB_CUDA(cudaFuncSetAttribute(k_rs_onesweep<ITEMS32, THREADS, uint32_t>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM32));
       if (c.device < 64) opted |= 1ull << c.device;
     }
   }
   constexpr int npass = 5;
-  const int64_t ntiles = (n + TILE - 1) / TILE;
+  const int64_t ntiles = (n + TILE - 1) / TILE, ntiles32 = (n + TILE32 - 1) / TILE32;
   DevBuf<uint32_t> hist((size_t)npass * RS_BINS + npass, c.stream);
-  DevBuf<unsigned long long> lookback((size_t)ntiles * RS_BINS, c.stream);
+  DevBuf<unsigned long long> lookback((size_t)std::max(ntiles, ntiles32) * RS_BINS, c.stream);
   SPB_CUDA(cudaMemsetAsync(hist.get(), 0, hist.n * sizeof(uint32_t), c.stream));
   SPB_CUDA(cudaMemsetAsync(lookback.get(), 0, lookback.n * sizeof(unsigned long long), c.stream));
   k_rs_hist<uint64_t><<<grid_for(n, 256, 148 * 4), 256, 0, c.stream>>>(keys, n, npass, hist.get());
@@ -598,7 +602,7 @@ void radix_sort_pairs_40(Ctx &c, const uint64_t *keys, uint32_t **vals, uint32_t
   std::swap(*vals, *vals_alt);
   uint32_t *ka = k32, *kb = k32_alt;
   for (int p = 1; p < npass; ++p) {
-    k_rs_onesweep<ITEMS, THREADS, uint32_t><<<(unsigned)ntiles, THREADS, SMEM32, c.stream>>>(
+    k_rs_onesweep<ITEMS32, THREADS, uint32_t><<<(unsigned)ntiles32, THREADS, SMEM32, c.stream>>>(
         ka, *vals, kb, *vals_alt, n, 8 * (p - 1), hist.get() + (size_t)p * RS_BINS, lookback.get(), ctr + p,
         (uint32_t)(2 * p + 1));
     SPB_LAUNCHED();
@@ -614,7 +618,7 @@ void radix_sort_pairs(Ctx &c, uint32_t **keys, uint32_t **vals, uint32_t **keys_
     return;
   }
   const int npass = std::max(1, std::min(4, (key_bits + 7) / 8));
-  onesweep_passes<SPB_RS_ITEMS, SPB_RS_THREADS, uint32_t>(c, keys, vals, keys_alt, vals_alt, n, npass, vals_iota);
+  onesweep_passes<SPB_RS_ITEMS32, SPB_RS_THREADS, uint32_t>(c, keys, vals, keys_alt, vals_alt, n, npass, vals_iota);
 }
 
 // ---------------------------------------------------------------------------

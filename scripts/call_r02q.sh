@@ -1,5 +1,3 @@
-# A/B: cell-tree leaf nodes written by k_cell_ranges (dnew) vs box array + hierarchy leaf writes (dold)
+# A/B: keys per thread of the 32-bit-key onesweep passes
 mkdir -p gpurun_out
-for v in dold dnew dold dnew; do cp var/$v.so paper_2409_10743_b200/libspb200.so; echo "== $v"; timeout 120 python scripts/ab_labels.py 134217728 3 2>&1 | tail -1 | cut -c 1-300; done
-cp var/dnew.so paper_2409_10743_b200/libspb200.so
-timeout 1500 python -m pytest tests/test_gpu_scale.py tests/test_gpu_dbscan.py tests/test_gpu_densebox.py tests/test_gpu_slabs.py tests/test_gpu_sequential.py -q -x 2>&1 | tail -2
+for v in i16 i20 i24; do cp var/$v.so paper_2409_10743_b200/libspb200.so; echo "== $v"; timeout 300 python scripts/build_probe.py 2>&1 | tail -2 | cut -c1-200; timeout 120 python scripts/ab_labels.py 134217728 3 2>&1 | tail -1 | cut -c 60-300; done
