@@ -557,6 +557,127 @@ __global__ void __launch_bounds__(128) k_knn(const float4 *__restrict__ nodes, i
   }
 }
 
+// k <= 16 with lower-bound keys.  The result set depends only on the exact
+// leaf distances (float(sqrt(S)) with S the double-accumulated square, as
+// box_dist computes them); the visiting order is free and a node may be
+// pruned whenever its distance is certainly above the current k-th.  Every
+// node -- internal or leaf -- is keyed by a fp32 LOWER bound: gaps, squares,
+// sum and square root all rounded toward zero (__f*_rd), so key <= the real
+// distance <= the exact float distance (a float within 2^-52 of the real value
+// rounds to itself), and `key > worst` prunes only what the exact test would.
+// The double-precision distance is computed once per leaf that survives the
+// bound, at its visit, from its node (in L1: the parent's expansion loaded
+// it); expansions are all fp32 and branch-free.  Leaves travel on the stack
+// as ~(leaf node index).
+__device__ __forceinline__ float gap_rd(float c, float lo, float hi) {
+  return fmaxf(fmaxf(__fsub_rd(lo, c), __fsub_rd(c, hi)), 0.f);
+}
+__device__ __forceinline__ float box_dist_lb(float x, float y, float z, const float4 &lo, const float4 &hi) {
+  const float gx = gap_rd(x, lo.x, hi.x), gy = gap_rd(y, lo.y, hi.y), gz = gap_rd(z, lo.z, hi.z);
+  return __fsqrt_rd(__fadd_rd(__fadd_rd(__fmul_rd(gx, gx), __fmul_rd(gy, gy)), __fmul_rd(gz, gz)));
+}
+
+__global__ void __launch_bounds__(128) k_knn16lb(const float4 *__restrict__ nodes, int64_t n,
+                                                 const float *__restrict__ origins, int dim,
+                                                 const int32_t *__restrict__ order, int64_t nq, int32_t k,
+                                                 int32_t *__restrict__ out_idx, float *__restrict__ out_dist) {
+  constexpr int K = 16;
+  const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (qi >= nq) return;
+  const int64_t q = order[qi];
+  const float x = origins[q * dim], y = origins[q * dim + 1], z = dim == 3 ? origins[q * dim + 2] : 0.f;
+  const int32_t kk = (int32_t)((int64_t)k < n ? (int64_t)k : n);
+  float hd[K];
+  int32_t hx[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const bool real = j >= K - kk;
+    hd[j] = __int_as_float(real ? 0x7f800000 : (int)0xff800000);
+    hx[j] = real ? 0x7fffffff : (int32_t)0x80000000;
+  }
+  int32_t size = 0;
+  uint2 stk[KNN_STACK];
+  int top = 0;
+  const int32_t first_leaf = (int32_t)(n - 1);
+  float d = 0.f;  // the root: always opened (or the single leaf)
+  int32_t ref = n == 1 ? ~0 : node_link(ld_node(nodes, 0));  // the root's left child
+  bool have = true;
+  for (;;) {
+    if (!have) {
+      if (top == 0) break;
+      --top;
+      const uint2 e = stk[top];
+      d = __uint_as_float(e.x);
+      ref = (int32_t)e.y;
+    }
+    have = false;
+    if (size == kk && d > hd[K - 1]) continue;
+    if (ref < 0) {  // a leaf: its exact distance decides
+      const int32_t leaf = ~ref;
+      const float4 lo = ld_node(nodes, 2 * ((int64_t)first_leaf + leaf));
+      const float dx = __double2float_rn(__dsqrt_rn(dist2(x, y, z, lo.x, lo.y, lo.z)));
+      const int32_t obj = node_link(lo);
+      if (cand_less(dx, obj, hd[K - 1], hx[K - 1])) {
+        bool lt[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) lt[j] = cand_less(dx, obj, hd[j], hx[j]);
+#pragma unroll
+        for (int j = K - 1; j > 0; --j) {
+          hd[j] = lt[j - 1] ? hd[j - 1] : (lt[j] ? dx : hd[j]);
+          hx[j] = lt[j - 1] ? hx[j - 1] : (lt[j] ? obj : hx[j]);
+        }
+        hd[0] = lt[0] ? dx : hd[0];
+        hx[0] = lt[0] ? obj : hx[0];
+        if (size < kk) ++size;
+      }
+      continue;
+    }
+    // an internal node: ref is its left child
+    const int32_t left = ref;
+    const float4 llo = ld_node(nodes, 2 * (int64_t)left), lhi = ld_node(nodes, 2 * (int64_t)left + 1);
+    const int32_t right = node_rope(lhi);
+    const float4 rlo = ld_node(nodes, 2 * (int64_t)right), rhi = ld_node(nodes, 2 * (int64_t)right + 1);
+    float dn = box_dist_lb(x, y, z, llo, lhi), df = box_dist_lb(x, y, z, rlo, rhi);
+    int32_t rn = left >= first_leaf ? ~(left - first_leaf) : node_link(llo);
+    int32_t rf = right >= first_leaf ? ~(right - first_leaf) : node_link(rlo);
+    if (df < dn) {
+      const float td = dn; dn = df; df = td;
+      const int32_t tr = rn; rn = rf; rf = tr;
+    }
+    const bool full = size == kk;
+    const float w = hd[K - 1];
+    const bool keep_f = !(full && df > w), keep_n = !(full && dn > w);
+    if (keep_n) {
+      if (keep_f && top < KNN_STACK) { stk[top] = make_uint2(__float_as_uint(df), (uint32_t)rf); ++top; }
+      d = dn;
+      ref = rn;
+      have = true;
+    } else if (keep_f) {
+      d = df;
+      ref = rf;
+      have = true;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const int32_t r = j - (K - kk);
+    if (r >= 0 && r < size) {
+      const int64_t o = q * (int64_t)k + r;
+      out_idx[o] = hx[j];
+      if (out_dist) out_dist[o] = hd[j];
+    }
+  }
+  for (int32_t j = size; j < k; ++j) {
+    const int64_t o = q * (int64_t)k + j;
+    out_idx[o] = -1;
+    if (out_dist) out_dist[o] = __int_as_float(0x7f800000);
+  }
+}
+
+#ifndef SPB_KNN_LB
+#define SPB_KNN_LB 1
+#endif
+
 void knn(Ctx &c, const Tree &t, const float *origins, int64_t nq, int32_t k, int32_t *idx, float *dist) {
   if (nq <= 0 || k <= 0) return;
   if (t.n == 0) {
@@ -567,7 +688,9 @@ void knn(Ctx &c, const Tree &t, const float *origins, int64_t nq, int32_t k, int
   sort_points(c, origins, nq, t.dim, order.get());
   unsigned g = (unsigned)((nq + 127) / 128);
   const int64_t kk = std::min<int64_t>(k, t.n);
-  if (kk <= 16) {
+  if (kk <= 16 && SPB_KNN_LB) {
+    k_knn16lb<<<g, 128, 0, c.stream>>>(t.nodes, t.n, origins, t.dim, order.get(), nq, k, idx, dist);
+  } else if (kk <= 16) {
     k_knn<16><<<g, 128, 0, c.stream>>>(t.nodes, t.n, origins, t.dim, order.get(), nq, k, nullptr, nullptr, idx, dist);
   } else if (kk <= 64) {
     k_knn<64><<<g, 128, 0, c.stream>>>(t.nodes, t.n, origins, t.dim, order.get(), nq, k, nullptr, nullptr, idx, dist);

@@ -1,3 +1,5 @@
-# A/B: keys per thread of the 32-bit-key onesweep passes
+# A/B: kNN with fp32 lower-bound keys and exact leaf distances at the visit (lb) vs exact keys (nolb)
 mkdir -p gpurun_out
-for v in i16 i20 i24; do cp var/$v.so paper_2409_10743_b200/libspb200.so; echo "== $v"; timeout 300 python scripts/build_probe.py 2>&1 | tail -2 | cut -c1-200; timeout 120 python scripts/ab_labels.py 134217728 3 2>&1 | tail -1 | cut -c 60-300; done
+cp var/lb.so paper_2409_10743_b200/libspb200.so
+timeout 1500 python -m pytest tests -q -x -m gpu -k "knn or nearest or c4 or query" 2>&1 | tail -2
+for v in nolb lb nolb lb; do cp var/$v.so paper_2409_10743_b200/libspb200.so; echo "== $v"; timeout 300 python scripts/c4_probe.py 16777216 4 | tail -1; done
