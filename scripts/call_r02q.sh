@@ -1,3 +1,3 @@
+# A/B: merge walk loads a leaf's parent with its node (pb1) vs after the test (pb0)
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,serial,clocks.sm,clocks.max.sm,clocks.max.mem --format=csv
-for v in nolb lb nolb lb; do cp var/$v.so paper_2409_10743_b200/libspb200.so; echo "== $v"; timeout 300 python scripts/c4_probe.py 16777216 4 | tail -1; done
+for v in pb0 pb1 pb0 pb1; do cp var/$v.so paper_2409_10743_b200/libspb200.so; echo "== $v"; timeout 120 python scripts/ab_labels.py 134217728 3 2>&1 | tail -1 | cut -c 1-300; done
