@@ -569,12 +569,28 @@ __global__ void __launch_bounds__(128) k_knn(const float4 *__restrict__ nodes, i
 // bound, at its visit, from its node (in L1: the parent's expansion loaded
 // it); expansions are all fp32 and branch-free.  Leaves travel on the stack
 // as ~(leaf node index).
+#ifndef SPB_KNN_SQ
+#define SPB_KNN_SQ 1
+#endif
 __device__ __forceinline__ float gap_rd(float c, float lo, float hi) {
   return fmaxf(fmaxf(__fsub_rd(lo, c), __fsub_rd(c, hi)), 0.f);
 }
 __device__ __forceinline__ float box_dist_lb(float x, float y, float z, const float4 &lo, const float4 &hi) {
   const float gx = gap_rd(x, lo.x, hi.x), gy = gap_rd(y, lo.y, hi.y), gz = gap_rd(z, lo.z, hi.z);
-  return __fsqrt_rd(__fadd_rd(__fadd_rd(__fmul_rd(gx, gx), __fmul_rd(gy, gy)), __fmul_rd(gz, gz)));
+  const float s = __fadd_rd(__fadd_rd(__fmul_rd(gx, gx), __fmul_rd(gy, gy)), __fmul_rd(gz, gz));
+#if SPB_KNN_SQ
+  return s;  // keys are squared lower bounds, pruned against knn_sq_bound(worst)
+#else
+  return __fsqrt_rd(s);
+#endif
+}
+// SPB_KNN_SQ: a node keyed by its squared lower bound s may be pruned when s >
+// T = ru((w + ulp(w))^2): then the real distance exceeds w + ulp(w), which
+// rounds (to nearest, through the double square root) to a float above w, so
+// the exact test `distance > w` holds -- ties at w are never pruned.
+__device__ __forceinline__ float knn_sq_bound(float w) {
+  const float w1 = __fadd_ru(w, __fsub_ru(nextafterf(w, __int_as_float(0x7f800000)), w));
+  return __fmul_ru(w1, w1);
 }
 
 __global__ void __launch_bounds__(128) k_knn16lb(const float4 *__restrict__ nodes, int64_t n,
@@ -596,6 +612,7 @@ __global__ void __launch_bounds__(128) k_knn16lb(const float4 *__restrict__ node
     hx[j] = real ? 0x7fffffff : (int32_t)0x80000000;
   }
   int32_t size = 0;
+  float wkey = __int_as_float(0x7f800000);  // prune keys above this (the k-th distance, or its squared bound)
   uint2 stk[KNN_STACK];
   int top = 0;
   const int32_t first_leaf = (int32_t)(n - 1);
@@ -611,7 +628,7 @@ __global__ void __launch_bounds__(128) k_knn16lb(const float4 *__restrict__ node
       ref = (int32_t)e.y;
     }
     have = false;
-    if (size == kk && d > hd[K - 1]) continue;
+    if (size == kk && d > wkey) continue;
     if (ref < 0) {  // a leaf: its exact distance decides
       const int32_t leaf = ~ref;
       const float4 lo = ld_node(nodes, 2 * ((int64_t)first_leaf + leaf));
@@ -629,6 +646,11 @@ __global__ void __launch_bounds__(128) k_knn16lb(const float4 *__restrict__ node
         hd[0] = lt[0] ? dx : hd[0];
         hx[0] = lt[0] ? obj : hx[0];
         if (size < kk) ++size;
+#if SPB_KNN_SQ
+        if (size == kk) wkey = knn_sq_bound(hd[K - 1]);
+#else
+        if (size == kk) wkey = hd[K - 1];
+#endif
       }
       continue;
     }
@@ -645,8 +667,7 @@ __global__ void __launch_bounds__(128) k_knn16lb(const float4 *__restrict__ node
       const int32_t tr = rn; rn = rf; rf = tr;
     }
     const bool full = size == kk;
-    const float w = hd[K - 1];
-    const bool keep_f = !(full && df > w), keep_n = !(full && dn > w);
+    const bool keep_f = !(full && df > wkey), keep_n = !(full && dn > wkey);
     if (keep_n) {
       if (keep_f && top < KNN_STACK) { stk[top] = make_uint2(__float_as_uint(df), (uint32_t)rf); ++top; }
       d = dn;
