@@ -639,35 +639,31 @@ __global__ void __launch_bounds__(256) k_delta(const uint64_t *__restrict__ sk, 
 }
 
 constexpr int CLIMB_BLK = 256;
+// Split lengths in 32-bit index arithmetic (n < 2^31: Karras indices are
+// int32).  D(-1) = D(n-1) = -1 while every real split length is >= 0, which
+// folds the range-end tests into the lengths themselves: a node [l, r] is its
+// parent's left child iff D(r) > D(l-1) (l == 0 makes D(l-1) = -1; r == n-1
+// makes D(r) = -1), it is the root iff both are -1, and its rope is the
+// sentinel iff D(r) = -1, else leaf r+1 when D(r+1) < D(r) (bvh.hpp:176-222),
+// else internal node r+1.
 struct HierView {
-  int64_t n;
+  int32_t n;
   const int32_t *delta;
   // (reading D from the CTA's staged copy in shared memory instead measured
   // slower: hierarchy 8.8 -> 10.0 ms at 2^27)
-  __device__ __forceinline__ int D(int64_t i) const { return (i < 0 || i >= n - 1) ? -1 : __ldg(delta + i); }
-  // A node covering [l, r] is its parent's left child iff it shares a longer
-  // prefix with the key after it than with the key before it.
-  __device__ __forceinline__ bool is_left(int64_t l, int64_t r) const {
-    return l == 0 || (r != n - 1 && D(r) > D(l - 1));
-  }
-  // The rope of any node whose key range ends at r: the right child that
-  // starts at r+1 (a leaf iff leaf r+1 is itself a right child), or the
-  // sentinel on the right-most path (bvh.hpp:176-222).
-  __device__ __forceinline__ int32_t rope(int64_t r) const {
-    if (r == n - 1) return kSentinel;
-    if (r + 1 == n - 1 || D(r + 1) < D(r)) return (int32_t)(n - 1 + r + 1);
-    return (int32_t)(r + 1);
+  __device__ __forceinline__ int D(int32_t i) const {
+    return (uint32_t)i < (uint32_t)(n - 1) ? __ldg(delta + i) : -1;
   }
 };
+__device__ __forceinline__ int32_t rope_of(int32_t n, int32_t r, int32_t dr, int32_t dr1) {
+  return dr < 0 ? kSentinel : (dr1 < dr ? n + r : r + 1);
+}
 
 // The climb from leaf p (leaf box in lo/hi, already written): the first child
 // to arrive at a parent records its far bound in flags[split] and stops; the
 // second knows the parent's full range [l, r] and split, recovers its Karras
 // index (r for a left child, l for a right child, 0 for the root), joins the
 // two child boxes left-first and writes {box, left, rope}.
-// Climbs at most max_levels merges through the global flags; returns true
-// when this thread still owns a node whose parent is not built yet (the state
-// in l, r, lo, hi).
 //
 // Block-local hand-off (k_hierarchy): a CTA owns the leaves [B, B + BLK).
 // When a parent lies inside, its two children meet in shared memory (box
@@ -681,12 +677,13 @@ struct HierView {
 // length on each side of a: prefix and suffix minima of the CTA's staged
 // D(B-1 .. B+BLK-1), computed once per CTA.
 struct LocalClimb {
-  int64_t B;
+  int32_t B;
   const uint8_t *in;  // [CLIMB_BLK] shared: the parent at split B + i lies inside
-  int32_t *flag;      // [CLIMB_BLK] shared flags, -1 = empty (modes 0, 1)
-  unsigned long long *flag128;  // [CLIMB_BLK][2] shared flag words, bound -1 = empty (mode 2)
-  unsigned long long *box;  // [2][CLIMB_BLK][3] shared child boxes (0 = left, 1 = right), float pairs
-  __device__ __forceinline__ bool inside(int64_t a) const { return a >= B && a < B + CLIMB_BLK && in[a - B]; }
+  unsigned long long *flag;  // [CLIMB_BLK][2] shared flag words {bound | lo.x, lo.y | lo.z}, bound -1 = empty
+  unsigned long long *box;   // [2][CLIMB_BLK][2] shared words {hi.x | hi.y, hi.z | pass} per side (0 = left)
+  __device__ __forceinline__ bool inside(int32_t a) const {
+    return (uint32_t)(a - B) < (uint32_t)CLIMB_BLK && in[a - B];
+  }
 };
 
 __device__ __forceinline__ int32_t exch_acq_rel_gpu(int32_t *p, int32_t v) {
@@ -694,16 +691,7 @@ __device__ __forceinline__ int32_t exch_acq_rel_gpu(int32_t *p, int32_t v) {
   asm volatile("atom.acq_rel.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
 }
-__device__ __forceinline__ int32_t exch_acq_rel_cta_shared(int32_t *p, int32_t v) {
-  int32_t old;
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
-  asm volatile("atom.acq_rel.cta.shared::cta.exch.b32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
-  return old;
-}
 
-#ifndef SPB_CLIMB_SMEM_MODE
-#define SPB_CLIMB_SMEM_MODE 2
-#endif
 __device__ __forceinline__ unsigned long long pack2(float a, float b) {
   return (unsigned long long)__float_as_uint(a) | ((unsigned long long)__float_as_uint(b) << 32);
 }
@@ -720,128 +708,124 @@ __device__ __forceinline__ void exch128(unsigned long long *p, unsigned long lon
                  " mov.b128 {%0, %1}, d; }" : "+l"(x), "+l"(y) : "r"(a) : "memory");
 }
 
-// One block-local hand-off at split a: publish this child's box, exchange
-// the flag; returns the first arrival's bound (second arrival, sibling box in
-// slo/shi) or -1 (first arrival).  Every shared access of the slots is an
-// atomic (racecheck tracks barriers, not acquire/release), either 64-bit
-// words (mode 1) or 128-bit exchanges (mode 2): the flag word carries
-// {bound, lo.xyz} of the first arrival, a second word its hi.xyz.
-__device__ __forceinline__ int32_t local_handoff(const LocalClimb &lc, int64_t a, bool L, int32_t bound,
+// One block-local hand-off at split a: publish this child's hi corner (and
+// `pass`: its far-side split lengths) in its side's slot, then exchange the
+// flag word {bound, lo.xyz} with CTA-scope acquire-release; returns the first
+// arrival's bound (second arrival: sibling box in slo/shi, its lengths in
+// *theirs) or -1 (first arrival).  Every shared access of the slots is a
+// 128-bit atomic exchange: racecheck tracks barriers, not acquire/release
+// (plain stores and loads were measured no faster).
+__device__ __forceinline__ int32_t local_handoff(const LocalClimb &lc, int32_t a, bool L, int32_t bound,
                                                  const float lo[3], const float hi[3], float4 &slo, float4 &shi,
-                                                 uint32_t pass = 0, uint32_t *theirs = nullptr) {
-  const int64_t k = a - lc.B;
-  if (SPB_CLIMB_SMEM_MODE == 2) {
-    // box: [2][CLIMB_BLK][2] words of 64 bit per side: hi.xyz of that side
-    // and 32 free bits (`pass`: split lengths for the sibling); flag words:
-    // [CLIMB_BLK][2] {bound | lo.x, lo.y | lo.z}
-    unsigned long long *hslot = lc.box + ((L ? 0 : CLIMB_BLK) + k) * 2;
-    unsigned long long h0 = pack2(hi[0], hi[1]), h1 = pack2(hi[2], __uint_as_float(pass));
-    exch128(hslot, h0, h1, false);
-    unsigned long long w0 = (unsigned long long)(uint32_t)bound | ((unsigned long long)__float_as_uint(lo[0]) << 32);
-    unsigned long long w1 = pack2(lo[1], lo[2]);
-    exch128(lc.flag128 + 2 * k, w0, w1, true);
-    const int32_t other = (int32_t)(uint32_t)w0;
-    if (other < 0) return other;
-    unsigned long long g0 = 0, g1 = 0;
-    exch128(lc.box + ((L ? CLIMB_BLK : 0) + k) * 2, g0, g1, false);
-    slo = make_float4(hi32f(w0), lo32f(w1), hi32f(w1), 0.f);
-    shi = make_float4(lo32f(g0), hi32f(g0), lo32f(g1), 0.f);
-    if (theirs) *theirs = (uint32_t)(g1 >> 32);
-    return other;
-  }
-  unsigned long long *mine = lc.box + ((L ? 0 : CLIMB_BLK) + k) * 3;
-  if (SPB_CLIMB_SMEM_MODE == 1) {
-    atomicExch(mine, pack2(lo[0], lo[1]));
-    atomicExch(mine + 1, pack2(lo[2], hi[0]));
-    atomicExch(mine + 2, pack2(hi[1], hi[2]));
-  } else {
-    mine[0] = pack2(lo[0], lo[1]);
-    mine[1] = pack2(lo[2], hi[0]);
-    mine[2] = pack2(hi[1], hi[2]);
-  }
-  const int32_t other = exch_acq_rel_cta_shared(lc.flag + k, bound);
+                                                 uint32_t pass, uint32_t &theirs) {
+  const int32_t k = a - lc.B;
+  unsigned long long h0 = pack2(hi[0], hi[1]), h1 = pack2(hi[2], __uint_as_float(pass));
+  exch128(lc.box + ((L ? 0 : CLIMB_BLK) + k) * 2, h0, h1, false);
+  unsigned long long w0 = (unsigned long long)(uint32_t)bound | ((unsigned long long)__float_as_uint(lo[0]) << 32);
+  unsigned long long w1 = pack2(lo[1], lo[2]);
+  exch128(lc.flag + 2 * k, w0, w1, true);
+  const int32_t other = (int32_t)(uint32_t)w0;
   if (other < 0) return other;
-  unsigned long long *sb = lc.box + ((L ? CLIMB_BLK : 0) + k) * 3;
-  unsigned long long w0, w1, w2;
-  if (SPB_CLIMB_SMEM_MODE == 1) {
-    w0 = atomicOr(sb, 0ull);
-    w1 = atomicOr(sb + 1, 0ull);
-    w2 = atomicOr(sb + 2, 0ull);
-  } else {
-    w0 = sb[0];
-    w1 = sb[1];
-    w2 = sb[2];
-  }
-  slo = make_float4(lo32f(w0), hi32f(w0), lo32f(w1), 0.f);
-  shi = make_float4(hi32f(w1), lo32f(w2), hi32f(w2), 0.f);
+  unsigned long long g0 = 0, g1 = 0;
+  exch128(lc.box + ((L ? CLIMB_BLK : 0) + k) * 2, g0, g1, false);
+  slo = make_float4(hi32f(w0), lo32f(w1), hi32f(w1), 0.f);
+  shi = make_float4(lo32f(g0), hi32f(g0), lo32f(g1), 0.f);
+  theirs = (uint32_t)(g1 >> 32);
   return other;
 }
 
+// One climb step of the node [l, r] (box lo/hi, split lengths dl1 = D(l-1),
+// dr = D(r), dr1 = D(r+1)), already written: the first child to arrive at the
+// parent records its far bound and stops; the second knows the parent's full
+// range and split, joins the two child boxes left-first and writes the parent
+// {box, left, rope} at its Karras index (r for a left child, l for a right
+// child, 0 for the root).  Returns 0 when this thread stops (first arrival, or
+// the root written), 1 when it now owns the parent after a block-local
+// hand-off, 2 after a global exchange.
+//
+// Block-local hand-off (k_hierarchy): a CTA owns the leaves [B, B + BLK).
+// When a parent lies inside, its two children meet in shared memory (no L2
+// round trip, no L1 invalidation); otherwise both use the global flag.  Both
+// children must choose alike, so the choice is a property of the split: the
+// parent at split a (the lowest common ancestor of leaves a and a + 1, prefix
+// length D(a)) spans [l'', r''] with l'' - 1 = max{j < a : D(j) < D(a)} and
+// r'' = min{j > a : D(j) < D(a)} (equal lengths are always separated by a
+// smaller one).  It lies inside the CTA iff the CTA holds a smaller split
+// length on each side of a: prefix and suffix minima of the CTA's staged
+// D(B-1 .. B+BLK-1), computed once per CTA.  A local hand-off passes the
+// child's far-side lengths along with its box (a left child D(l-1), a right
+// child D(r) and D(r+1), 16 bits each), so local levels read no split lengths
+// from memory.
+//
+// Ordering: the global exchange is acquire-release -- the release half
+// orders this node's stores before the flag changes hands, the acquire half
+// orders the second arrival's reads of the sibling after the first arrival's
+// stores (the PTX memory model gives no ordering through the address
+// dependency alone); the sibling is read with L2-coherent loads.
 template <bool LOCAL>
-__device__ __forceinline__ bool climb(const HierView &H, int64_t &l, int64_t &r, float lo[3], float hi[3],
-                                      float4 *nodes, int32_t *flags, int max_levels, const LocalClimb &lc) {
-  const int64_t n = H.n;
-  // the split lengths around the node [l, r], carried from level to level: a
-  // block-local hand-off passes the sibling's far-side lengths along with its
-  // box, so the local levels read no split lengths from memory
-  int32_t dl1 = H.D(l - 1), dr = H.D(r), dr1 = H.D(r + 1);
+__device__ __forceinline__ int climb_step(const HierView &H, int32_t &l, int32_t &r, float lo[3], float hi[3],
+                                          int32_t &dl1, int32_t &dr, int32_t &dr1, float4 *nodes, int32_t *flags,
+                                          const LocalClimb &lc) {
+  const int32_t n = H.n;
+  const bool L = dr > dl1;
+  const int32_t a = L ? r : l - 1;  // the parent's split position
+  const int32_t bound = L ? l : r;
+  const bool local = LOCAL && lc.inside(a);
+  float4 slo, shi;
+  if (local) {
+    const uint32_t mine = L ? (uint32_t)(uint16_t)dl1 : ((uint32_t)(uint16_t)dr | ((uint32_t)(uint16_t)dr1 << 16));
+    uint32_t theirs = 0;
+    const int32_t other = local_handoff(lc, a, L, bound, lo, hi, slo, shi, mine, theirs);
+    if (other < 0) return 0;
+    if (L) {
+      r = other;
+      dr = (int16_t)(theirs & 0xffffu);
+      dr1 = (int16_t)(theirs >> 16);
+    } else {
+      l = other;
+      dl1 = (int16_t)(theirs & 0xffffu);
+    }
+  } else {
+    const int32_t other = exch_acq_rel_gpu(flags + a, bound);
+    if (other < 0) return 0;
+    if (L) {
+      r = other;
+      dr = H.D(r);
+      dr1 = H.D(r + 1);
+    } else {
+      l = other;
+      dl1 = H.D(l - 1);
+    }
+    const int32_t sib = L ? ((a + 1 == r) ? n - 1 + r : a + 1) : ((a == l) ? n - 1 + l : a);
+    slo = __ldcg(nodes + 2 * (int64_t)sib);
+    shi = __ldcg(nodes + 2 * (int64_t)sib + 1);
+  }
+  if (L) {  // this node is the left child
+    lo[0] = keep_min(lo[0], slo.x); lo[1] = keep_min(lo[1], slo.y); lo[2] = keep_min(lo[2], slo.z);
+    hi[0] = keep_max(hi[0], shi.x); hi[1] = keep_max(hi[1], shi.y); hi[2] = keep_max(hi[2], shi.z);
+  } else {
+    lo[0] = keep_min(slo.x, lo[0]); lo[1] = keep_min(slo.y, lo[1]); lo[2] = keep_min(slo.z, lo[2]);
+    hi[0] = keep_max(shi.x, hi[0]); hi[1] = keep_max(shi.y, hi[1]); hi[2] = keep_max(shi.z, hi[2]);
+  }
+  const int32_t left = (a == l) ? n - 1 + l : a;
+  const int64_t k = dr > dl1 ? r : l;  // the root (both -1) lands at l = 0
+  nodes[2 * k] = make_float4(lo[0], lo[1], lo[2], __int_as_float(left));
+  nodes[2 * k + 1] = make_float4(hi[0], hi[1], hi[2], __int_as_float(rope_of(n, r, dr, dr1)));
+  if ((dl1 & dr) < 0) return 0;  // the root
+  return local ? 1 : 2;
+}
+
+// Climbs at most max_levels merges through the global flags; returns true
+// when this thread still owns a node whose parent is not built yet (the state
+// in l, r, lo, hi).
+template <bool LOCAL>
+__device__ __forceinline__ bool climb(const HierView &H, int32_t &l, int32_t &r, float lo[3], float hi[3],
+                                      int32_t dl1, int32_t dr, int32_t dr1, float4 *nodes, int32_t *flags,
+                                      int max_levels, const LocalClimb &lc) {
   for (int level = 0; level < max_levels;) {
-    const bool L = l == 0 || (r != n - 1 && dr > dl1);  // HierView::is_left
-    const int64_t a = L ? r : l - 1;  // the parent's split position
-    const int32_t bound = (int32_t)(L ? l : r);
-    // Acquire-release exchanges: the release half orders this node's box
-    // stores before the flag changes hands; the acquire half orders the second
-    // arrival's reads of the sibling box after the first arrival's stores (the
-    // PTX memory model gives no ordering through the address dependency
-    // alone).  The global sibling box is read with L2-coherent loads.
-    const bool local = LOCAL && lc.inside(a);
-    float4 slo, shi;
-    if (local) {
-      // the parent keeps this child's far side: a left child hands over
-      // D(l-1), a right child D(r) and D(r+1) (16 bits each; -1 sentinel)
-      const uint32_t mine = L ? (uint32_t)(uint16_t)dl1 : ((uint32_t)(uint16_t)dr | ((uint32_t)(uint16_t)dr1 << 16));
-      uint32_t theirs = 0;
-      const int32_t other = local_handoff(lc, a, L, bound, lo, hi, slo, shi, mine, &theirs);
-      if (other < 0) return false;  // first arrival: the sibling is inside and will come
-      if (L) {
-        r = other;
-        dr = (int16_t)(theirs & 0xffffu);
-        dr1 = (int16_t)(theirs >> 16);
-      } else {
-        l = other;
-        dl1 = (int16_t)(theirs & 0xffffu);
-      }
-    } else {
-      const int32_t other = exch_acq_rel_gpu(flags + a, bound);
-      if (other < 0) return false;  // first arrival
-      if (L) {
-        r = other;
-        dr = H.D(r);
-        dr1 = H.D(r + 1);
-      } else {
-        l = other;
-        dl1 = H.D(l - 1);
-      }
-      const int64_t sib = L ? ((a + 1 == r) ? n - 1 + r : a + 1) : ((a == l) ? n - 1 + l : a);
-      slo = __ldcg(nodes + 2 * sib);
-      shi = __ldcg(nodes + 2 * sib + 1);
-      ++level;
-    }
-    const int64_t left = (a == l) ? n - 1 + l : a;
-    if (L) {  // this node is the left child
-      lo[0] = keep_min(lo[0], slo.x); lo[1] = keep_min(lo[1], slo.y); lo[2] = keep_min(lo[2], slo.z);
-      hi[0] = keep_max(hi[0], shi.x); hi[1] = keep_max(hi[1], shi.y); hi[2] = keep_max(hi[2], shi.z);
-    } else {
-      lo[0] = keep_min(slo.x, lo[0]); lo[1] = keep_min(slo.y, lo[1]); lo[2] = keep_min(slo.z, lo[2]);
-      hi[0] = keep_max(shi.x, hi[0]); hi[1] = keep_max(shi.y, hi[1]); hi[2] = keep_max(shi.z, hi[2]);
-    }
-    const bool root = (l == 0 && r == n - 1);
-    const int64_t k = root ? 0 : ((l == 0 || (r != n - 1 && dr > dl1)) ? r : l);
-    const int32_t rope = r == n - 1 ? kSentinel
-                                    : ((r + 1 == n - 1 || dr1 < dr) ? (int32_t)(n - 1 + r + 1) : (int32_t)(r + 1));
-    nodes[2 * k] = make_float4(lo[0], lo[1], lo[2], __int_as_float((int)left));
-    nodes[2 * k + 1] = make_float4(hi[0], hi[1], hi[2], __int_as_float(rope));
-    if (root) return false;
+    const int st = climb_step<LOCAL>(H, l, r, lo, hi, dl1, dr, dr1, nodes, flags, lc);
+    if (st == 0) return false;
+    if (st == 2) ++level;
   }
   return true;
 }
@@ -850,37 +834,61 @@ __device__ __forceinline__ bool climb(const HierView &H, int64_t &l, int64_t &r,
 // {hi xyz, unused}.  The first kernel does the bottom levels for every leaf;
 // the few threads still climbing continue here, packed densely, instead of
 // holding mostly-finished warps for the whole height of the tree.
-__global__ void __launch_bounds__(256) k_climb_rest(int64_t n, const int32_t *__restrict__ delta,
+__global__ void __launch_bounds__(256) k_climb_rest(int32_t n, const int32_t *__restrict__ delta,
                                                     const float4 *__restrict__ queue,
                                                     const uint32_t *__restrict__ qcount, float4 *nodes,
                                                     int32_t *flags) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)*qcount) return;
-  HierView H{n, delta};
+  const HierView H{n, delta};
   const float4 s0 = queue[2 * i], s1 = queue[2 * i + 1];
-  int64_t l = __float_as_int(s0.x), r = __float_as_int(s0.y);
+  int32_t l = __float_as_int(s0.x), r = __float_as_int(s0.y);
   float lo[3] = {s0.z, s0.w, s1.x}, hi[3] = {s1.y, s1.z, s1.w};
-  climb<false>(H, l, r, lo, hi, nodes, flags, 1 << 30, LocalClimb{0, nullptr, nullptr, nullptr, nullptr});
+  climb<false>(H, l, r, lo, hi, H.D(l - 1), H.D(r), H.D(r + 1), nodes, flags, 1 << 30,
+               LocalClimb{0, nullptr, nullptr, nullptr});
 }
 
 template <bool POINTS>
-__global__ void __launch_bounds__(CLIMB_BLK) k_hierarchy(int64_t n, const int32_t *__restrict__ delta,
+__global__ void __launch_bounds__(CLIMB_BLK) k_hierarchy(int32_t n, const int32_t *__restrict__ delta,
                                                    const uint32_t *__restrict__ perm, const float *__restrict__ obj,
                                                    int dim, float4 *nodes, int32_t *flags,
                                                    int32_t *__restrict__ perm_out, float4 *__restrict__ leafpt,
                                                    int max_levels, float4 *__restrict__ queue,
                                                    uint32_t *__restrict__ qcount, const float4 *spts) {
-  __shared__ int32_t s_flag[CLIMB_BLK];
   __shared__ int32_t s_D[CLIMB_BLK + 1], s_pre[CLIMB_BLK], s_suf[CLIMB_BLK + 1], s_wmin[2][CLIMB_BLK / 32];
   __shared__ uint8_t s_in[CLIMB_BLK];
-  __shared__ __align__(16) unsigned long long s_box[2 * CLIMB_BLK * 3];
-  __shared__ __align__(16) unsigned long long s_flag128[2 * CLIMB_BLK];
+  __shared__ __align__(16) unsigned long long s_box[2 * CLIMB_BLK * 2];
+  __shared__ __align__(16) unsigned long long s_flag[2 * CLIMB_BLK];
   const HierView H{n, delta};
-  const int64_t B = (int64_t)blockIdx.x * CLIMB_BLK;
+  const int32_t B = (int32_t)blockIdx.x * CLIMB_BLK;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  s_flag[t] = -1;
-  s_flag128[2 * t] = 0xffffffffull;  // bound -1
-  s_flag128[2 * t + 1] = 0;
+  const int32_t p = B + t;
+  const bool valid = p < n;
+  // the leaf's box first: its load latency overlaps the staging below
+  uint32_t oi = (uint32_t)p;
+  float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f};
+  if (!valid) {
+  } else if (POINTS && spts) {  // sorted points from the top-bits sort (3-D): no gather
+    const float4 q = spts[p];
+    oi = __float_as_uint(q.w);
+    lo[0] = hi[0] = q.x;
+    lo[1] = hi[1] = q.y;
+    lo[2] = hi[2] = q.z;
+  } else if (!POINTS && !obj) {  // leaf nodes written by the caller (k_cell_ranges): read the box back
+    const float4 a = nodes[2 * (int64_t)(n - 1 + p)], b = nodes[2 * (int64_t)(n - 1 + p) + 1];
+    lo[0] = a.x; lo[1] = a.y; lo[2] = a.z;
+    hi[0] = b.x; hi[1] = b.y; hi[2] = b.z;
+  } else {
+    oi = perm ? perm[p] : (uint32_t)p;
+    const int sz = POINTS ? dim : 2 * dim;
+    const float *o = obj + (int64_t)oi * sz;
+    for (int k = 0; k < dim; ++k) {
+      lo[k] = o[k];
+      hi[k] = POINTS ? lo[k] : o[dim + k];
+    }
+  }
+  s_flag[2 * t] = 0xffffffffull;  // bound -1
+  s_flag[2 * t + 1] = 0;
   const int32_t dv = H.D(B - 1 + t);  // element t of D(B-1 .. B+BLK-1)
   s_D[t] = dv;
   if (t == 0) s_D[CLIMB_BLK] = H.D(B + CLIMB_BLK - 1);
@@ -906,44 +914,23 @@ __global__ void __launch_bounds__(CLIMB_BLK) k_hierarchy(int64_t n, const int32_
   // s_pre[t], right minimum over D(a+1 .. B+BLK-1) = s_suf[t + 2]
   s_in[t] = t + 1 < CLIMB_BLK && s_pre[t] < s_D[t + 1] && s_suf[t + 2] < s_D[t + 1];
   __syncthreads();
-  const int64_t p = B + threadIdx.x;
-  if (p >= n) return;
-  uint32_t oi;
-  float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f};
-  if (POINTS && spts) {  // sorted points from the top-32 sort (3-D): no gather
-    const float4 q = spts[p];
-    oi = __float_as_uint(q.w);
-    lo[0] = hi[0] = q.x;
-    lo[1] = hi[1] = q.y;
-    lo[2] = hi[2] = q.z;
-  } else if (!POINTS && !obj) {  // leaf nodes written by the caller (k_cell_ranges): read the box back
-    oi = (uint32_t)p;
-    const float4 a = nodes[2 * (n - 1 + p)], b = nodes[2 * (n - 1 + p) + 1];
-    lo[0] = a.x; lo[1] = a.y; lo[2] = a.z;
-    hi[0] = b.x; hi[1] = b.y; hi[2] = b.z;
-  } else {
-    oi = perm ? perm[p] : (uint32_t)p;
-    const int sz = POINTS ? dim : 2 * dim;
-    const float *o = obj + (int64_t)oi * sz;
-    for (int k = 0; k < dim; ++k) {
-      lo[k] = o[k];
-      hi[k] = POINTS ? lo[k] : o[dim + k];
-    }
-  }
+  if (!valid) return;
+  // split lengths around the leaf: D(p-1), D(p), D(p+1)
+  int32_t dl1 = dv, dr = s_D[t + 1], dr1 = t + 2 <= CLIMB_BLK ? s_D[t + 2] : H.D(p + 1);
   if (perm_out) perm_out[p] = (int32_t)oi;
   const int64_t leaf = n - 1 + p;
-  const int32_t leaf_rope = H.rope(p);
+  const int32_t leaf_rope = rope_of(n, p, dr, dr1);
   if (POINTS || obj) {
     nodes[2 * leaf] = make_float4(lo[0], lo[1], lo[2], __int_as_float((int)oi));
     nodes[2 * leaf + 1] = make_float4(hi[0], hi[1], hi[2], __int_as_float(leaf_rope));
   }
   if (POINTS) leafpt[p] = make_float4(lo[0], lo[1], lo[2], __int_as_float(leaf_rope));
   if (n == 1) return;
-  int64_t l = p, r = p;
-  const LocalClimb lc{B, s_in, s_flag, s_flag128, s_box};
-  if (climb<true>(H, l, r, lo, hi, nodes, flags, max_levels, lc)) {
+  int32_t l = p, r = p;
+  const LocalClimb lc{B, s_in, s_flag, s_box};
+  if (climb<true>(H, l, r, lo, hi, dl1, dr, dr1, nodes, flags, max_levels, lc)) {
     const uint32_t slot = atomicAdd(qcount, 1u);
-    queue[2 * (int64_t)slot] = make_float4(__int_as_float((int)l), __int_as_float((int)r), lo[0], lo[1]);
+    queue[2 * (int64_t)slot] = make_float4(__int_as_float(l), __int_as_float(r), lo[0], lo[1]);
     queue[2 * (int64_t)slot + 1] = make_float4(lo[2], hi[0], hi[1], hi[2]);
   }
 }
