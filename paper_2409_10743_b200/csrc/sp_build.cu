@@ -1116,21 +1116,30 @@ __global__ void __launch_bounds__(256) k_fix_gather(const float *__restrict__ pt
 
 // Each element of a run of equal top bits [s, e) takes rank #{q in run :
 // (code, index)(q) < (code, index)(p)} and moves to s + rank; singletons copy.
-// The same in shared memory: a CTA stages the keys, codes and indices of its
+// The same in shared memory: a CTA stages the codes and indices of its
 // FIX_CH positions and FIX_MAX_RUN more on each side (every run of at most
 // FIX_MAX_RUN through a position of the chunk lies inside), so the run scans
 // and the O(run) ranking read shared memory (clustered fields have runs of
 // hundreds: the global-memory version took 20 ms at 2^27 on H(2^27)).
+// The CTA also ranks the halo elements of the runs that reach into its chunk
+// and keeps the sorted (code, index) of positions [c0, c0 + FIX_CH] in shared
+// memory, so it writes the split lengths D(c0 .. c0 + FIX_CH - 1) of the
+// hierarchy itself (k_delta's pass over the sorted codes and indices, and
+// writing those, are gone); the sorted points go to spts.
 constexpr int FIX_CH = 2048;
 constexpr int FIX_WIN = FIX_CH + 2 * FIX_MAX_RUN;
+constexpr size_t FIX_SMEM = (size_t)(FIX_WIN + FIX_CH + 1) * (sizeof(uint64_t) + sizeof(uint32_t));
 template <int SHIFT>  // runs: equal code >> SHIFT (31: top 32 of 63 bits, 23: top 40)
 __global__ void __launch_bounds__(256) k_fix_runs_win(int64_t n, const uint64_t *__restrict__ tcode,
-                                                      const float4 *__restrict__ tpt, uint64_t *__restrict__ code,
-                                                      uint32_t *__restrict__ perm, float4 *__restrict__ spts,
-                                                      int *overflow) {
-  __shared__ uint64_t sc[FIX_WIN];
-  __shared__ uint32_t si[FIX_WIN];
-  const int64_t c0 = (int64_t)blockIdx.x * FIX_CH, w0 = c0 - FIX_MAX_RUN;
+                                                      const float4 *__restrict__ tpt, float4 *__restrict__ spts,
+                                                      int32_t *__restrict__ delta, int *overflow) {
+  extern __shared__ __align__(16) unsigned char fix_smem[];
+  uint64_t *sc = reinterpret_cast<uint64_t *>(fix_smem);  // [FIX_WIN] window codes
+  uint64_t *oc = sc + FIX_WIN;                              // [FIX_CH + 1] sorted codes at c0 ..
+  uint32_t *si = reinterpret_cast<uint32_t *>(oc + FIX_CH + 1);  // [FIX_WIN] window indices
+  uint32_t *ox = si + FIX_WIN;                                   // [FIX_CH + 1] sorted indices at c0 ..
+  constexpr int M = FIX_MAX_RUN;  // window index of c0
+  const int64_t c0 = (int64_t)blockIdx.x * FIX_CH, w0 = c0 - M;
   const int lo_lim = w0 < 0 ? (int)(-w0) : 0;
   const int hi_lim = (int)((n - w0) < FIX_WIN ? (n - w0) : FIX_WIN);
   for (int i = threadIdx.x; i < FIX_WIN; i += blockDim.x) {
@@ -1141,16 +1150,18 @@ __global__ void __launch_bounds__(256) k_fix_runs_win(int64_t n, const uint64_t 
     }
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < FIX_CH; j += blockDim.x) {
-    const int64_t p = c0 + j;
-    if (p >= n) break;
-    const int li = j + FIX_MAX_RUN;
+  const int last = min(M + FIX_CH, hi_lim - 1);  // the sorted positions kept: window [M, last]
+  for (int li = threadIdx.x; li < FIX_WIN; li += blockDim.x) {
+    if (li < lo_lim || li >= hi_lim || M > last) continue;
     const uint64_t c = sc[li], k = c >> SHIFT;
+    // a halo element matters only if its run reaches the kept positions
+    // (equal top bits are contiguous in sorted order)
+    if (li < M ? (sc[M] >> SHIFT) != k : (li > last && (sc[last] >> SHIFT) != k)) continue;
     int s = li, e = li + 1;
     while (s > lo_lim && li - s < FIX_MAX_RUN && (sc[s - 1] >> SHIFT) == k) --s;
     while (e < hi_lim && e - li <= FIX_MAX_RUN && (sc[e] >> SHIFT) == k) ++e;
     const uint32_t i = si[li];
-    int64_t dst = p;
+    int d = li;
     if (e - s > 1) {
       if (e - s > FIX_MAX_RUN) {
         *overflow = 1;
@@ -1161,11 +1172,20 @@ __global__ void __launch_bounds__(256) k_fix_runs_win(int64_t n, const uint64_t 
         const uint64_t cq = sc[q];
         r += (cq < c) | ((cq == c) & (si[q] < i));
       }
-      dst = w0 + s + r;
+      d = s + r;
     }
-    code[dst] = c;
-    perm[dst] = i;
-    spts[dst] = tpt[p];
+    if (d >= M && d <= last) {
+      oc[d - M] = c;
+      ox[d - M] = i;
+    }
+    if (li >= M && li < M + FIX_CH) spts[w0 + d] = tpt[w0 + li];
+  }
+  __syncthreads();
+  // D(p) of sorted positions p, p + 1 (k_delta with 64-bit codes)
+  for (int j = threadIdx.x; j < FIX_CH; j += blockDim.x) {
+    if (M + j + 1 > last) break;
+    const uint64_t a = oc[j], b = oc[j + 1];
+    delta[c0 + j] = a != b ? __clzll((long long)(a ^ b)) : 64 + __clz((int)(ox[j] ^ ox[j + 1]));
   }
 }
 
@@ -1272,6 +1292,7 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
 
   DevBuf<uint64_t> k0(n, c.stream), k1(n, c.stream);
   DevBuf<uint32_t> v0(n, c.stream), v1(n, c.stream);
+  DevBuf<int32_t> delta(n > 1 ? n - 1 : 1, c.stream), flags(n > 1 ? n - 1 : 1, c.stream);
   uint64_t *ka = k0.get(), *kb = k1.get();
   uint32_t *va = v0.get(), *vb = v1.get();
   const float4 *spts = nullptr;  // points in sorted order (the top-32 path writes them)
@@ -1301,21 +1322,28 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
     k_fix_gather<<<(unsigned)((n + 256 * FIX_ILP - 1) / (256 * FIX_ILP)), 256, 0, c.stream>>>(
         objects, n, width, t.scene, va, tcode, tpt);
     SPB_LAUNCHED();
+    {
+      static std::mutex mu;
+      static uint64_t opted = 0;
+      std::lock_guard<std::mutex> g(mu);
+      if (c.device >= 64 || !((opted >> c.device) & 1)) {
+        SPB_CUDA(cudaFuncSetAttribute(k_fix_runs_win<31>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FIX_SMEM));
+        SPB_CUDA(cudaFuncSetAttribute(k_fix_runs_win<23>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FIX_SMEM));
+        if (c.device < 64) opted |= 1ull << c.device;
+      }
+    }
     const unsigned gw = (unsigned)((n + FIX_CH - 1) / FIX_CH);
     if (topbits == 32)
-      k_fix_runs_win<31><<<gw, 256, 0, c.stream>>>(n, tcode, tpt, k1.get(), vb, t.leafpt, ovf.get());
+      k_fix_runs_win<31><<<gw, 256, FIX_SMEM, c.stream>>>(n, tcode, tpt, t.leafpt, delta.get(), ovf.get());
     else
-      k_fix_runs_win<23><<<gw, 256, 0, c.stream>>>(n, tcode, tpt, k1.get(), vb, t.leafpt, ovf.get());
+      k_fix_runs_win<23><<<gw, 256, FIX_SMEM, c.stream>>>(n, tcode, tpt, t.leafpt, delta.get(), ovf.get());
     SPB_LAUNCHED();
     int h_ovf = 0;
     peek(c, {{ovf.get(), &h_ovf, sizeof(int)}});
     c.count("sort_top_bits", topbits);
     c.count("sort_fallback", h_ovf);
     if (!h_ovf) {
-      ka = k1.get();
-      kb = k0.get();
-      std::swap(va, vb);
-      spts = t.leafpt;
+      spts = t.leafpt;  // sorted points, their indices in .w, and D written
     } else {
       va = v0.get();  // a run longer than FIX_MAX_RUN: the full 63-bit sort below
       vb = v1.get();
@@ -1327,10 +1355,11 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
     radix_sort_pairs(c, &ka, &va, &kb, &vb, n, (width / dim) * dim, /*vals_iota=*/true);
   }
   mark(c, "sort");
-  DevBuf<int32_t> delta(n > 1 ? n - 1 : 1, c.stream), flags(n > 1 ? n - 1 : 1, c.stream);
   if (n > 1) {
-    k_delta<<<grid_for(n, 256, 148 * 16), 256, 0, c.stream>>>(ka, va, n, width, delta.get());
-    SPB_LAUNCHED();
+    if (!spts) {
+      k_delta<<<grid_for(n, 256, 148 * 16), 256, 0, c.stream>>>(ka, va, n, width, delta.get());
+      SPB_LAUNCHED();
+    }
     SPB_CUDA(cudaMemsetAsync(flags.get(), 0xff, (size_t)(n - 1) * sizeof(int32_t), c.stream));
   }
   unsigned g = (unsigned)((n + 255) / 256);
