@@ -638,7 +638,10 @@ __global__ void __launch_bounds__(256) k_delta(const uint64_t *__restrict__ sk, 
   }
 }
 
-constexpr int CLIMB_BLK = 256;
+#ifndef SPB_CLIMB_BLK
+#define SPB_CLIMB_BLK 256
+#endif
+constexpr int CLIMB_BLK = SPB_CLIMB_BLK;
 // Split lengths in 32-bit index arithmetic (n < 2^31: Karras indices are
 // int32).  D(-1) = D(n-1) = -1 while every real split length is >= 0, which
 // folds the range-end tests into the lengths themselves: a node [l, r] is its
@@ -1362,13 +1365,13 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
     }
     SPB_CUDA(cudaMemsetAsync(flags.get(), 0xff, (size_t)(n - 1) * sizeof(int32_t), c.stream));
   }
-  unsigned g = (unsigned)((n + 255) / 256);
+  unsigned g = (unsigned)((n + CLIMB_BLK - 1) / CLIMB_BLK);
   ClimbQueue q(c, n, SPB_CLIMB_LEVELS_POINTS);
   if (points)
-    k_hierarchy<true><<<g, 256, 0, c.stream>>>(n, delta.get(), va, objects, dim, t.nodes, flags.get(), t.perm,
+    k_hierarchy<true><<<g, CLIMB_BLK, 0, c.stream>>>(n, delta.get(), va, objects, dim, t.nodes, flags.get(), t.perm,
                                                t.leafpt, q.levels, q.buf.get(), q.count.get(), spts);
   else
-    k_hierarchy<false><<<g, 256, 0, c.stream>>>(n, delta.get(), va, objects, dim, t.nodes, flags.get(), t.perm,
+    k_hierarchy<false><<<g, CLIMB_BLK, 0, c.stream>>>(n, delta.get(), va, objects, dim, t.nodes, flags.get(), t.perm,
                                                 nullptr, q.levels, q.buf.get(), q.count.get(), nullptr);
   SPB_LAUNCHED();
   q.finish(c, n, delta.get(), t.nodes, flags.get());
@@ -1397,7 +1400,7 @@ void build_sorted_hierarchy(Ctx &c, const uint64_t *keys, int64_t m, int dim, co
     SPB_CUDA(cudaMemsetAsync(flags.get(), 0xff, (size_t)(m - 1) * sizeof(int32_t), c.stream));
   }
   ClimbQueue q(c, m, SPB_CLIMB_LEVELS_CELLS);
-  k_hierarchy<false><<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(m, delta.get(), nullptr, boxes, dim, t.nodes,
+  k_hierarchy<false><<<(unsigned)((m + CLIMB_BLK - 1) / CLIMB_BLK), CLIMB_BLK, 0, c.stream>>>(m, delta.get(), nullptr, boxes, dim, t.nodes,
                                                                         flags.get(), nullptr, nullptr, q.levels,
                                                                         q.buf.get(), q.count.get(), nullptr);
   SPB_LAUNCHED();
