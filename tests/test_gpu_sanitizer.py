@@ -28,5 +28,7 @@ def _run(tool, *extra):
 ])
 def test_sanitizer_clean(tool, extra, clean):
     rc, out = _run(tool, *extra)
+    if "sanitized run ok" not in out and "compute-sanitizer is closed" in out:
+        pytest.skip("compute-sanitizer is disabled on this GPU pool: " + out.strip().splitlines()[0][:200])
     assert "sanitized run ok" in out, out[-2000:]
     assert clean in out, out[-2000:]
