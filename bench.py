@@ -177,6 +177,19 @@ def profiled_traffic(phase: str, n: int):
         return None
 
 
+def profiled_l1(phase: str, n: int):
+    """l1tex__throughput (fraction of peak) of the phase's kernel from the
+    committed capture (profiles/r02), headline size only; None otherwise."""
+    if n != (1 << 27) or phase not in PROFILED:
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", PROFILED[phase] + ".summary.json")) as f:
+            d = json.load(f)
+        return round(float(d["L1 throughput % of peak"].split()[0]) / 100.0, 3)
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------------------
 # reference CPU path (oracle/_ref) — the cpu_baseline leg and --impl reference
 # ---------------------------------------------------------------------------
@@ -429,6 +442,12 @@ def run_ours(args, rank, world, local_rank):
                     "frac": round(ach / peak, 4), "traffic": profiled_traffic(dom, n), "peak_source": peak_src,
                     "algorithmic_bytes_per_launch": ach_bytes, "kernel_ms": round(phases[dom], 3),
                     "share_of_step": round(phases[dom] / ms_per_step, 3)}
+        l1 = profiled_l1(dom, n)
+        if l1 is not None:
+            # the traversal kernels are bound by the L1 (load wavefronts of
+            # L1-hot node reads), not by HBM: ncu's l1tex throughput of the
+            # committed capture of this kernel, as a fraction of its peak
+            roofline["l1_throughput_frac"] = l1
         build_ms = sum(phases.get(k, 0.0) for k in ("bounds", "morton", "sort", "hierarchy"))
     else:
         build_ms = None

@@ -7,6 +7,7 @@ METRICS = [
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram % of peak"),
     ("lts__t_sector_hit_rate.pct", "L2 hit rate"),
     ("l1tex__t_sector_hit_rate.pct", "L1 hit rate"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1 throughput % of peak"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active"),
     ("smsp__thread_inst_executed_per_inst_executed.ratio", "threads per warp instruction"),
