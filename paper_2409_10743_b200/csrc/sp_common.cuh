@@ -174,6 +174,23 @@ __host__ __device__ __forceinline__ float float_of_ord(int32_t i) {
 }
 
 __device__ __forceinline__ float4 ld_node(const float4 *nodes, int64_t i) { return __ldg(nodes + i); }
+// Both halves of node j (float4 2j and 2j + 1, one 32-byte sector) in one
+// 256-bit read-only load (LDG.E.ENL2.256 on sm_100a): one L1 request per node
+// visit instead of two -- the traversal walks are bound by L1 requests on
+// L1-hot nodes, not by HBM.
+#ifndef SPB_LD256
+#define SPB_LD256 1
+#endif
+__device__ __forceinline__ void ld_node2(const float4 *nodes, int64_t j, float4 &lo, float4 &hi) {
+#if SPB_LD256
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
+      : "l"(nodes + 2 * j));
+#else
+  lo = __ldg(nodes + 2 * j);
+  hi = __ldg(nodes + 2 * j + 1);
+#endif
+}
 
 // Four consecutive 3-D points (12 floats) as three 16-byte loads; the array
 // must be 16-byte aligned.

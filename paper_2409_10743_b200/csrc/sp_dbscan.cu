@@ -60,7 +60,8 @@ __global__ void __launch_bounds__(128, 1) k_core_flags(const float4 *__restrict_
           if (!counted && hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z) && ++c == min_pts) cur = kSentinel;
           else cur = __float_as_int(L.w);
         } else {
-          const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+          float4 lo, hi;
+          ld_node2(nodes, (int64_t)cur, lo, hi);
           cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
         }
       }
@@ -125,8 +126,8 @@ __global__ void __launch_bounds__(128, 1) k_merge_pairs(const float4 *__restrict
           merge_pair<FOF, SEQ>((int32_t)p, q, core_p, root_p, parent, corep, claims);
         cur = __float_as_int(L.w);
       } else {
-        const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
-        const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+        float4 lo, hi;
+        ld_node2(nodes, (int64_t)cur, lo, hi);
         cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
       }
     }
@@ -164,7 +165,8 @@ __global__ void __launch_bounds__(128) k_border_seq(const float4 *__restrict__ n
       found = take ? q : found;
       cur = take ? kSentinel : __float_as_int(L.w);
     } else {
-      const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+      float4 lo, hi;
+      ld_node2(nodes, (int64_t)cur, lo, hi);
       cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
     }
   }

@@ -865,7 +865,8 @@ __device__ __forceinline__ void fof_cell_walk(const float4 *__restrict__ nodes, 
                                               const float4 *__restrict__ cpts, const Radius &R, int32_t *parent,
                                               int64_t a, unsigned long long *stats = nullptr) {
   const int32_t first_leaf = (int32_t)(m - 1);
-  const float4 qlo = ld_node(nodes, 2 * (first_leaf + a)), qhi = ld_node(nodes, 2 * (first_leaf + a) + 1);
+  float4 qlo, qhi;
+  ld_node2(nodes, (first_leaf + a), qlo, qhi);
   const int64_t sa = cell_start[a], ea = a + 1 < m ? cell_start[a + 1] : n;
   int32_t root = (int32_t)a;
   int32_t cur = node_rope(qhi);
@@ -876,7 +877,8 @@ __device__ __forceinline__ void fof_cell_walk(const float4 *__restrict__ nodes, 
   // and the walk then runs about 5x slower.
   while (cur != kSentinel) {
     if (STATS) ++visits;
-    const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+    float4 lo, hi;
+    ld_node2(nodes, (int64_t)cur, lo, hi);
     const bool far = cells_far(R, qlo, qhi, lo, hi);
     const bool descend = !far && cur < first_leaf;
     if (STATS) {
@@ -1482,7 +1484,8 @@ __global__ void __launch_bounds__(128) k_cells_core(const float4 *__restrict__ n
     const int64_t w_hi = own + SPB_CORE_WINDOW < m - 1 ? own + SPB_CORE_WINDOW : m - 1;
     for (int64_t b = w_lo; b <= w_hi && cnt < min_pts; ++b) {
       if (b == own) continue;
-      const float4 lo = ld_node(nodes, 2 * (first_leaf + b)), hi = ld_node(nodes, 2 * (first_leaf + b) + 1);
+      float4 lo, hi;
+      ld_node2(nodes, (first_leaf + b), lo, hi);
       if (!hit_box(R, me.x, me.y, me.z, lo, hi)) continue;
       const int64_t e = cell_end(cell_start, m, n, b);
       for (int64_t j = cell_start[b]; j < e && cnt < min_pts; ++j) {
@@ -1493,7 +1496,8 @@ __global__ void __launch_bounds__(128) k_cells_core(const float4 *__restrict__ n
     if (cnt < min_pts) {
       int32_t cur = 0;  // root: internal 0, or leaf 0 when m == 1
       while (cur != kSentinel) {
-        const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+        float4 lo, hi;
+        ld_node2(nodes, (int64_t)cur, lo, hi);
         if (cur < first_leaf) {
           cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
           continue;
@@ -1541,12 +1545,14 @@ __global__ void __launch_bounds__(128) k_cells_core_merge(const float4 *__restri
   for (int64_t a; w.next(a);)
     if (a >= 0 && hascore[a]) {
       const int64_t first_leaf = m - 1;
-      const float4 qlo = ld_node(nodes, 2 * (first_leaf + a)), qhi = ld_node(nodes, 2 * (first_leaf + a) + 1);
+      float4 qlo, qhi;
+      ld_node2(nodes, (first_leaf + a), qlo, qhi);
       const int64_t sa = cell_start[a], ea = cell_end(cell_start, m, n, a);
       int32_t root = (int32_t)a;
       int32_t cur = node_rope(qhi);
       while (cur != kSentinel) {
-        const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+        float4 lo, hi;
+        ld_node2(nodes, (int64_t)cur, lo, hi);
         if (cells_far(R, qlo, qhi, lo, hi)) {
           cur = node_rope(hi);
           continue;
@@ -1605,7 +1611,8 @@ __global__ void __launch_bounds__(128) k_cells_border(const float4 *__restrict__
       const int64_t first_leaf = m - 1;
       int32_t cur = 0;
       while (cur != kSentinel && found < 0) {
-        const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+        float4 lo, hi;
+        ld_node2(nodes, (int64_t)cur, lo, hi);
         if (cur < first_leaf) {
           cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
           continue;

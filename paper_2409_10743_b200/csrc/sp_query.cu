@@ -72,8 +72,8 @@ __device__ __forceinline__ void range_count_one(const float4 *__restrict__ nodes
     c = 0;
     int32_t cur = 0;
     while (cur != kSentinel) {
-      const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
-      const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+      float4 lo, hi;
+      ld_node2(nodes, (int64_t)cur, lo, hi);
       const bool hit = box_touch(lo, hi, b);
       if (cur >= n - 1) {
         cur = (hit && ++c == cap) ? kSentinel : node_rope(hi);
@@ -238,8 +238,8 @@ __global__ void __launch_bounds__(128) k_range_fill(const float4 *__restrict__ n
     }
     int32_t cur = 0;
     while (cur != kSentinel) {
-      const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
-      const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+      float4 lo, hi;
+      ld_node2(nodes, (int64_t)cur, lo, hi);
       const bool leaf = cur >= n - 1;
       const bool hit = MODE == 1 ? (leaf ? hit_box(R, cx, cy, cz, lo, hi) : maybe_box(R, cx, cy, cz, lo, hi))
                                  : box_touch(lo, hi, b);
@@ -309,8 +309,8 @@ __global__ void __launch_bounds__(128) k_pairs(const float4 *__restrict__ nodes,
   int64_t w = FILL ? offsets[p] : 0;
   int32_t c = 0;
   while (cur != kSentinel) {
-    const float4 lo = ld_node(nodes, 2 * (int64_t)cur);
-    const float4 hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+    float4 lo, hi;
+    ld_node2(nodes, (int64_t)cur, lo, hi);
     const bool leaf = cur >= n - 1;
     const bool hit = leaf ? hit_box(R, me.x, me.y, me.z, lo, hi) : maybe_box(R, me.x, me.y, me.z, lo, hi);
     if (leaf) {
@@ -487,9 +487,11 @@ __global__ void __launch_bounds__(128) k_knn(const float4 *__restrict__ nodes, i
       continue;
     }
     const int32_t left = ref;
-    const float4 llo = ld_node(nodes, 2 * (int64_t)left), lhi = ld_node(nodes, 2 * (int64_t)left + 1);
+    float4 llo, lhi;
+    ld_node2(nodes, (int64_t)left, llo, lhi);
     const int32_t right = node_rope(lhi);
-    const float4 rlo = ld_node(nodes, 2 * (int64_t)right), rhi = ld_node(nodes, 2 * (int64_t)right + 1);
+    float4 rlo, rhi;
+    ld_node2(nodes, (int64_t)right, rlo, rhi);
     float dn = box_dist(x, y, z, llo, lhi), df = box_dist(x, y, z, rlo, rhi);
     int32_t rn = left >= n - 1 ? ~node_link(llo) : node_link(llo);
     int32_t rf = right >= n - 1 ? ~node_link(rlo) : node_link(rlo);
@@ -656,9 +658,11 @@ __global__ void __launch_bounds__(128) k_knn16lb(const float4 *__restrict__ node
     }
     // an internal node: ref is its left child
     const int32_t left = ref;
-    const float4 llo = ld_node(nodes, 2 * (int64_t)left), lhi = ld_node(nodes, 2 * (int64_t)left + 1);
+    float4 llo, lhi;
+    ld_node2(nodes, (int64_t)left, llo, lhi);
     const int32_t right = node_rope(lhi);
-    const float4 rlo = ld_node(nodes, 2 * (int64_t)right), rhi = ld_node(nodes, 2 * (int64_t)right + 1);
+    float4 rlo, rhi;
+    ld_node2(nodes, (int64_t)right, rlo, rhi);
     float dn = box_dist_lb(x, y, z, llo, lhi), df = box_dist_lb(x, y, z, rlo, rhi);
     int32_t rn = left >= first_leaf ? ~(left - first_leaf) : node_link(llo);
     int32_t rf = right >= first_leaf ? ~(right - first_leaf) : node_link(rlo);
@@ -742,7 +746,8 @@ __global__ void k_walk_lengths(const float4 *__restrict__ nodes, const float4 *_
       h += hit_point(R, me.x, me.y, me.z, L.x, L.y, L.z);
       cur = __float_as_int(L.w);
     } else {
-      const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+      float4 lo, hi;
+      ld_node2(nodes, (int64_t)cur, lo, hi);
       cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
     }
   }
@@ -826,7 +831,8 @@ __global__ void __launch_bounds__(128) k_eq_border(const float4 *__restrict__ no
       }
       cur = __float_as_int(L.w);
     } else {
-      const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+      float4 lo, hi;
+      ld_node2(nodes, (int64_t)cur, lo, hi);
       cur = maybe_box(R, me.x, me.y, me.z, lo, hi) ? node_link(lo) : node_rope(hi);
     }
   }

@@ -104,7 +104,8 @@ __device__ __forceinline__ int32_t count_sphere(const float4 *__restrict__ nodes
         hit = hit_point(R, cx, cy, cz, L.x, L.y, L.z);
         next = __float_as_int(L.w);
       } else {
-        const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+        float4 lo, hi;
+        ld_node2(nodes, (int64_t)cur, lo, hi);
         hit = hit_box(R, cx, cy, cz, lo, hi);
         next = node_rope(hi);
       }
@@ -112,7 +113,8 @@ __device__ __forceinline__ int32_t count_sphere(const float4 *__restrict__ nodes
       // the warp its per-iteration reconvergence)
       cur = (hit && ++c == cap) ? kSentinel : next;
     } else {
-      const float4 lo = ld_node(nodes, 2 * (int64_t)cur), hi = ld_node(nodes, 2 * (int64_t)cur + 1);
+      float4 lo, hi;
+      ld_node2(nodes, (int64_t)cur, lo, hi);
       cur = maybe_box(R, cx, cy, cz, lo, hi) ? node_link(lo) : node_rope(hi);
     }
   }
