@@ -2,13 +2,14 @@
 # (with its C3/C5 extras and CPU baseline), the reference arm, the other
 # SURVEY configs, the one-rank slab path, launch lists and ncu --set full
 # captures of the top kernels.  Outputs under gpurun_out/r02/.
-O=gpurun_out/r02d
+O=gpurun_out/r02e
 mkdir -p $O
 python paper_2409_10743_b200/build.py >/dev/null
 make -s -C oracle all
 (nproc; free -g; nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv) > $O/host.txt 2>&1
 timeout 1500 python -m pytest tests -q -m gpu > $O/gpu_tests.log 2>&1; tail -2 $O/gpu_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
+python scripts/pcie_probe.py > $O/pcie.txt 2>&1
 timeout 1200 python bench.py --steps 10 --warmup 3 > $O/bench_ours.json 2> $O/bench_ours.err; tail -1 $O/bench_ours.json | cut -c1-300
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err; tail -1 $O/bench_ref.json | cut -c1-300
 timeout 600 python bench.py --workload c1 --steps 50 --warmup 10 > $O/cfg_c1.json 2> $O/cfg_c1.err
