@@ -630,7 +630,7 @@ __global__ void __launch_bounds__(128) k_knn16lb(const float4 *__restrict__ node
       ref = (int32_t)e.y;
     }
     have = false;
-    if (size == kk && d > wkey) continue;
+    if (d > wkey) continue;  // wkey stays +inf until the list is full
     if (ref < 0) {  // a leaf: its exact distance decides
       const int32_t leaf = ~ref;
       const float4 lo = ld_node(nodes, 2 * ((int64_t)first_leaf + leaf));
@@ -670,8 +670,7 @@ __global__ void __launch_bounds__(128) k_knn16lb(const float4 *__restrict__ node
       const float td = dn; dn = df; df = td;
       const int32_t tr = rn; rn = rf; rf = tr;
     }
-    const bool full = size == kk;
-    const bool keep_f = !(full && df > wkey), keep_n = !(full && dn > wkey);
+    const bool keep_f = !(df > wkey), keep_n = !(dn > wkey);
     if (keep_n) {
       if (keep_f && top < KNN_STACK) { stk[top] = make_uint2(__float_as_uint(df), (uint32_t)rf); ++top; }
       d = dn;
