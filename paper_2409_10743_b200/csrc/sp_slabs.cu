@@ -648,6 +648,16 @@ __global__ void k_slab_unpack(const int32_t *__restrict__ slot_of_row, const int
   }
 }
 
+// Labels of a rank that ran the single-GPU FoF in place: local smallest index
+// -> global (first + local).
+__global__ void k_slab_offset(int32_t *labels, int64_t n, int32_t first) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) {
+    const int32_t l = labels[i];
+    if (l >= 0) labels[i] = l + first;
+  }
+}
+
 __global__ void k_copy_u64(const unsigned long long *__restrict__ src, unsigned long long *dst, int count) {
   for (int i = threadIdx.x; i < count; i += blockDim.x) dst[i] = src[i];
 }
@@ -770,6 +780,30 @@ void fof_slabs(std::vector<SlabInput> &inputs, SlabExchange &ex, float eps) {
     int64_t p = 0;
     for (int s = 0; s < G; ++s) p += ghost(s, r) + nearc(s, r);
     pmax = std::max(pmax, p);
+  }
+  // An empty exchange (every rank's rows are its own, no point is a ghost
+  // anywhere: one rank, or slabs further than eps apart) leaves each rank a
+  // plain FoF over its own rows: run it in place, labels offset to global
+  // indices.  The matrix is the same on every rank, so all ranks take this
+  // branch together and no collective is left unmatched.
+  bool exchange_empty = true;
+  for (int a = 0; a < G; ++a)
+    for (int b = 0; b < G; ++b)
+      if (a != b && (owned(a, b) || ghost(a, b) || nearc(a, b))) exchange_empty = false;
+  if (exchange_empty) {
+    each([&](int l, SlabRank &r, Ctx &c) {
+      (void)l;
+      if (r.in.n > 0) {
+        dbscan(c, r.in.pts, r.in.n, 3, eps, 2, 1, 64, r.in.labels, r.in.core, nullptr, nullptr);
+        if (r.in.first != 0) {
+          k_slab_offset<<<grid_for(r.in.n, 256, 148 * 8), 256, 0, c.stream>>>(r.in.labels, r.in.n,
+                                                                             (int32_t)r.in.first);
+          SPB_LAUNCHED();
+        }
+      }
+      mark(c, "slab_local");
+    });
+    return;
   }
 
   // C: pack and exchange (xyz, global id)

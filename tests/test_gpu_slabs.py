@@ -91,6 +91,25 @@ def test_slabs_multi_empty_rank_and_host_buffers(sp, G):
     assert torch.equal(lab, want.labels.cpu()) and torch.equal(core, want.core_flags.cpu())
 
 
+@pytest.mark.parametrize("G", [2, 4])
+def test_slabs_multi_empty_exchange(sp, G):
+    # each rank's rows fill their own x band, the bands further than eps
+    # apart: no row moves and no point is a ghost anywhere, so every rank runs
+    # the single-GPU FoF in place (labels offset to global indices)
+    g = torch.Generator().manual_seed(7 + G)
+    n = 1 << 16
+    per = n // G
+    p = torch.rand(n, 3, generator=g)
+    band = torch.arange(n) // per
+    p[:, 0] = (band.float() + 0.4 * p[:, 0]) / G
+    eps = float(np.float32(0.02 / G))
+    p = p.contiguous().cuda()
+    want = sp.friends_of_friends(p, eps)
+    lab, core = _run_multi(sp, p, eps, G)
+    assert torch.equal(lab, want.labels.cpu()) and torch.equal(core, want.core_flags.cpu())
+    assert int((want.labels >= per).sum()) > 0  # labels beyond the first rank's rows occur
+
+
 def test_slabs_multi_h27_against_reference(sp):
     # 8 ranks x 2^24 rows of H(2^27): the labels of the unmodified reference
     g = golden_hashes()["H_2^27"]
