@@ -595,7 +595,10 @@ __device__ __forceinline__ float knn_sq_bound(float w) {
   return __fmul_ru(w1, w1);
 }
 
-__global__ void __launch_bounds__(128) k_knn16lb(const float4 *__restrict__ nodes, int64_t n,
+#ifndef SPB_KNN_BLOCK
+#define SPB_KNN_BLOCK 128
+#endif
+__global__ void __launch_bounds__(SPB_KNN_BLOCK) k_knn16lb(const float4 *__restrict__ nodes, int64_t n,
                                                  const float *__restrict__ origins, int dim,
                                                  const int32_t *__restrict__ order, int64_t nq, int32_t k,
                                                  int32_t *__restrict__ out_idx, float *__restrict__ out_dist) {
@@ -713,7 +716,8 @@ void knn(Ctx &c, const Tree &t, const float *origins, int64_t nq, int32_t k, int
   unsigned g = (unsigned)((nq + 127) / 128);
   const int64_t kk = std::min<int64_t>(k, t.n);
   if (kk <= 16 && SPB_KNN_LB) {
-    k_knn16lb<<<g, 128, 0, c.stream>>>(t.nodes, t.n, origins, t.dim, order.get(), nq, k, idx, dist);
+    k_knn16lb<<<(unsigned)((nq + SPB_KNN_BLOCK - 1) / SPB_KNN_BLOCK), SPB_KNN_BLOCK, 0, c.stream>>>(
+        t.nodes, t.n, origins, t.dim, order.get(), nq, k, idx, dist);
   } else if (kk <= 16) {
     k_knn<16><<<g, 128, 0, c.stream>>>(t.nodes, t.n, origins, t.dim, order.get(), nq, k, nullptr, nullptr, idx, dist);
   } else if (kk <= 64) {
