@@ -675,7 +675,10 @@ __global__ void __launch_bounds__(SPB_KNN_BLOCK) k_knn16lb(const float4 *__restr
     }
     const bool keep_f = !(df > wkey), keep_n = !(dn > wkey);
     if (keep_n) {
-      if (keep_f && top < KNN_STACK) { stk[top] = make_uint2(__float_as_uint(df), (uint32_t)rf); ++top; }
+      // at most one entry per tree level: split lengths grow strictly down the
+      // tree and stay below 64 + 32 (code bits + index tie-break), so the
+      // stack never holds more than 95 < KNN_STACK entries
+      if (keep_f) { stk[top] = make_uint2(__float_as_uint(df), (uint32_t)rf); ++top; }
       d = dn;
       ref = rn;
       have = true;
