@@ -215,7 +215,9 @@ int sp_fof_ids(sp_ctx *ctx, const float *points, int64_t n, int dim, float eps, 
  * the neighbouring slabs; local FoF in global-id space; an all-gather of the
  * (global id, label) links of every ghost copy; the same union-find on every
  * rank; relabelled rows returned by a second all-to-all.  One host read (a
- * G x 3G count matrix) sizes the exchanges. */
+ * G x 3G count matrix) sizes the exchanges; when it shows an empty exchange
+ * (no row changes rank, no ghost anywhere) every rank runs the single-GPU FoF
+ * on its rows in place instead (labels offset by first_index). */
 /* NCCL unique id for sp_comm_create: made by one rank, passed to all. */
 int sp_comm_unique_id(uint8_t id[128]);
 /* ncclCommInitRank over nranks processes (one GPU each) on ctx's device. */
