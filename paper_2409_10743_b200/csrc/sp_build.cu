@@ -305,6 +305,9 @@ void morton_codes(Ctx &c, const float *objects, int64_t n, int dim, bool points,
 #define SPB_RS_MINBLOCKS 3
 #endif
 constexpr int RS_BINS = 256;
+#ifndef SPB_FUSED_HIST
+#define SPB_FUSED_HIST 1  // digit counts accumulated by the key kernels (HistAcc)
+#endif
 constexpr int RS_WH = RS_BINS + 1;  // + one slot for out-of-range items
 
 template <int ITEMS, int THREADS, class K>
@@ -514,7 +517,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS * ITEMS <= 2048) ? 4
 
 template <int ITEMS, int THREADS, class K>
 void onesweep_passes(Ctx &c, K **keys, uint32_t **vals, K **keys_alt, uint32_t **vals_alt, int64_t n,
-                     int npass, bool vals_iota) {
+                     int npass, bool vals_iota, uint32_t *hist_in = nullptr) {
   constexpr int TILE = THREADS * ITEMS;
   constexpr size_t SMEM = rs_smem_bytes<ITEMS, THREADS, K>();
   // the dynamic shared-memory opt-in is per device (and per kernel)
@@ -529,19 +532,28 @@ void onesweep_passes(Ctx &c, K **keys, uint32_t **vals, K **keys_alt, uint32_t *
     }
   }
   const int64_t ntiles = (n + TILE - 1) / TILE;
-  DevBuf<uint32_t> hist((size_t)npass * RS_BINS + npass, c.stream);
+  // hist_in: the digit counts already accumulated by the key kernel (fused
+  // histogram, RS_HIST_ENTRIES(npass) zeroed entries), else counted here
+  DevBuf<uint32_t> own;
+  uint32_t *hist = hist_in;
+  if (!hist) {
+    own = DevBuf<uint32_t>((size_t)npass * RS_BINS + npass, c.stream);
+    hist = own.get();
+    SPB_CUDA(cudaMemsetAsync(hist, 0, own.n * sizeof(uint32_t), c.stream));
+  }
   DevBuf<unsigned long long> lookback((size_t)ntiles * RS_BINS, c.stream);
-  SPB_CUDA(cudaMemsetAsync(hist.get(), 0, hist.n * sizeof(uint32_t), c.stream));
   SPB_CUDA(cudaMemsetAsync(lookback.get(), 0, lookback.n * sizeof(unsigned long long), c.stream));
-  k_rs_hist<K><<<grid_for(n, 256, 148 * 4), 256, 0, c.stream>>>(*keys, n, npass, hist.get());
+  if (!hist_in) {
+    k_rs_hist<K><<<grid_for(n, 256, 148 * 4), 256, 0, c.stream>>>(*keys, n, npass, hist);
+    SPB_LAUNCHED();
+  }
+  k_rs_scan<<<npass, RS_BINS, 0, c.stream>>>(hist);
   SPB_LAUNCHED();
-  k_rs_scan<<<npass, RS_BINS, 0, c.stream>>>(hist.get());
-  SPB_LAUNCHED();
-  uint32_t *ctr = hist.get() + (size_t)npass * RS_BINS;
+  uint32_t *ctr = hist + (size_t)npass * RS_BINS;
   for (int p = 0; p < npass; ++p) {
     k_rs_onesweep<ITEMS, THREADS, K><<<(unsigned)ntiles, THREADS, SMEM, c.stream>>>(
         *keys, (p == 0 && vals_iota) ? nullptr : *vals, *keys_alt, *vals_alt, n, 8 * p,
-        hist.get() + (size_t)p * RS_BINS, lookback.get(), ctr + p, (uint32_t)(2 * p + 1));
+        hist + (size_t)p * RS_BINS, lookback.get(), ctr + p, (uint32_t)(2 * p + 1));
     SPB_LAUNCHED();
     std::swap(*keys, *keys_alt);
     std::swap(*vals, *vals_alt);
@@ -564,7 +576,7 @@ void radix_sort_pairs(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_
 // the sorted values come back (*vals); the keys are consumed.  k32 and k32_alt
 // hold n u32 each.
 void radix_sort_pairs_40(Ctx &c, const uint64_t *keys, uint32_t **vals, uint32_t **vals_alt, uint32_t *k32,
-                         uint32_t *k32_alt, int64_t n, bool vals_iota) {
+                         uint32_t *k32_alt, int64_t n, bool vals_iota, uint32_t *hist_in) {
   if (n <= 1) {
     if (n == 1 && vals_iota) SPB_CUDA(cudaMemsetAsync(*vals, 0, sizeof(uint32_t), c.stream));
     return;
@@ -587,23 +599,30 @@ void radix_sort_pairs_40(Ctx &c, const uint64_t *keys, uint32_t **vals, uint32_t
   }
   constexpr int npass = 5;
   const int64_t ntiles = (n + TILE - 1) / TILE, ntiles32 = (n + TILE32 - 1) / TILE32;
-  DevBuf<uint32_t> hist((size_t)npass * RS_BINS + npass, c.stream);
+  DevBuf<uint32_t> own;
+  uint32_t *hist = hist_in;  // counts from the key kernel (fused histogram), else counted here
+  if (!hist) {
+    own = DevBuf<uint32_t>((size_t)npass * RS_BINS + npass, c.stream);
+    hist = own.get();
+    SPB_CUDA(cudaMemsetAsync(hist, 0, own.n * sizeof(uint32_t), c.stream));
+  }
   DevBuf<unsigned long long> lookback((size_t)std::max(ntiles, ntiles32) * RS_BINS, c.stream);
-  SPB_CUDA(cudaMemsetAsync(hist.get(), 0, hist.n * sizeof(uint32_t), c.stream));
   SPB_CUDA(cudaMemsetAsync(lookback.get(), 0, lookback.n * sizeof(unsigned long long), c.stream));
-  k_rs_hist<uint64_t><<<grid_for(n, 256, 148 * 4), 256, 0, c.stream>>>(keys, n, npass, hist.get());
+  if (!hist_in) {
+    k_rs_hist<uint64_t><<<grid_for(n, 256, 148 * 4), 256, 0, c.stream>>>(keys, n, npass, hist);
+    SPB_LAUNCHED();
+  }
+  k_rs_scan<<<npass, RS_BINS, 0, c.stream>>>(hist);
   SPB_LAUNCHED();
-  k_rs_scan<<<npass, RS_BINS, 0, c.stream>>>(hist.get());
-  SPB_LAUNCHED();
-  uint32_t *ctr = hist.get() + (size_t)npass * RS_BINS;
+  uint32_t *ctr = hist + (size_t)npass * RS_BINS;
   k_rs_onesweep<ITEMS, THREADS, uint64_t, uint32_t><<<(unsigned)ntiles, THREADS, SMEM64, c.stream>>>(
-      keys, vals_iota ? nullptr : *vals, k32, *vals_alt, n, 0, hist.get(), lookback.get(), ctr, 1u, 8);
+      keys, vals_iota ? nullptr : *vals, k32, *vals_alt, n, 0, hist, lookback.get(), ctr, 1u, 8);
   SPB_LAUNCHED();
   std::swap(*vals, *vals_alt);
   uint32_t *ka = k32, *kb = k32_alt;
   for (int p = 1; p < npass; ++p) {
     k_rs_onesweep<ITEMS32, THREADS, uint32_t><<<(unsigned)ntiles32, THREADS, SMEM32, c.stream>>>(
-        ka, *vals, kb, *vals_alt, n, 8 * (p - 1), hist.get() + (size_t)p * RS_BINS, lookback.get(), ctr + p,
+        ka, *vals, kb, *vals_alt, n, 8 * (p - 1), hist + (size_t)p * RS_BINS, lookback.get(), ctr + p,
         (uint32_t)(2 * p + 1));
     SPB_LAUNCHED();
     std::swap(ka, kb);
@@ -612,13 +631,14 @@ void radix_sort_pairs_40(Ctx &c, const uint64_t *keys, uint32_t **vals, uint32_t
 }
 
 void radix_sort_pairs(Ctx &c, uint32_t **keys, uint32_t **vals, uint32_t **keys_alt, uint32_t **vals_alt, int64_t n,
-                      int key_bits, bool vals_iota) {
+                      int key_bits, bool vals_iota, uint32_t *hist_in) {
   if (n <= 1) {
     if (n == 1 && vals_iota) SPB_CUDA(cudaMemsetAsync(*vals, 0, sizeof(uint32_t), c.stream));
     return;
   }
   const int npass = std::max(1, std::min(4, (key_bits + 7) / 8));
-  onesweep_passes<SPB_RS_ITEMS32, SPB_RS_THREADS, uint32_t>(c, keys, vals, keys_alt, vals_alt, n, npass, vals_iota);
+  onesweep_passes<SPB_RS_ITEMS32, SPB_RS_THREADS, uint32_t>(c, keys, vals, keys_alt, vals_alt, n, npass, vals_iota,
+                                                            hist_in);
 }
 
 // ---------------------------------------------------------------------------
@@ -984,7 +1004,11 @@ constexpr int FIX_MAX_RUN = 512;
 constexpr int FIX_ILP = SPB_FIX_ILP;
 
 __global__ void __launch_bounds__(256) k_morton_top32(const float *__restrict__ pts, int64_t n, int width,
-                                                      const float *__restrict__ scene, uint32_t *__restrict__ key32) {
+                                                      const float *__restrict__ scene, uint32_t *__restrict__ key32,
+                                                      uint32_t *ghist = nullptr) {
+  __shared__ uint32_t s_hist[4 * 256];
+  HistAcc<4> H;
+  H.init(s_hist, ghist);
   const int bits = width / 3;
   const uint32_t top = bits >= 32 ? 0xffffffffu : ((1u << bits) - 1u);
   const double scale = (double)(1ull << bits);
@@ -1006,8 +1030,16 @@ __global__ void __launch_bounds__(256) k_morton_top32(const float *__restrict__ 
     k.z = code(x[2], y[2], z[2]);
     k.w = code(x[3], y[3], z[3]);
     reinterpret_cast<uint4 *>(key32)[ch] = k;
+    H.add(k.x);
+    H.add(k.y);
+    H.add(k.z);
+    H.add(k.w);
   }
-  for (int64_t i = chunks * 4 + t0; i < n; i += stride) key32[i] = code(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+  for (int64_t i = chunks * 4 + t0; i < n; i += stride) {
+    key32[i] = code(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+    H.add(key32[i]);
+  }
+  H.flush();
 }
 
 // Query ordering (sort_points): top 32 bits and the full code, both in input
@@ -1245,7 +1277,11 @@ int choose_top_bits(Ctx &c, const float *pts, int64_t n, const float *scene) {
   return !h[0] ? 32 : (!h[1] ? 40 : 0);
 }
 __global__ void __launch_bounds__(256) k_morton_top40(const float *__restrict__ pts, int64_t n,
-                                                      const float *__restrict__ scene, uint64_t *__restrict__ key) {
+                                                      const float *__restrict__ scene, uint64_t *__restrict__ key,
+                                                      uint32_t *ghist = nullptr) {
+  __shared__ uint32_t s_hist[5 * 256];
+  HistAcc<5> H;
+  H.init(s_hist, ghist);
   const int bits = 21;
   const uint32_t top = (1u << bits) - 1u;
   const double scale = (double)(1ull << bits);
@@ -1260,10 +1296,20 @@ __global__ void __launch_bounds__(256) k_morton_top40(const float *__restrict__ 
   for (int64_t ch = t0; ch < chunks; ch += stride) {
     float x[4], y[4], z[4];
     load4pts(pts, ch, x, y, z);
-    reinterpret_cast<ulonglong2 *>(key)[2 * ch] = make_ulonglong2(code(x[0], y[0], z[0]), code(x[1], y[1], z[1]));
-    reinterpret_cast<ulonglong2 *>(key)[2 * ch + 1] = make_ulonglong2(code(x[2], y[2], z[2]), code(x[3], y[3], z[3]));
+    const ulonglong2 a = make_ulonglong2(code(x[0], y[0], z[0]), code(x[1], y[1], z[1]));
+    const ulonglong2 b = make_ulonglong2(code(x[2], y[2], z[2]), code(x[3], y[3], z[3]));
+    reinterpret_cast<ulonglong2 *>(key)[2 * ch] = a;
+    reinterpret_cast<ulonglong2 *>(key)[2 * ch + 1] = b;
+    H.add(a.x);
+    H.add(a.y);
+    H.add(b.x);
+    H.add(b.y);
   }
-  for (int64_t i = chunks * 4 + t0; i < n; i += stride) key[i] = code(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+  for (int64_t i = chunks * 4 + t0; i < n; i += stride) {
+    key[i] = code(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+    H.add(key[i]);
+  }
+  H.flush();
 }
 
 void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, int width, Tree &t) {
@@ -1306,16 +1352,22 @@ void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, i
   if (topbits) {
     if (topbits == 32) {
       uint32_t *k32a = reinterpret_cast<uint32_t *>(k0.get()), *k32b = k32a + n;
-      k_morton_top32<<<grid_for((n + 3) / 4, 256, 148 * 16), 256, 0, c.stream>>>(objects, n, width, t.scene, k32a);
+      DevBuf<uint32_t> hist(SPB_FUSED_HIST ? RS_HIST_ENTRIES(4) : 0, c.stream);
+      if (SPB_FUSED_HIST) SPB_CUDA(cudaMemsetAsync(hist.get(), 0, hist.n * sizeof(uint32_t), c.stream));
+      k_morton_top32<<<grid_for((n + 3) / 4, 256, 148 * 16), 256, 0, c.stream>>>(objects, n, width, t.scene, k32a,
+                                                                                   hist.get());
       SPB_LAUNCHED();
       mark(c, "morton");
-      radix_sort_pairs(c, &k32a, &va, &k32b, &vb, n, 32, /*vals_iota=*/true);
+      radix_sort_pairs(c, &k32a, &va, &k32b, &vb, n, 32, /*vals_iota=*/true, hist.get());
     } else {
-      k_morton_top40<<<grid_for((n + 3) / 4, 256, 148 * 16), 256, 0, c.stream>>>(objects, n, t.scene, k0.get());
+      DevBuf<uint32_t> hist(SPB_FUSED_HIST ? RS_HIST_ENTRIES(5) : 0, c.stream);
+      if (SPB_FUSED_HIST) SPB_CUDA(cudaMemsetAsync(hist.get(), 0, hist.n * sizeof(uint32_t), c.stream));
+      k_morton_top40<<<grid_for((n + 3) / 4, 256, 148 * 16), 256, 0, c.stream>>>(objects, n, t.scene, k0.get(),
+                                                                                   hist.get());
       SPB_LAUNCHED();
       mark(c, "morton");
       uint32_t *k32 = reinterpret_cast<uint32_t *>(k1.get());
-      radix_sort_pairs_40(c, k0.get(), &va, &vb, k32, k32 + n, n, /*vals_iota=*/true);
+      radix_sort_pairs_40(c, k0.get(), &va, &vb, k32, k32 + n, n, /*vals_iota=*/true, hist.get());
     }
     // scratch in the node array (written by the hierarchy afterwards)
     float4 *tpt = reinterpret_cast<float4 *>(t.nodes);

@@ -173,6 +173,35 @@ __host__ __device__ __forceinline__ float float_of_ord(int32_t i) {
 #endif
 }
 
+// Fused radix histogram (radix_sort_pairs' hist_in): the kernel that writes
+// the sort keys also counts their NPASS 8-bit digits in shared memory and adds
+// the block's counts to the global ones once, so the sort skips its own
+// counting pass over the keys.  Every thread of the block must call init and
+// flush (no early return between them).
+template <int NPASS>
+struct HistAcc {
+  uint32_t *sh;  // NPASS * 256 shared counters
+  uint32_t *g;   // global counts (nullptr: no histogram)
+  __device__ __forceinline__ void init(uint32_t *shared, uint32_t *global) {
+    sh = shared;
+    g = global;
+    if (!g) return;
+    for (int i = threadIdx.x; i < NPASS * 256; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+  }
+  __device__ __forceinline__ void add(uint64_t k) {
+    if (!g) return;
+#pragma unroll
+    for (int p = 0; p < NPASS; ++p) atomicAdd(&sh[p * 256 + (uint32_t)((k >> (8 * p)) & 0xffu)], 1u);
+  }
+  __device__ __forceinline__ void flush() {
+    if (!g) return;
+    __syncthreads();
+    for (int i = threadIdx.x; i < NPASS * 256; i += blockDim.x)
+      if (sh[i]) atomicAdd(&g[i], sh[i]);
+  }
+};
+
 __device__ __forceinline__ float4 ld_node(const float4 *nodes, int64_t i) { return __ldg(nodes + i); }
 // Both halves of node j (float4 2j and 2j + 1, one 32-byte sector) in one
 // 256-bit read-only load (LDG.E.ENL2.256 on sm_100a): one L1 request per node

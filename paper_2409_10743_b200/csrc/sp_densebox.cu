@@ -100,7 +100,10 @@ __global__ void k_cell_keys(const float *__restrict__ pts, int64_t n, int dim, c
 // 3-D points, 16-byte aligned: Morton cell keys, four points per step.
 __global__ void __launch_bounds__(256) k_cell_keys_p3v(const float *__restrict__ pts, int64_t n,
                                                        const float *__restrict__ scene, float cell,
-                                                       uint64_t *__restrict__ keys) {
+                                                       uint64_t *__restrict__ keys, uint32_t *ghist = nullptr) {
+  __shared__ uint32_t s_hist[5 * 256];
+  HistAcc<5> H;  // the 40-bit sort's five digits (radix_sort_pairs_40), when ghist is given
+  H.init(s_hist, ghist);
   const float a0 = scene[0], a1 = scene[1], a2 = scene[2];
   const int64_t chunks = n / 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -119,8 +122,16 @@ __global__ void __launch_bounds__(256) k_cell_keys_p3v(const float *__restrict__
     k23.y = key(x[3], y[3], z[3]);
     reinterpret_cast<ulonglong2 *>(keys)[2 * ch] = k01;
     reinterpret_cast<ulonglong2 *>(keys)[2 * ch + 1] = k23;
+    H.add(k01.x);
+    H.add(k01.y);
+    H.add(k23.x);
+    H.add(k23.y);
   }
-  for (int64_t i = chunks * 4 + t0; i < n; i += stride) keys[i] = key(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+  for (int64_t i = chunks * 4 + t0; i < n; i += stride) {
+    keys[i] = key(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+    H.add(keys[i]);
+  }
+  H.flush();
 }
 
 __global__ void k_gather_keys(const float *__restrict__ pts, int64_t n, int dim, const float *__restrict__ scene,
@@ -1232,6 +1243,9 @@ void densebox(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t m
 // false (nothing computed) when the grid does not apply: coordinates that
 // could saturate (no dense cells in the reference either) or cell coordinates
 // too wide for a 63-bit Morton key.
+#ifndef SPB_FUSED_HIST
+#define SPB_FUSED_HIST 1
+#endif
 #ifndef SPB_SORT40
 #define SPB_SORT40 1
 #endif
@@ -1272,9 +1286,14 @@ bool build_cell_grid(Ctx &c, const float *pts, int64_t n, int dim, float eps, Ce
   g.k1 = DevBuf<uint64_t>((size_t)n, c.stream);
   g.v0 = DevBuf<uint32_t>((size_t)n, c.stream);
   g.v1 = DevBuf<uint32_t>((size_t)n, c.stream);
-  if (dim == 3 && aligned16(pts) && aligned16(g.k0.get()))
+  const bool sort40 = SPB_SORT40 && dim == 3 && bits * dim > 32 && bits * dim <= 40 && aligned16(pts);
+  const bool keys_p3v = dim == 3 && aligned16(pts) && aligned16(g.k0.get());
+  // the 40-bit sort's digit counts come from the key kernel (HistAcc)
+  DevBuf<uint32_t> hist(sort40 && keys_p3v && SPB_FUSED_HIST ? RS_HIST_ENTRIES(5) : 0, c.stream);
+  if (hist.n) SPB_CUDA(cudaMemsetAsync(hist.get(), 0, hist.n * sizeof(uint32_t), c.stream));
+  if (keys_p3v)
     k_cell_keys_p3v<<<grid_for((n + 3) / 4, 256, 148 * 16), 256, 0, c.stream>>>(pts, n, scene.get(), cell,
-                                                                                 g.k0.get());
+                                                                                 g.k0.get(), hist.get());
   else
     k_cell_keys<<<G, 256, 0, c.stream>>>(pts, n, dim, scene.get(), cell, -1, g.k0.get());
   SPB_LAUNCHED();
@@ -1282,11 +1301,11 @@ bool build_cell_grid(Ctx &c, const float *pts, int64_t n, int dim, float eps, Ce
   uint64_t *ka = g.k0.get(), *kb = g.k1.get();
   uint32_t *va = g.v0.get(), *vb = g.v1.get();
   g.cpts = DevBuf<float4>((size_t)n, c.stream);
-  if (SPB_SORT40 && dim == 3 && bits * dim > 32 && bits * dim <= 40 && aligned16(pts)) {
+  if (sort40) {
     // five passes, the last four over 32-bit keys; the keys are recomputed
     // from the gathered points
     uint32_t *k32 = reinterpret_cast<uint32_t *>(kb);
-    radix_sort_pairs_40(c, ka, &va, &vb, k32, k32 + n, n, true);
+    radix_sort_pairs_40(c, ka, &va, &vb, k32, k32 + n, n, true, hist.get());
     g.order = va;
     mark(c, "sort");
     k_cell_points3v_keys<<<(unsigned)((n + 256 * CP_ILP - 1) / (256 * CP_ILP)), 256, 0, c.stream>>>(

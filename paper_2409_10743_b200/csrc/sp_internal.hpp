@@ -150,10 +150,14 @@ void morton_codes(Ctx &c, const float *objects, int64_t n, int dim, bool points,
 // the pointers may be swapped.
 void radix_sort_pairs(Ctx &c, uint64_t **keys, uint32_t **vals, uint64_t **keys_alt, uint32_t **vals_alt, int64_t n,
                       int key_bits, bool vals_iota);
+// hist_in: the pass digit counts already accumulated by the kernel that wrote
+// the keys (RS_HIST_ENTRIES(npass) entries, zeroed before that kernel; see
+// hist_acc in sp_common.cuh), or nullptr to count them here.
 void radix_sort_pairs(Ctx &c, uint32_t **keys, uint32_t **vals, uint32_t **keys_alt, uint32_t **vals_alt, int64_t n,
-                      int key_bits, bool vals_iota);
+                      int key_bits, bool vals_iota, uint32_t *hist_in = nullptr);
 void radix_sort_pairs_40(Ctx &c, const uint64_t *keys, uint32_t **vals, uint32_t **vals_alt, uint32_t *k32,
-                         uint32_t *k32_alt, int64_t n, bool vals_iota);
+                         uint32_t *k32_alt, int64_t n, bool vals_iota, uint32_t *hist_in = nullptr);
+constexpr int RS_HIST_ENTRIES(int npass) { return npass * 256 + npass; }
 // Full Bvh::build into `t` (allocates t.nodes/perm/scene). Throws
 // InvalidArgument on non-finite input.
 void build_tree(Ctx &c, const float *objects, int64_t n, int dim, bool points, int width, Tree &t);
