@@ -1046,7 +1046,11 @@ __global__ void __launch_bounds__(256) k_morton_top32(const float *__restrict__ 
 // order; the run fix-up below reads full codes only for members of runs.
 __global__ void __launch_bounds__(256) k_morton_top32_full(const float *__restrict__ pts, int64_t n, int width,
                                                            const float *__restrict__ scene,
-                                                           uint32_t *__restrict__ key32, uint64_t *__restrict__ code) {
+                                                           uint32_t *__restrict__ key32, uint64_t *__restrict__ code,
+                                                           uint32_t *ghist = nullptr) {
+  __shared__ uint32_t s_hist[4 * 256];
+  HistAcc<4> H;
+  H.init(s_hist, ghist);
   const int bits = width / 3;
   const uint32_t top = bits >= 32 ? 0xffffffffu : ((1u << bits) - 1u);
   const double scale = (double)(1ull << bits);
@@ -1070,12 +1074,16 @@ __global__ void __launch_bounds__(256) k_morton_top32_full(const float *__restri
                    (uint32_t)(c[3] >> shift));
     reinterpret_cast<ulonglong2 *>(code)[2 * ch] = make_ulonglong2(c[0], c[1]);
     reinterpret_cast<ulonglong2 *>(code)[2 * ch + 1] = make_ulonglong2(c[2], c[3]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) H.add(c[j] >> shift);
   }
   for (int64_t i = chunks * 4 + t0; i < n; i += stride) {
     const uint64_t c = full(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
     key32[i] = (uint32_t)(c >> shift);
     code[i] = c;
+    H.add(c >> shift);
   }
+  H.flush();
 }
 
 // Runs of equal top bits ordered by (full code, index); singletons keep
@@ -1471,10 +1479,12 @@ void sort_points(Ctx &c, const float *pts, int64_t n, int dim, int32_t *order) {
     // top 32 bits in four passes, runs ordered by the full codes (k1)
     uint32_t *k32a = reinterpret_cast<uint32_t *>(k0.get()), *k32b = k32a + n;
     uint32_t *va = v0.get(), *vb = v1.get();
+    DevBuf<uint32_t> hist(SPB_FUSED_HIST ? RS_HIST_ENTRIES(4) : 0, c.stream);
+    if (hist.n) SPB_CUDA(cudaMemsetAsync(hist.get(), 0, hist.n * sizeof(uint32_t), c.stream));
     k_morton_top32_full<<<grid_for((n + 3) / 4, 256, 148 * 16), 256, 0, c.stream>>>(pts, n, 64, scene.get(), k32a,
-                                                                                   k1.get());
+                                                                                   k1.get(), hist.get());
     SPB_LAUNCHED();
-    radix_sort_pairs(c, &k32a, &va, &k32b, &vb, n, 32, /*vals_iota=*/true);
+    radix_sort_pairs(c, &k32a, &va, &k32b, &vb, n, 32, /*vals_iota=*/true, hist.get());
     DevBuf<int> ovf(1, c.stream);
     SPB_CUDA(cudaMemsetAsync(ovf.get(), 0, sizeof(int), c.stream));
     k_fix_runs_order<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(k32a, n, va, k1.get(), order, ovf.get());
