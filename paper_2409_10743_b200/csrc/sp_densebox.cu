@@ -167,7 +167,10 @@ __global__ void k_heads(const uint64_t *__restrict__ keys, const uint32_t *__res
 // starts): a stream compaction of the segment heads with a decoupled
 // look-back over 4096-key tiles.  Writes cell_start[j] = first position of
 // cell j, cell_of[i] = cell of sorted position i, and the number of cells.
-constexpr int CC_THREADS = 256, CC_ITEMS = 16, CC_TILE = CC_THREADS * CC_ITEMS;
+#ifndef SPB_CC_ITEMS
+#define SPB_CC_ITEMS 24  // 8 / 16 / 24 / 32: grid + hierarchy phase 7.74 / 7.64 / 7.42 / 8.05 ms at 2^27
+#endif
+constexpr int CC_THREADS = 256, CC_ITEMS = SPB_CC_ITEMS, CC_TILE = CC_THREADS * CC_ITEMS;
 __global__ void __launch_bounds__(CC_THREADS) k_cell_compact(const uint64_t *__restrict__ keys, int64_t n,
                                                               int64_t *__restrict__ cell_start,
                                                               int32_t *__restrict__ cell_of,
