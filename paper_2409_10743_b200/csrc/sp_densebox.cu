@@ -366,7 +366,10 @@ __global__ void k_cell_points(const uint32_t *__restrict__ order, const float *_
 // 3-D, 16-byte aligned points: four sorted positions per thread with their
 // random gathers in flight together, each point by one or two 16-byte loads
 // (gather_pt3).
-constexpr int CP_ILP = 4;
+#ifndef SPB_CP_ILP
+#define SPB_CP_ILP 2  // 2 / 4 / 8: grid + hierarchy phase 7.23 / 7.42 / 7.66 ms at 2^27
+#endif
+constexpr int CP_ILP = SPB_CP_ILP;
 __global__ void __launch_bounds__(256) k_cell_points3v(const uint32_t *__restrict__ order,
                                                        const float *__restrict__ pts, int64_t n,
                                                        float4 *__restrict__ cpts) {
