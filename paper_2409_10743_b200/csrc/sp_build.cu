@@ -1169,7 +1169,10 @@ __global__ void __launch_bounds__(256) k_fix_gather(const float *__restrict__ pt
 // memory, so it writes the split lengths D(c0 .. c0 + FIX_CH - 1) of the
 // hierarchy itself (k_delta's pass over the sorted codes and indices, and
 // writing those, are gone); the sorted points go to spts.
-constexpr int FIX_CH = 2048;
+#ifndef SPB_FIX_CH
+#define SPB_FIX_CH 1024  // 1024 / 2048 / 4096: field build 16.10 / 16.17 / 16.69 ms
+#endif
+constexpr int FIX_CH = SPB_FIX_CH;
 constexpr int FIX_WIN = FIX_CH + 2 * FIX_MAX_RUN;
 constexpr size_t FIX_SMEM = (size_t)(FIX_WIN + FIX_CH + 1) * (sizeof(uint64_t) + sizeof(uint32_t));
 template <int SHIFT>  // runs: equal code >> SHIFT (31: top 32 of 63 bits, 23: top 40)
