@@ -25,7 +25,7 @@ cap k_fof_cells_merge merge_cells_2p27 "scripts/prof_fof.py $N 2"
 cap k_rs_onesweep sort_cells_2p27 "scripts/prof_fof.py $N 2" 7
 cap "k_hierarchy" hier_cells_2p27 "scripts/prof_fof.py $N 2"
 cap "k_hierarchy" hier_2p27 "scripts/prof_build.py $N 2"
-cap "k_rs_onesweep" sort_2p27 "scripts/prof_build.py $N 2" 2
+cap "k_rs_onesweep<16, 256, unsigned int, unsigned int>" sort_2p27 "scripts/prof_build.py $N 2" 2
 cap k_knn c4_knn_2p24 "scripts/c4_probe.py $((1<<24)) 2"
 cap k_range_count c2_range_2p24 "scripts/c2_probe.py $((1<<24)) 2"
 ls -la $O | tail -40
