@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(256) k_delta(const uint64_t *__restrict__ sk, 
 }
 
 #ifndef SPB_CLIMB_BLK
-#define SPB_CLIMB_BLK 256
+#define SPB_CLIMB_BLK 128  // 128 / 256 / 512: field build 15.83 / 16.13 / slower (hierarchy 6.23 vs 6.52 ms)
 #endif
 constexpr int CLIMB_BLK = SPB_CLIMB_BLK;
 // Split lengths in 32-bit index arithmetic (n < 2^31: Karras indices are

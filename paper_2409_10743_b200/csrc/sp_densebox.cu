@@ -928,7 +928,10 @@ __global__ void __launch_bounds__(128, 1) k_fof_cells_merge(const float4 *__rest
 
 // The same walks on the SM-affine schedule (sm_slices, sp_common.cuh).
 template <bool FAST>
-__global__ void __launch_bounds__(128, 1) k_fof_cells_merge_sm(const float4 *__restrict__ nodes, int64_t m,
+#ifndef SPB_MERGE_THREADS
+#define SPB_MERGE_THREADS 128
+#endif
+__global__ void __launch_bounds__(SPB_MERGE_THREADS, 1) k_fof_cells_merge_sm(const float4 *__restrict__ nodes, int64_t m,
                                                             const int64_t *__restrict__ cell_start, int64_t n,
                                                             const float4 *__restrict__ cpts, Radius R,
                                                             int32_t *parent, unsigned long long *slices,
@@ -1399,10 +1402,10 @@ bool fof_cells(Ctx &c, const float *pts, int64_t n, int dim, float eps, int32_t 
     } else if (SPB_MERGE_SM && m >= SPB_SM_MIN_ITEMS) {
       SmSlices sl(c);
       if (R.fast)
-        k_fof_cells_merge_sm<true><<<sl.grid(k_fof_cells_merge_sm<true>, 128), 128, 0, c.stream>>>(
+        k_fof_cells_merge_sm<true><<<sl.grid(k_fof_cells_merge_sm<true>, SPB_MERGE_THREADS), SPB_MERGE_THREADS, 0, c.stream>>>(
             g.t.nodes, m, g.cell_start.get(), n, g.cpts.get(), R, parent.get(), sl.ctr.get(), sl.nsm);
       else
-        k_fof_cells_merge_sm<false><<<sl.grid(k_fof_cells_merge_sm<false>, 128), 128, 0, c.stream>>>(
+        k_fof_cells_merge_sm<false><<<sl.grid(k_fof_cells_merge_sm<false>, SPB_MERGE_THREADS), SPB_MERGE_THREADS, 0, c.stream>>>(
             g.t.nodes, m, g.cell_start.get(), n, g.cpts.get(), R, parent.get(), sl.ctr.get(), sl.nsm);
     } else if (R.fast)
       k_fof_cells_merge<true><<<(unsigned)((m + 127) / 128), 128, 0, c.stream>>>(g.t.nodes, m, g.cell_start.get(), n,
