@@ -364,6 +364,9 @@ __global__ void __launch_bounds__(THREADS, (THREADS * ITEMS <= 2048) ? 4
     unsigned long long *lookback, uint32_t *tile_ctr, uint32_t tag, int oshift = 0) {
   constexpr int TILE = THREADS * ITEMS;
   constexpr int WARPS = THREADS / 32;
+  // one thread per digit bin in the per-tile scans and the look-back (128
+  // threads fault: measured)
+  static_assert(THREADS >= RS_BINS, "onesweep needs at least one thread per digit bin");
   extern __shared__ __align__(16) unsigned char rs_smem[];
   K *skeys = reinterpret_cast<K *>(rs_smem);
   uint32_t *svals = reinterpret_cast<uint32_t *>(skeys + TILE);
